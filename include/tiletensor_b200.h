@@ -1,0 +1,210 @@
+/*
+ * tiletensor_b200.h -- C-ABI of the B200-native tile-tensor hot path.
+ *
+ * The reference (arXiv 2011.01805, /root/reference/proj) is a header-only
+ * C++20 library in namespace `tiletensor`; it has no FFI of its own.  This
+ * header is the thin `extern "C"` layer that the C++ host mirror
+ * (paper_2011_01805_b200/include/tiletensor_b200/*.hpp, same signatures as
+ * the reference's inc/*.hpp) and the Python binding call.  Every entry point
+ * below names the reference symbol it replaces (path:line relative to
+ * /root/reference/proj/include/tiletensor/).
+ *
+ * Conventions
+ *  - A tile tensor lives on the device as ONE contiguous fp64 array
+ *    [tile_count][slot_count], row-major over the external grid: exactly the
+ *    concatenation of the reference's `TileTensor::tiles()[flat].slots()`.
+ *  - Dense tensors are row-major fp64 device arrays over the shape's n_i.
+ *  - All pointers passed to op entry points are DEVICE pointers unless the
+ *    name says `host`.  Ops are asynchronous on the session's stream.
+ *  - No entry point throws.  Each returns a tt_status; on failure
+ *    tt_last_error() (thread-local) holds the message the reference's
+ *    exception would carry, and the C++ mirror rethrows the exact type.
+ *  - Shape checks, depth (chain) checks and the cost counters are evaluated
+ *    on the host before any launch, so a failing call launches nothing and
+ *    changes no counter (the reference throws before its first primitive
+ *    for every shape/depth error it can raise on these paths).
+ */
+#ifndef TILETENSOR_B200_H
+#define TILETENSOR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TT_MAX_RANK 8
+
+/* Status codes; map 1:1 onto the reference's exception types. */
+typedef enum tt_status {
+  TT_OK = 0,
+  TT_ERR_SHAPE = 1,            /* tiletensor::ShapeError            shape.hpp:21   */
+  TT_ERR_SHAPE_PARSE = 2,      /* tiletensor::ShapeParseError       shape.hpp:26   */
+  TT_ERR_DEPTH = 3,            /* tiletensor::DepthExhaustedError   backend.hpp:18 */
+  TT_ERR_INVALID_ARGUMENT = 4, /* std::invalid_argument                            */
+  TT_ERR_OUT_OF_RANGE = 5,     /* std::out_of_range                                */
+  TT_ERR_LOGIC = 6,            /* std::logic_error                                 */
+  TT_ERR_CUDA = 7,             /* CUDA runtime failure (no reference equivalent)   */
+  TT_ERR_NO_DEVICE = 8         /* no CUDA device: the product never falls back     */
+} tt_status;
+
+typedef enum tt_op { TT_OP_ADD = 0, TT_OP_MUL = 1 } tt_op;          /* OpKind shape.hpp:284 */
+
+typedef enum tt_variant {                                             /* SumVariant rotate_sum.hpp:20 */
+  TT_VARIANT_AUTO = -1, /* std::nullopt -> auto_variant(n)  rotate_sum.hpp:99 */
+  TT_VARIANT_LEFT_TO_RIGHT = 0,
+  TT_VARIANT_RIGHT_TO_LEFT = 1,
+  TT_VARIANT_POWER_OF_TWO = 2
+} tt_variant;
+
+/* DimSpec (shape.hpp:37).  `interleaved` is the north star's `~` tiling,
+ * which the reference does not implement: element j of
+ * an interleaved dim sits in external tile l = j mod e at in-tile coordinate
+ * m = j div e, instead of l = j div t, m = j mod t. */
+typedef struct tt_dim {
+  int64_t n;
+  int64_t d;
+  int64_t t;
+  int32_t unknown;
+  int32_t interleaved;
+} tt_dim;
+
+/* TileTensorShape (shape.hpp:72). */
+typedef struct tt_shape {
+  int32_t rank;
+  int32_t relaxed;
+  tt_dim dims[TT_MAX_RANK];
+} tt_shape;
+
+/* CostReport (backend.hpp:28). */
+typedef struct tt_cost {
+  uint64_t additions;
+  uint64_t multiplications;
+  uint64_t mask_multiplications;
+  uint64_t rotations;
+  uint64_t bootstraps;
+  uint64_t power_of_two_rotations;
+} tt_cost;
+
+typedef struct tt_session tt_session; /* Session backend.hpp:83 */
+
+/* ---- errors ------------------------------------------------------------ */
+const char* tt_last_error(void);
+int64_t tt_last_error_position(void); /* ShapeParseError::position() shape.hpp:31 */
+const char* tt_version(void);
+
+/* ---- shape algebra (host only; no device needed) ----------------------- */
+int tt_shape_parse(const char* text, tt_shape* out);                  /* parse_shape        shape.hpp:250 */
+int tt_shape_format(const tt_shape* s, char* buf, int64_t cap);       /* format_shape       shape.hpp:256 */
+int tt_shape_check(const tt_shape* s);                                /* TileTensorShape()  shape.hpp:74  */
+int tt_shape_external(const tt_shape* s, int64_t* ext_out);           /* external_extents   shape.hpp:99  */
+int64_t tt_shape_tile_count(const tt_shape* s);                       /* tile_count         shape.hpp:106 */
+int64_t tt_shape_tile_slots(const tt_shape* s);                       /* tile_slots         shape.hpp:86  */
+int64_t tt_shape_used_slots(const tt_shape* s);                       /* used_slots         shape.hpp:112 */
+int tt_shape_elementwise_result(const tt_shape* a, const tt_shape* b, int op,
+                                tt_shape* out);                       /* elementwise_result_shape shape.hpp:293 */
+int tt_shape_sum_result(const tt_shape* s, int dim, tt_shape* out);   /* sum_result_shape   shape.hpp:357 */
+/* logical_indices / slot_of (tile_tensor.hpp:96,114) */
+int tt_logical_indices(const tt_shape* s, const int64_t* tile_index, int64_t h, int64_t* j_out);
+int tt_slot_of(const tt_shape* s, const int64_t* j, int64_t* tile_index_out, int64_t* h_out);
+/* closed-form rotation counts rotate_sum.hpp:33-39 */
+int64_t tt_rotations_left_to_right(int64_t n);
+int64_t tt_rotations_right_to_left(int64_t n);
+
+/* ---- session ----------------------------------------------------------- */
+int tt_device_count(int* out);
+/* Session(slots, depth) backend.hpp:85-91; binds `device` and creates a stream. */
+int tt_session_create(int64_t slot_count, int64_t max_chain_index, int device, tt_session** out);
+void tt_session_destroy(tt_session* s);
+int64_t tt_session_slot_count(const tt_session* s);
+int64_t tt_session_max_chain_index(const tt_session* s);
+int tt_session_device(const tt_session* s);
+/* Run subsequent ops on an external stream (e.g. torch's current stream; NULL
+ * is the legacy default stream).  tt_session_use_own_stream restores the
+ * session's private stream. */
+int tt_session_set_stream(tt_session* s, void* cuda_stream);
+int tt_session_use_own_stream(tt_session* s);
+void* tt_session_stream(const tt_session* s);
+int tt_session_synchronize(tt_session* s);
+void tt_session_cost(const tt_session* s, tt_cost* out);              /* cost_report    backend.hpp:171 */
+void tt_session_reset_counters(tt_session* s);                        /* reset_counters backend.hpp:182 */
+/* Number of kernels this session has launched (evidence counter for bench/tests). */
+uint64_t tt_session_launches(const tt_session* s);
+/* Counts `count` bootstraps (backend.hpp:165); values are unchanged so no launch. */
+void tt_session_count_bootstraps(tt_session* s, int64_t count);
+
+/* ---- device memory helpers -------------------------------------------- */
+int tt_device_alloc(tt_session* s, int64_t bytes, void** out);
+int tt_device_free(tt_session* s, void* p);
+int tt_copy_h2d(tt_session* s, void* dst, const void* host_src, int64_t bytes);
+int tt_copy_d2h(tt_session* s, void* host_dst, const void* src, int64_t bytes);
+int tt_copy_d2d(tt_session* s, void* dst, const void* src, int64_t bytes);
+/* Seeded synthetic input (bench/tests), bit-identical to the CPU generator
+ * or_fill_uniform in oracle/tt_oracle.c: u = splitmix64(splitmix64(seed) ^ (offset+i)),
+ * x = lo + (hi-lo) * (u>>11) * 2^-53. */
+int tt_fill_uniform(tt_session* s, double* out, int64_t count, uint64_t seed, int64_t offset,
+                    double lo, double hi);
+
+/* ---- tile-tensor operators (device pointers) -------------------------- */
+/* pack tile_tensor.hpp:167-220.  `dense` holds prod(n_i) values row-major;
+ * `tiles` receives tile_count*slot_count values. */
+int tt_pack(tt_session* s, const double* dense, const tt_shape* shape, double* tiles);
+/* unpack tile_tensor.hpp:222-242 (replica 0 of every element). */
+int tt_unpack(tt_session* s, const tt_shape* shape, const double* tiles, double* dense);
+/* tt_elementwise / tt_add / tt_mul tile_tensor.hpp:244-279 with external
+ * broadcast.  chain_* are the operands' chain indices (TileTensor::chain_index
+ * tile_tensor.hpp:145); *out_chain receives the result's. */
+int tt_elementwise(tt_session* s, int op, const tt_shape* a, const double* ta, int64_t chain_a,
+                   const tt_shape* b, const double* tb, int64_t chain_b, tt_shape* out_shape,
+                   double* out, int64_t* out_chain);
+/* tt_sum tile_tensor.hpp:286-347 (external left fold + in-tile rotate-and-sum). */
+int tt_sum(tt_session* s, const tt_shape* in_shape, const double* tin, int dim, int variant,
+           tt_shape* out_shape, double* out);
+/* tt_sum(tt_mul(a,b), dim, variant) fused: the product is never materialised.
+ * The body of matvec_a/b and matmul_a/b linalg.hpp:41-73. Counters and
+ * results equal the two-call composition exactly. */
+int tt_mul_sum(tt_session* s, const tt_shape* a, const double* ta, int64_t chain_a,
+               const tt_shape* b, const double* tb, int64_t chain_b, int dim, int variant,
+               tt_shape* out_shape, double* out, int64_t* out_chain);
+/* matvec_a/matvec_b/matmul_a/matmul_b linalg.hpp:41-73 (adds the rank and
+ * replication preconditions of linalg.hpp:32-37 to tt_mul_sum).
+ * which: 0=matvec_a 1=matvec_b 2=matmul_a 3=matmul_b. */
+int tt_linalg_product(tt_session* s, int which, const tt_shape* a, const double* ta,
+                      int64_t chain_a, const tt_shape* b, const double* tb, int64_t chain_b,
+                      int variant, tt_shape* out_shape, double* out, int64_t* out_chain);
+/* clean_unknowns tile_tensor.hpp:352-386.  Returns the input unchanged (a
+ * device copy when out != in) at zero cost when the shape has no '?'. */
+int tt_clean_unknowns(tt_session* s, const tt_shape* in_shape, const double* tin, int64_t chain,
+                      tt_shape* out_shape, double* out, int64_t* out_chain);
+/* replicate_dim tile_tensor.hpp:391-420. */
+int tt_replicate_dim(tt_session* s, const tt_shape* in_shape, const double* tin, int dim,
+                     tt_shape* out_shape, double* out);
+
+/* ---- tile-level primitives (Session / rotate_sum.hpp), batched over n_tiles ---- */
+int tt_tiles_binary(tt_session* s, int op, const double* a, const double* b, double* out,
+                    int64_t n_tiles, const int64_t* chain_a, const int64_t* chain_b,
+                    int64_t* chain_out);                              /* Session::add/mul backend.hpp:117-136 */
+int tt_tiles_mask_mul(tt_session* s, const double* a, const double* mask, double* out,
+                      int64_t n_tiles, const int64_t* chain_a, int64_t* chain_out); /* backend.hpp:138 */
+int tt_tiles_rotate(tt_session* s, const double* in, int64_t offset, double* out,
+                    int64_t n_tiles);                                 /* Session::rotate backend.hpp:152 */
+int tt_sum_tile_strided(tt_session* s, const double* in, int64_t n, int64_t stride, int variant,
+                        double* out, int64_t n_tiles);                /* rotate_sum.hpp:44-90 */
+int tt_sum_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents, int rank,
+                    int dim, int variant, double* out, int64_t n_tiles); /* rotate_sum.hpp:109-120 */
+int tt_replicate_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents, int rank,
+                          int dim, double* out, int64_t n_tiles);     /* rotate_sum.hpp:128-152 */
+
+/* ---- sharding (north star item 5) -------------------------------------- */
+/* Block-partition external dim `shard_dim` (1-based) of `shape` over
+ * `world` ranks; rank r owns external indices [*begin, *end).  Returns the
+ * rank's local shape (same dims, n restricted to the slab). */
+int tt_shard_plan(const tt_shape* shape, int shard_dim, int world, int rank, int64_t* begin,
+                  int64_t* end, tt_shape* local_shape);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TILETENSOR_B200_H */

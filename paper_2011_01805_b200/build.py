@@ -1,0 +1,98 @@
+"""In-tree build of the native libraries.
+
+* ``paper_2011_01805_b200/_lib/libtiletensor_b200.so`` -- the product: C-ABI +
+  sm_100a kernels (nvcc, ``-gencode arch=compute_100a,code=sm_100a``).
+* ``paper_2011_01805_b200/_lib/tt_host_tests`` -- C++ tests of the host mirror
+  headers (run by ``tests/test_cpp_host.py`` on a GPU).
+* ``oracle/_build/libttoracle.so`` -- the CPU restatement (test checker only).
+* ``oracle/_ref/libttref.so`` -- the reference itself, only when
+  ``/root/reference`` is present (this container; never on the GPU box).
+
+Sources are compiled only when newer than their outputs.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB_DIR = PKG / "_lib"
+OBJ_DIR = LIB_DIR / "obj"
+LIB = LIB_DIR / "libtiletensor_b200.so"
+HOST_TESTS = LIB_DIR / "tt_host_tests"
+ORACLE_DIR = ROOT / "oracle"
+ORACLE_LIB = ORACLE_DIR / "_build" / "libttoracle.so"
+REF_LIB = ORACLE_DIR / "_ref" / "libttref.so"
+REF_INC = Path(os.environ.get("TT_REFERENCE_INCLUDE", "/root/reference/proj/include"))
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
+           "-ffp-contract=off", "--fmad=false", "-I", str(ROOT / "include"), "-I", str(CSRC)]
+SOURCES = ["tt_shape.cpp", "tt_schedule.cpp", "tt_capi.cpp", "tt_kernels.cu"]
+HEADERS = [CSRC / "tt_internal.hpp", CSRC / "tt_launch.hpp", ROOT / "include" / "tiletensor_b200.h"]
+
+
+def _run(cmd: list[str], cwd: Path | None = None) -> None:
+    proc = subprocess.run(cmd, cwd=cwd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        sys.stderr.write(proc.stdout + proc.stderr)
+        raise RuntimeError(f"build step failed: {' '.join(cmd)}")
+
+
+def _stale(out: Path, deps: list[Path]) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(d.exists() and d.stat().st_mtime > t for d in deps)
+
+
+def build_product(verbose: bool = False) -> Path:
+    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        s = CSRC / src
+        o = OBJ_DIR / (src + ".o")
+        objs.append(o)
+        if _stale(o, [s, *HEADERS]):
+            if verbose:
+                print(f"[build] nvcc {src}")
+            _run([NVCC, *ARCH, *NVFLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", str(s),
+                  "-o", str(o)])
+    if _stale(LIB, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"])
+    return LIB
+
+
+def build_host_tests(verbose: bool = False) -> Path:
+    src = PKG / "tests_cpp" / "host_tests.cpp"
+    hdrs = sorted((PKG / "include" / "tiletensor_b200").glob("*.hpp"))
+    if src.exists() and _stale(HOST_TESTS, [src, LIB, *hdrs]):
+        if verbose:
+            print("[build] g++ host_tests.cpp")
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", str(ROOT / "include"),
+              "-I", str(PKG / "include"), str(src), "-o", str(HOST_TESTS), "-L", str(LIB_DIR),
+              "-ltiletensor_b200", f"-Wl,-rpath,{LIB_DIR}", "-pthread"])
+    return HOST_TESTS
+
+
+def build_oracle(verbose: bool = False) -> None:
+    targets = ["oracle"]
+    if (REF_INC / "tiletensor").is_dir():
+        targets.append("ref")
+    _run(["make", "-s", "-C", str(ORACLE_DIR), *targets, f"REF_INC={REF_INC}"])
+
+
+def build_all(verbose: bool = False) -> None:
+    build_product(verbose)
+    build_oracle(verbose)
+    build_host_tests(verbose)
+
+
+if __name__ == "__main__":
+    build_all(verbose="-v" in sys.argv)
+    print(f"built {LIB}")

@@ -1,0 +1,808 @@
+// tt_capi.cpp -- the extern "C" boundary (include/tiletensor_b200.h).
+//
+// Each entry point: (1) validates shapes / chains on the host exactly as the
+// reference operator would (raising the same error kinds and messages),
+// (2) adds the reference's primitive counts to the session counters,
+// (3) launches the sm_100a kernels on the session stream.  Nothing here
+// computes slot values on the CPU: a session cannot be created without a
+// CUDA device (TT_ERR_NO_DEVICE), so there is no host fallback path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "tt_internal.hpp"
+#include "tt_launch.hpp"
+
+struct tt_session {
+  int64_t slots = 1;
+  int64_t depth = 1;
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::atomic<uint64_t> adds{0}, muls{0}, masks{0}, rots{0}, boots{0}, pow2{0};
+  uint64_t launches = 0;
+  std::mutex mu;  // serialises launches + scratch (counters are atomic)
+  double* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int sm_count = 148;
+  size_t smem_optin = 227 * 1024;
+};
+
+namespace {
+
+using namespace ttb;
+
+thread_local std::string g_error;
+thread_local int64_t g_error_pos = -1;
+
+int set_error(int code, const std::string& msg, int64_t pos = -1) {
+  g_error = msg;
+  g_error_pos = pos;
+  return code;
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    g_error.clear();
+    g_error_pos = -1;
+    return TT_OK;
+  } catch (const Error& e) {
+    return set_error(e.code, e.what(), e.position);
+  } catch (const std::bad_alloc&) {
+    return set_error(TT_ERR_CUDA, "out of memory");
+  } catch (const std::exception& e) {
+    return set_error(TT_ERR_LOGIC, e.what());
+  }
+}
+
+double* scratch_fn(void* owner, size_t bytes) {
+  auto* s = static_cast<tt_session*>(owner);
+  if (bytes > s->scratch_bytes) {
+    if (s->scratch) {
+      check_cuda(cudaStreamSynchronize(s->stream), "scratch sync");
+      check_cuda(cudaFree(s->scratch), "scratch free");
+      s->scratch = nullptr;
+    }
+    check_cuda(cudaMalloc(&s->scratch, bytes), "scratch alloc");
+    s->scratch_bytes = bytes;
+  }
+  return s->scratch;
+}
+
+LaunchCtx ctx_of(tt_session* s) {
+  check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+  LaunchCtx c;
+  c.stream = s->stream;
+  c.device = s->device;
+  c.sm_count = s->sm_count;
+  c.smem_optin = s->smem_optin;
+  c.launches = &s->launches;
+  c.scratch = scratch_fn;
+  c.scratch_owner = s;
+  return c;
+}
+
+void need_session(const tt_session* s) {
+  if (s == nullptr) invalid_argument("null session");
+}
+
+void add_cost(tt_session* s, const tt_cost& c, uint64_t times) {
+  s->adds += c.additions * times;
+  s->muls += c.multiplications * times;
+  s->masks += c.mask_multiplications * times;
+  s->rots += c.rotations * times;
+  s->boots += c.bootstraps * times;
+  s->pow2 += c.power_of_two_rotations * times;
+}
+
+void check_tiles_addressable(const Shape& sh) {
+  if (sh.tile_count() >= (int64_t{1} << 31))
+    invalid_argument("tile count exceeds 2^31 - 1 per tensor (shard the tensor)");
+}
+
+void copy_tiles(const LaunchCtx& c, double* out, const double* in, int64_t count) {
+  if (out == in || count == 0) return;
+  check_cuda(cudaMemcpyAsync(out, in, static_cast<size_t>(count) * sizeof(double),
+                             cudaMemcpyDeviceToDevice, c.stream),
+             "device copy");
+}
+
+// Operand tile-index strides of a broadcast operand over the out grid.
+void operand_strides(const Shape& op, std::vector<int64_t>& st) {
+  const auto e = op.external();
+  const auto rs = row_major_strides(e);
+  st.resize(e.size());
+  for (size_t i = 0; i < e.size(); ++i) st[i] = e[i] == 1 ? 0 : rs[i];
+}
+
+// Group grid of a reduction over dim `di` of a product grid with external
+// extents `ext`.  Dims along which an operand broadcasts are iterated
+// innermost so that consecutive groups share that operand's tiles in L2.
+GroupSpec make_group_spec(const std::vector<int64_t>& ext, int di,
+                          const std::vector<int64_t>& a_st, const std::vector<int64_t>& b_st,
+                          bool has_b) {
+  GroupSpec g;
+  std::vector<int64_t> gext = ext;
+  gext[di] = 1;
+  const auto out_st = row_major_strides(gext);
+  std::vector<int> order;
+  for (int i = 0; i < static_cast<int>(ext.size()); ++i)
+    if (i != di && ext[i] > 1) order.push_back(i);
+  auto broadcast = [&](int i) { return a_st[i] == 0 || (has_b && b_st[i] == 0); };
+  std::stable_partition(order.begin(), order.end(), [&](int i) { return !broadcast(i); });
+  g.nd = static_cast<int>(order.size());
+  g.groups = 1;
+  for (int k = 0; k < g.nd; ++k) {
+    const int i = order[k];
+    g.ext[k] = ext[i];
+    g.out_stride[k] = out_st[i];
+    g.a_stride[k] = a_st[i];
+    g.b_stride[k] = has_b ? b_st[i] : 0;
+    g.groups *= ext[i];
+  }
+  g.astep = a_st[di];
+  g.bstep = has_b ? b_st[di] : 0;
+  return g;
+}
+
+// Shared body of tt_sum / tt_mul_sum for a non-degenerate summed dim.
+void run_reduction(tt_session* s, const Shape& prod, int di, int variant, const double* ta,
+                   const std::vector<int64_t>& a_st, const double* tb,
+                   const std::vector<int64_t>& b_st, double* out) {
+  const Dim& ds = prod.dims[di];
+  if (ds.interleaved && ds.unknown && ds.used() < prod.ext(di) * ds.t)
+    shape_error("sum over an unknown interleaved dimension requires clean_unknowns first");
+  const auto ext = prod.external();
+  const int64_t stride = tile_strides(prod)[di];
+  const Program prog =
+      build_sum_program(ext[di], ds.t, stride, s->slots, ds.used(), ds.unknown, variant);
+  const GroupSpec g = make_group_spec(ext, di, a_st, b_st, tb != nullptr);
+  add_cost(s, prog.per_group, static_cast<uint64_t>(g.groups));
+  launch_group_program(ctx_of(s), prog, g, s->slots, ta, tb, out);
+}
+
+void require_slots(const tt_session* s, const Shape& sh, const char* who) {
+  if (!sh.relaxed && sh.tile_slots() != s->slots)
+    shape_error(std::string(who) + ": shape " + format_shape(sh) + " needs " +
+                std::to_string(sh.tile_slots()) + " slots per tile, backend has " +
+                std::to_string(s->slots));
+  if (sh.relaxed && sh.tile_slots() > s->slots)
+    shape_error(std::string(who) + ": relaxed shape exceeds the backend slot count");
+}
+
+int64_t mul_chain(int64_t ca, int64_t cb) {
+  const int64_t c = std::min(ca, cb);
+  if (c < 1) depth_error("multiplication at chain index 0 (bootstrap required)");
+  return c - 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tt_last_error(void) { return g_error.c_str(); }
+int64_t tt_last_error_position(void) { return g_error_pos; }
+const char* tt_version(void) { return "tiletensor_b200 0.1 (sm_100a)"; }
+
+// ---- shape algebra ------------------------------------------------------------
+
+int tt_shape_parse(const char* text, tt_shape* out) {
+  return guarded([&] {
+    if (!text || !out) invalid_argument("null argument");
+    to_c(parse_shape(text), out);
+  });
+}
+
+int tt_shape_format(const tt_shape* s, char* buf, int64_t cap) {
+  return guarded([&] {
+    const std::string f = format_shape(from_c(s));
+    if (cap < static_cast<int64_t>(f.size()) + 1) invalid_argument("format buffer too small");
+    std::memcpy(buf, f.c_str(), f.size() + 1);
+  });
+}
+
+int tt_shape_check(const tt_shape* s) {
+  return guarded([&] { (void)from_c(s); });
+}
+
+int tt_shape_external(const tt_shape* s, int64_t* ext_out) {
+  return guarded([&] {
+    const Shape sh = from_c(s);
+    for (int i = 0; i < sh.rank(); ++i) ext_out[i] = sh.ext(i);
+  });
+}
+
+int64_t tt_shape_tile_count(const tt_shape* s) {
+  try {
+    return from_c(s).tile_count();
+  } catch (...) {
+    return -1;
+  }
+}
+int64_t tt_shape_tile_slots(const tt_shape* s) {
+  try {
+    return from_c(s).tile_slots();
+  } catch (...) {
+    return -1;
+  }
+}
+int64_t tt_shape_used_slots(const tt_shape* s) {
+  try {
+    return from_c(s).used_slots();
+  } catch (...) {
+    return -1;
+  }
+}
+
+int tt_shape_elementwise_result(const tt_shape* a, const tt_shape* b, int op, tt_shape* out) {
+  return guarded([&] { to_c(elementwise_result_shape(from_c(a), from_c(b), op), out); });
+}
+
+int tt_shape_sum_result(const tt_shape* s, int dim, tt_shape* out) {
+  return guarded([&] { to_c(sum_result_shape(from_c(s), dim), out); });
+}
+
+// logical_indices tile_tensor.hpp:96-111
+int tt_logical_indices(const tt_shape* s, const int64_t* tile_index, int64_t h, int64_t* j_out) {
+  return guarded([&] {
+    const Shape sh = from_c(s);
+    if (h < 0 || h >= sh.tile_slots()) shape_error("slot index out of range");
+    const auto st = tile_strides(sh);
+    for (int i = 0; i < sh.rank(); ++i) {
+      if (tile_index[i] < 0 || tile_index[i] >= sh.ext(i)) shape_error("tile index out of range");
+      const int64_t m = (h / st[i]) % sh.dims[i].t;
+      j_out[i] = sh.dims[i].interleaved ? m * sh.ext(i) + tile_index[i]
+                                        : tile_index[i] * sh.dims[i].t + m;
+    }
+  });
+}
+
+// slot_of tile_tensor.hpp:114-128
+int tt_slot_of(const tt_shape* s, const int64_t* j, int64_t* tile_index_out, int64_t* h_out) {
+  return guarded([&] {
+    const Shape sh = from_c(s);
+    const auto st = tile_strides(sh);
+    int64_t h = 0;
+    for (int i = 0; i < sh.rank(); ++i) {
+      const int64_t t = sh.dims[i].t;
+      const int64_t e = sh.ext(i);
+      if (j[i] < 0 || j[i] >= e * t) shape_error("logical index out of range");
+      if (sh.dims[i].interleaved) {
+        tile_index_out[i] = j[i] % e;
+        h += (j[i] / e) * st[i];
+      } else {
+        tile_index_out[i] = j[i] / t;
+        h += (j[i] % t) * st[i];
+      }
+    }
+    *h_out = h;
+  });
+}
+
+int64_t tt_rotations_left_to_right(int64_t n) { return ttb::rotations_left_to_right(n); }
+int64_t tt_rotations_right_to_left(int64_t n) { return ttb::rotations_right_to_left(n); }
+
+// ---- session --------------------------------------------------------------------
+
+int tt_device_count(int* out) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+  cudaGetLastError();
+  *out = n;
+  return TT_OK;
+}
+
+int tt_session_create(int64_t slot_count, int64_t max_chain_index, int device, tt_session** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (slot_count < 1) invalid_argument("slot count must be >= 1");       // backend.hpp:86
+    if (max_chain_index < 1) invalid_argument("max chain index must be >= 1");  // :87-88
+    if (slot_count >= (int64_t{1} << 31)) invalid_argument("slot count must be < 2^31");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      throw Error(TT_ERR_NO_DEVICE, "no CUDA device: the tile-tensor backend runs only on the GPU");
+    }
+    if (device < 0 || device >= n) invalid_argument("device ordinal out of range");
+    auto* s = new tt_session();
+    s->slots = slot_count;
+    s->depth = max_chain_index;
+    s->device = device;
+    try {
+      check_cuda(cudaSetDevice(device), "cudaSetDevice");
+      check_cuda(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking), "stream");
+      s->stream = s->own_stream;
+      cudaDeviceProp prop{};
+      check_cuda(cudaGetDeviceProperties(&prop, device), "device properties");
+      s->sm_count = prop.multiProcessorCount;
+      s->smem_optin = prop.sharedMemPerBlockOptin;
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+void tt_session_destroy(tt_session* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  if (s->own_stream) cudaStreamSynchronize(s->own_stream);
+  if (s->scratch) cudaFree(s->scratch);
+  if (s->own_stream) cudaStreamDestroy(s->own_stream);
+  delete s;
+}
+
+int64_t tt_session_slot_count(const tt_session* s) { return s ? s->slots : -1; }
+int64_t tt_session_max_chain_index(const tt_session* s) { return s ? s->depth : -1; }
+int tt_session_device(const tt_session* s) { return s ? s->device : -1; }
+
+int tt_session_set_stream(tt_session* s, void* stream) {
+  return guarded([&] {
+    need_session(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int tt_session_use_own_stream(tt_session* s) {
+  return guarded([&] {
+    need_session(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->stream = s->own_stream;
+  });
+}
+
+void* tt_session_stream(const tt_session* s) { return s ? s->stream : nullptr; }
+
+int tt_session_synchronize(tt_session* s) {
+  return guarded([&] {
+    need_session(s);
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    check_cuda(cudaStreamSynchronize(s->stream), "stream synchronize");
+  });
+}
+
+void tt_session_cost(const tt_session* s, tt_cost* out) {
+  std::memset(out, 0, sizeof(*out));
+  if (!s) return;
+  out->additions = s->adds.load(std::memory_order_relaxed);
+  out->multiplications = s->muls.load(std::memory_order_relaxed);
+  out->mask_multiplications = s->masks.load(std::memory_order_relaxed);
+  out->rotations = s->rots.load(std::memory_order_relaxed);
+  out->bootstraps = s->boots.load(std::memory_order_relaxed);
+  out->power_of_two_rotations = s->pow2.load(std::memory_order_relaxed);
+}
+
+void tt_session_reset_counters(tt_session* s) {
+  if (!s) return;
+  s->adds = 0;
+  s->muls = 0;
+  s->masks = 0;
+  s->rots = 0;
+  s->boots = 0;
+  s->pow2 = 0;
+}
+
+uint64_t tt_session_launches(const tt_session* s) { return s ? s->launches : 0; }
+
+void tt_session_count_bootstraps(tt_session* s, int64_t count) {
+  if (s && count > 0) s->boots += static_cast<uint64_t>(count);
+}
+
+// ---- memory -----------------------------------------------------------------------
+
+int tt_device_alloc(tt_session* s, int64_t bytes, void** out) {
+  return guarded([&] {
+    need_session(s);
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    *out = nullptr;
+    if (bytes > 0) check_cuda(cudaMalloc(out, static_cast<size_t>(bytes)), "cudaMalloc");
+  });
+}
+
+int tt_device_free(tt_session* s, void* p) {
+  return guarded([&] {
+    need_session(s);
+    if (p) check_cuda(cudaFree(p), "cudaFree");
+  });
+}
+
+int tt_copy_h2d(tt_session* s, void* dst, const void* src, int64_t bytes) {
+  return guarded([&] {
+    need_session(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    if (bytes > 0)
+      check_cuda(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyHostToDevice,
+                                 s->stream),
+                 "h2d copy");
+  });
+}
+
+int tt_copy_d2h(tt_session* s, void* dst, const void* src, int64_t bytes) {
+  return guarded([&] {
+    need_session(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    if (bytes > 0) {
+      check_cuda(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost,
+                                 s->stream),
+                 "d2h copy");
+      check_cuda(cudaStreamSynchronize(s->stream), "d2h sync");
+    }
+  });
+}
+
+int tt_copy_d2d(tt_session* s, void* dst, const void* src, int64_t bytes) {
+  return guarded([&] {
+    need_session(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    if (bytes > 0)
+      check_cuda(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice,
+                                 s->stream),
+                 "d2d copy");
+  });
+}
+
+int tt_fill_uniform(tt_session* s, double* out, int64_t count, uint64_t seed, int64_t offset,
+                    double lo, double hi) {
+  return guarded([&] {
+    need_session(s);
+    std::lock_guard<std::mutex> lk(s->mu);
+    launch_fill_uniform(ctx_of(s), out, count, seed, offset, lo, hi);
+  });
+}
+
+// ---- tile-tensor operators ------------------------------------------------------
+
+int tt_pack(tt_session* s, const double* dense, const tt_shape* shape, double* tiles) {
+  return guarded([&] {
+    need_session(s);
+    const Shape sh = from_c(shape);
+    if (sh.has_unknown())  // tile_tensor.hpp:169-170
+      shape_error("pack target shape may not contain '?': " + format_shape(sh));
+    require_slots(s, sh, "pack");
+    check_tiles_addressable(sh);
+    std::lock_guard<std::mutex> lk(s->mu);
+    launch_pack(ctx_of(s), sh, s->slots, dense, tiles);
+  });
+}
+
+int tt_unpack(tt_session* s, const tt_shape* shape, const double* tiles, double* dense) {
+  return guarded([&] {
+    need_session(s);
+    const Shape sh = from_c(shape);
+    require_slots(s, sh, "unpack");
+    check_tiles_addressable(sh);
+    std::lock_guard<std::mutex> lk(s->mu);
+    launch_unpack(ctx_of(s), sh, s->slots, tiles, dense);
+  });
+}
+
+int tt_elementwise(tt_session* s, int op, const tt_shape* a, const double* ta, int64_t chain_a,
+                   const tt_shape* b, const double* tb, int64_t chain_b, tt_shape* out_shape,
+                   double* out, int64_t* out_chain) {
+  return guarded([&] {
+    need_session(s);
+    if (op != TT_OP_ADD && op != TT_OP_MUL) invalid_argument("unknown elementwise op");
+    const Shape sa = from_c(a), sb = from_c(b);
+    const Shape so = elementwise_result_shape(sa, sb, op);
+    require_slots(s, sa, "elementwise");
+    require_slots(s, sb, "elementwise");
+    check_tiles_addressable(so);
+    const int64_t chain = op == TT_OP_MUL ? mul_chain(chain_a, chain_b) : std::min(chain_a, chain_b);
+    to_c(so, out_shape);
+    if (out_chain) *out_chain = chain;
+    const uint64_t n = static_cast<uint64_t>(so.tile_count());
+    if (op == TT_OP_ADD)
+      s->adds += n;
+    else
+      s->muls += n;
+    std::lock_guard<std::mutex> lk(s->mu);
+    launch_elementwise(ctx_of(s), op, so, sa, sb, s->slots, ta, tb, out);
+  });
+}
+
+int tt_sum(tt_session* s, const tt_shape* in_shape, const double* tin, int dim, int variant,
+           tt_shape* out_shape, double* out) {
+  return guarded([&] {
+    need_session(s);
+    const Shape sh = from_c(in_shape);
+    const Shape so = sum_result_shape(sh, dim);
+    require_slots(s, sh, "tt_sum");
+    check_tiles_addressable(sh);
+    to_c(so, out_shape);
+    const int di = dim - 1;
+    const Dim& ds = sh.dims[di];
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (ds.n == 1 && ds.d > 1) {  // degenerate: tiles unchanged (tile_tensor.hpp:295)
+      copy_tiles(ctx_of(s), out, tin, sh.tile_count() * s->slots);
+      return;
+    }
+    std::vector<int64_t> st;
+    operand_strides(sh, st);
+    run_reduction(s, sh, di, variant, tin, st, nullptr, st, out);
+  });
+}
+
+int tt_mul_sum(tt_session* s, const tt_shape* a, const double* ta, int64_t chain_a,
+               const tt_shape* b, const double* tb, int64_t chain_b, int dim, int variant,
+               tt_shape* out_shape, double* out, int64_t* out_chain) {
+  return guarded([&] {
+    need_session(s);
+    const Shape sa = from_c(a), sb = from_c(b);
+    const Shape prod = elementwise_result_shape(sa, sb, TT_OP_MUL);  // tt_mul
+    require_slots(s, sa, "tt_mul");
+    require_slots(s, sb, "tt_mul");
+    check_tiles_addressable(prod);
+    const int64_t chain = mul_chain(chain_a, chain_b);
+    const Shape so = sum_result_shape(prod, dim);  // tt_sum
+    to_c(so, out_shape);
+    if (out_chain) *out_chain = chain;
+    s->muls += static_cast<uint64_t>(prod.tile_count());
+    std::lock_guard<std::mutex> lk(s->mu);
+    const int di = dim - 1;
+    const Dim& ds = prod.dims[di];
+    if (ds.n == 1 && ds.d > 1) {  // degenerate sum: the product itself
+      launch_elementwise(ctx_of(s), TT_OP_MUL, prod, sa, sb, s->slots, ta, tb, out);
+      return;
+    }
+    std::vector<int64_t> ast, bst;
+    operand_strides(sa, ast);
+    operand_strides(sb, bst);
+    run_reduction(s, prod, di, variant, ta, ast, tb, bst, out);
+  });
+}
+
+int tt_linalg_product(tt_session* s, int which, const tt_shape* a, const double* ta,
+                      int64_t chain_a, const tt_shape* b, const double* tb, int64_t chain_b,
+                      int variant, tt_shape* out_shape, double* out, int64_t* out_chain) {
+  int rc = guarded([&] {
+    static const char* names[] = {"matvec_a", "matvec_b", "matmul_a", "matmul_b"};
+    if (which < 0 || which > 3) invalid_argument("unknown product form");
+    const Shape sa = from_c(a), sb = from_c(b);
+    const int rank = which < 2 ? 2 : 3;
+    if (sa.rank() != rank || sb.rank() != rank)
+      shape_error(std::string(names[which]) + " expects rank-" + std::to_string(rank) +
+                  " operands");
+    // require_replicated linalg.hpp:32-37
+    auto req = [&](const Shape& sh, int d0) {
+      const Dim& ds = sh.dims[d0];
+      if (!(ds.n == 1 && ds.d == ds.t))
+        shape_error(std::string(names[which]) + ": operand dimension " + std::to_string(d0 + 1) +
+                    " must be fully replicated, got " + format_shape(sh));
+    };
+    if (which == 0) req(sb, 0);
+    if (which == 1) req(sb, 1);
+    if (which == 2) {
+      req(sa, 2);
+      req(sb, 0);
+    }
+    if (which == 3) {
+      req(sa, 2);
+      req(sb, 1);
+    }
+  });
+  if (rc != TT_OK) return rc;
+  const int dim = (which == 0 || which == 2) ? 2 : 1;
+  return tt_mul_sum(s, a, ta, chain_a, b, tb, chain_b, dim, variant, out_shape, out, out_chain);
+}
+
+int tt_clean_unknowns(tt_session* s, const tt_shape* in_shape, const double* tin, int64_t chain,
+                      tt_shape* out_shape, double* out, int64_t* out_chain) {
+  return guarded([&] {
+    need_session(s);
+    Shape sh = from_c(in_shape);
+    require_slots(s, sh, "clean_unknowns");
+    check_tiles_addressable(sh);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (!sh.has_unknown()) {  // tile_tensor.hpp:354: returned as is, zero cost
+      to_c(sh, out_shape);
+      if (out_chain) *out_chain = chain;
+      copy_tiles(ctx_of(s), out, tin, sh.tile_count() * s->slots);
+      return;
+    }
+    if (chain < 1)  // backend.hpp:142-143
+      depth_error("plaintext multiplication at chain index 0 (bootstrap required)");
+    const LaunchCtx c = ctx_of(s);
+    launch_clean(c, sh, s->slots, tin, out);
+    s->masks += static_cast<uint64_t>(sh.tile_count());
+    for (auto& d : sh.dims) d.unknown = false;
+    to_c(sh, out_shape);
+    if (out_chain) *out_chain = chain - 1;
+  });
+}
+
+int tt_replicate_dim(tt_session* s, const tt_shape* in_shape, const double* tin, int dim,
+                     tt_shape* out_shape, double* out) {
+  return guarded([&] {
+    need_session(s);
+    Shape sh = from_c(in_shape);
+    if (dim < 1 || dim > sh.rank()) shape_error("replicate dimension out of range");
+    const int di = dim - 1;
+    const Dim ds = sh.dims[di];
+    if (ds.unknown)
+      shape_error("replicate_dim requires a clean dimension (run clean_unknowns first)");
+    if (ds.n != 1 || ds.d != 1)
+      shape_error("replicate_dim requires a degenerate dimension (n=1, d=1)");
+    if (sh.relaxed) shape_error("replicate_dim is not defined for relaxed shapes");
+    require_slots(s, sh, "replicate_dim");
+    check_tiles_addressable(sh);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (ds.t == 1) {
+      to_c(sh, out_shape);
+      copy_tiles(ctx_of(s), out, tin, sh.tile_count() * s->slots);
+      return;
+    }
+    const int64_t stride = tile_strides(sh)[di];
+    const Program prog = build_replicate_program(ds.t, stride, s->slots);
+    GroupSpec g;
+    g.nd = 1;
+    g.ext[0] = sh.tile_count();
+    g.out_stride[0] = 1;
+    g.a_stride[0] = 1;
+    g.groups = sh.tile_count();
+    add_cost(s, prog.per_group, static_cast<uint64_t>(g.groups));
+    launch_group_program(ctx_of(s), prog, g, s->slots, tin, nullptr, out);
+    sh.dims[di].d = ds.t;
+    sh.dims[di].interleaved = false;
+    to_c(sh, out_shape);
+  });
+}
+
+// ---- tile-level primitives ----------------------------------------------------------
+
+int tt_tiles_binary(tt_session* s, int op, const double* a, const double* b, double* out,
+                    int64_t n_tiles, const int64_t* chain_a, const int64_t* chain_b,
+                    int64_t* chain_out) {
+  return guarded([&] {
+    need_session(s);
+    if (op != TT_OP_ADD && op != TT_OP_MUL) invalid_argument("unknown elementwise op");
+    if (chain_a && chain_b) {
+      for (int64_t i = 0; i < n_tiles; ++i) {
+        const int64_t c = op == TT_OP_MUL ? mul_chain(chain_a[i], chain_b[i])
+                                          : std::min(chain_a[i], chain_b[i]);
+        if (chain_out) chain_out[i] = c;
+      }
+    }
+    if (op == TT_OP_ADD)
+      s->adds += static_cast<uint64_t>(n_tiles);
+    else
+      s->muls += static_cast<uint64_t>(n_tiles);
+    std::lock_guard<std::mutex> lk(s->mu);
+    launch_binary_flat(ctx_of(s), op, a, b, out, n_tiles * s->slots);
+  });
+}
+
+int tt_tiles_mask_mul(tt_session* s, const double* a, const double* mask, double* out,
+                      int64_t n_tiles, const int64_t* chain_a, int64_t* chain_out) {
+  return guarded([&] {
+    need_session(s);
+    if (chain_a) {
+      for (int64_t i = 0; i < n_tiles; ++i) {
+        if (chain_a[i] < 1)
+          depth_error("plaintext multiplication at chain index 0 (bootstrap required)");
+        if (chain_out) chain_out[i] = chain_a[i] - 1;
+      }
+    }
+    s->masks += static_cast<uint64_t>(n_tiles);
+    std::lock_guard<std::mutex> lk(s->mu);
+    launch_binary_flat(ctx_of(s), TT_OP_MUL, a, mask, out, n_tiles * s->slots);
+  });
+}
+
+int tt_tiles_rotate(tt_session* s, const double* in, int64_t offset, double* out,
+                    int64_t n_tiles) {
+  return guarded([&] {
+    need_session(s);
+    const int64_t sl = s->slots;
+    const int64_t r = ((offset % sl) + sl) % sl;  // backend.hpp:155
+    std::lock_guard<std::mutex> lk(s->mu);
+    const LaunchCtx c = ctx_of(s);
+    if (r == 0) {  // free and uncounted (backend.hpp:156)
+      copy_tiles(c, out, in, n_tiles * sl);
+      return;
+    }
+    if (in == out) invalid_argument("rotate cannot run in place");
+    s->rots += static_cast<uint64_t>(n_tiles);
+    if ((r & (r - 1)) == 0) s->pow2 += static_cast<uint64_t>(n_tiles);
+    launch_rotate(c, in, out, sl, r, n_tiles);
+  });
+}
+
+namespace {
+int run_tile_program(tt_session* s, const Program& prog, const double* in, double* out,
+                     int64_t n_tiles) {
+  GroupSpec g;
+  g.nd = 1;
+  g.ext[0] = n_tiles;
+  g.out_stride[0] = 1;
+  g.a_stride[0] = 1;
+  g.groups = n_tiles;
+  add_cost(s, prog.per_group, static_cast<uint64_t>(n_tiles));
+  launch_group_program(ctx_of(s), prog, g, s->slots, in, nullptr, out);
+  return TT_OK;
+}
+}  // namespace
+
+int tt_sum_tile_strided(tt_session* s, const double* in, int64_t n, int64_t stride, int variant,
+                        double* out, int64_t n_tiles) {
+  return guarded([&] {
+    need_session(s);
+    const Program prog = build_strided_program(n, stride, s->slots, variant);
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (n == 1) {
+      copy_tiles(ctx_of(s), out, in, n_tiles * s->slots);
+      return;
+    }
+    run_tile_program(s, prog, in, out, n_tiles);
+  });
+}
+
+int tt_sum_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents, int rank,
+                    int dim, int variant, double* out, int64_t n_tiles) {
+  return guarded([&] {
+    need_session(s);
+    if (dim < 1 || dim > rank) invalid_argument("tile dimension out of range");
+    int64_t stride = 1;
+    for (int x = dim; x < rank; ++x) stride *= tile_extents[x];
+    const int64_t n = tile_extents[dim - 1];
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (n == 1) {
+      copy_tiles(ctx_of(s), out, in, n_tiles * s->slots);
+      return;
+    }
+    run_tile_program(s, build_strided_program(n, stride, s->slots, variant), in, out, n_tiles);
+  });
+}
+
+int tt_replicate_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents, int rank,
+                          int dim, double* out, int64_t n_tiles) {
+  return guarded([&] {
+    need_session(s);
+    if (dim < 1 || dim > rank) invalid_argument("tile dimension out of range");
+    int64_t stride = 1;
+    for (int x = dim; x < rank; ++x) stride *= tile_extents[x];
+    const int64_t t = tile_extents[dim - 1];
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (t == 1) {
+      copy_tiles(ctx_of(s), out, in, n_tiles * s->slots);
+      return;
+    }
+    run_tile_program(s, build_replicate_program(t, stride, s->slots), in, out, n_tiles);
+  });
+}
+
+// ---- sharding ---------------------------------------------------------------------
+
+int tt_shard_plan(const tt_shape* shape, int shard_dim, int world, int rank, int64_t* begin,
+                  int64_t* end, tt_shape* local_shape) {
+  return guarded([&] {
+    Shape sh = from_c(shape);
+    if (shard_dim < 1 || shard_dim > sh.rank()) shape_error("shard dimension out of range");
+    if (world < 1 || rank < 0 || rank >= world) invalid_argument("bad rank/world");
+    const int di = shard_dim - 1;
+    Dim& d = sh.dims[di];
+    if (d.interleaved) shape_error("interleaved dimensions cannot be block-sharded");
+    if (d.n == 1 && d.d > 1) shape_error("replicated dimensions are not sharded");
+    const int64_t e = sh.ext(di);
+    const int64_t b = e * rank / world, en = e * (rank + 1) / world;
+    *begin = b;
+    *end = en;
+    const int64_t lo = b * d.t;
+    const int64_t hi = std::min(d.used(), en * d.t);
+    d.n = std::max<int64_t>(hi - lo, 0);
+    if (d.n == 0) d.n = 1;  // an empty rank still carries a valid shape
+    to_c(sh, local_shape);
+  });
+}
+
+}  // extern "C"

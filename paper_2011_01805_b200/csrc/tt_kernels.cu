@@ -1,0 +1,929 @@
+// tt_kernels.cu -- hand-written sm_100a kernels of the tile-tensor hot path.
+//
+// Everything here is HBM-bandwidth bound fp64 gather/stream/reduction work
+// (SURVEY 8d): no tensor cores.  Design rules applied throughout:
+//  * persistent grids sized to (SM count x resident CTAs), grid-stride work;
+//  * coalesced 16-byte (double2) accesses on the streamed operand;
+//  * integer index math through precomputed magic-number division (no
+//    hardware div/mod per slot);
+//  * every fp64 operation is __dadd_rn / __dmul_rn, so ptxas cannot contract
+//    a multiply and an add into an FMA: results are bit-identical to the
+//    reference's scalar x86 loops (which have no FMA);
+//  * reductions keep the reference's association exactly: the external left
+//    fold (tile_tensor.hpp:323-324) runs per slot in registers, and the
+//    in-tile rotate-and-sum schedule runs from shared memory without any HBM
+//    round trip per rotation (north-star item 3).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "tt_launch.hpp"
+
+namespace ttb {
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(TT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+constexpr int R = TT_MAX_RANK;
+
+// ---- magic-number division ----------------------------------------------------
+
+struct FastDiv64 {
+  uint64_t d = 1, m = 0;
+  uint32_t l = 0;
+};
+
+FastDiv64 make_div64(uint64_t d) {
+  FastDiv64 f;
+  f.d = d;
+  if (d <= 1) return f;
+  uint32_t l = 0;
+  while ((uint64_t{1} << l) < d) ++l;  // l = ceil(log2 d), 1..63
+  const unsigned __int128 two64 = static_cast<unsigned __int128>(1) << 64;
+  const unsigned __int128 num = two64 * ((static_cast<unsigned __int128>(1) << l) - d);
+  f.m = static_cast<uint64_t>(num / d) + 1;
+  f.l = l;
+  return f;
+}
+
+__device__ __forceinline__ uint64_t fdiv(uint64_t n, const FastDiv64& f) {
+  if (f.d == 1) return n;
+  const uint64_t t = __umul64hi(n, f.m);
+  return (t + ((n - t) >> 1)) >> (f.l - 1);
+}
+
+struct FastDiv32 {
+  uint32_t d = 1, m = 0, l = 0;
+};
+
+FastDiv32 make_div32(uint32_t d) {
+  FastDiv32 f;
+  f.d = d;
+  if (d <= 1) return f;
+  uint32_t l = 0;
+  while ((uint64_t{1} << l) < d) ++l;
+  const uint64_t num = (uint64_t{1} << 32) * ((uint64_t{1} << l) - d);
+  f.m = static_cast<uint32_t>(num / d + 1);
+  f.l = l;
+  return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv32& f) {
+  if (f.d == 1) return n;
+  const uint32_t t = __umulhi(n, f.m);
+  return (t + ((n - t) >> 1)) >> (f.l - 1);
+}
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+int grid_for(const LaunchCtx& c, const void* kernel, int threads, size_t smem, int64_t work) {
+  int per_sm = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem),
+             "occupancy query");
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = static_cast<int64_t>(c.sm_count) * per_sm;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cap, work)));
+}
+
+void count_launch(const LaunchCtx& c) {
+  if (c.launches) ++*c.launches;
+}
+
+void post_launch(const LaunchCtx& c, const char* what) {
+  count_launch(c);
+  check_cuda(cudaGetLastError(), what);
+}
+
+// ---- tile-grid geometry shared by pack / unpack / clean ------------------------
+
+struct Geo {
+  int rank;
+  int64_t s;            // slots per tile
+  int64_t tile_slots;   // prod t_i (< s only for relaxed shapes)
+  int64_t n_tiles;
+  FastDiv32 tdiv[R];    // divide by t_i
+  FastDiv32 ediv[R];    // divide by ext_i
+  FastDiv64 ndiv[R];    // divide by n_i (dense decomposition)
+  int64_t t[R], ext[R], used[R], n[R];
+  int64_t tstride[R];   // in-tile stride of dim i
+  int64_t estride[R];   // external (tile-index) stride of dim i
+  int64_t dstride[R];   // dense stride of dim i, 0 when n_i == 1 (replication)
+  int32_t inter[R];
+};
+
+Geo make_geo(const Shape& sh, int64_t s) {
+  Geo g;
+  std::memset(&g, 0, sizeof(g));
+  g.rank = sh.rank();
+  g.s = s;
+  g.tile_slots = sh.tile_slots();
+  g.n_tiles = sh.tile_count();
+  const auto ext = sh.external();
+  const auto ts = tile_strides(sh);
+  const auto es = row_major_strides(ext);
+  std::vector<int64_t> nn;
+  for (const auto& d : sh.dims) nn.push_back(d.n);
+  const auto ds = row_major_strides(nn);
+  for (int i = 0; i < g.rank; ++i) {
+    const Dim& d = sh.dims[i];
+    g.tdiv[i] = make_div32(static_cast<uint32_t>(d.t));
+    g.ediv[i] = make_div32(static_cast<uint32_t>(ext[i]));
+    g.ndiv[i] = make_div64(static_cast<uint64_t>(d.n));
+    g.t[i] = d.t;
+    g.ext[i] = ext[i];
+    g.used[i] = d.used();
+    g.n[i] = d.n;
+    g.tstride[i] = ts[i];
+    g.estride[i] = es[i];
+    g.dstride[i] = d.n == 1 ? 0 : ds[i];
+    g.inter[i] = d.interleaved ? 1 : 0;
+  }
+  return g;
+}
+
+// Decompose tile index `flat` into external coordinates l_i.
+template <int RK>
+__device__ __forceinline__ void tile_coords(const Geo& g, uint32_t flat, uint32_t* l) {
+#pragma unroll
+  for (int i = RK - 1; i >= 0; --i) {
+    if (i < g.rank) {
+      const uint32_t q = fdiv(flat, g.ediv[i]);
+      l[i] = flat - q * g.ediv[i].d;
+      flat = q;
+    }
+  }
+}
+
+// Eq.(1) (tile_tensor.hpp:205-214): source offset of slot h of the tile with
+// coordinates l, or -1 when the slot is outside the used box (zero padding).
+template <int RK>
+__device__ __forceinline__ int64_t slot_source(const Geo& g, const uint32_t* l, uint32_t h) {
+  if (h >= static_cast<uint64_t>(g.tile_slots)) return -1;
+  int64_t src = 0;
+#pragma unroll
+  for (int i = RK - 1; i >= 0; --i) {
+    if (i < g.rank) {
+      const uint32_t q = fdiv(h, g.tdiv[i]);
+      const int64_t m = h - q * g.tdiv[i].d;
+      h = q;
+      const int64_t j = g.inter[i] ? m * g.ext[i] + l[i] : static_cast<int64_t>(l[i]) * g.t[i] + m;
+      if (j >= g.used[i]) return -1;
+      src += j * g.dstride[i];
+    }
+  }
+  return src;
+}
+
+// ---- pack ------------------------------------------------------------------------
+// One work item = 4 consecutive slots of one tile; a warp writes 1 KiB
+// contiguous with two 16-byte stores per lane, and gathers its sources in
+// runs of t_k contiguous dense elements.
+
+template <int RK, bool VEC>
+__global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ Geo g,
+                                                    const double* __restrict__ dense,
+                                                    double* __restrict__ tiles,
+                                                    FastDiv64 quads_div) {
+  const uint64_t total = static_cast<uint64_t>(g.n_tiles) * quads_div.d;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t flat = fdiv(w, quads_div);
+    const uint32_t h0 = static_cast<uint32_t>((w - flat * quads_div.d) * 4);
+    uint32_t l[RK];
+    tile_coords<RK>(g, static_cast<uint32_t>(flat), l);
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t src = slot_source<RK>(g, l, h0 + k);
+      v[k] = src >= 0 ? __ldg(dense + src) : 0.0;
+    }
+    double* out = tiles + flat * g.s + h0;
+    if (VEC && h0 + 4 <= g.s) {
+      reinterpret_cast<double2*>(out)[0] = make_double2(v[0], v[1]);
+      reinterpret_cast<double2*>(out)[1] = make_double2(v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (h0 + k < g.s) out[k] = v[k];
+    }
+  }
+}
+
+// ---- unpack ----------------------------------------------------------------------
+// One work item = 4 consecutive dense elements (coalesced writes); each reads
+// replica 0 (tile_tensor.hpp:231-239).
+
+template <int RK>
+__global__ void __launch_bounds__(256) unpack_kernel(const __grid_constant__ Geo g,
+                                                      const double* __restrict__ tiles,
+                                                      double* __restrict__ dense,
+                                                      uint64_t total) {
+  const uint64_t quads = (total + 3) / 4;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < quads;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t f = w * 4;
+    int64_t j[RK];
+    uint64_t rem = f;
+#pragma unroll
+    for (int i = RK - 1; i >= 0; --i) {
+      if (i < g.rank) {
+        const uint64_t q = fdiv(rem, g.ndiv[i]);
+        j[i] = static_cast<int64_t>(rem - q * g.ndiv[i].d);
+        rem = q;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (f + k < total) {
+        int64_t tile = 0, h = 0;
+#pragma unroll
+        for (int i = 0; i < RK; ++i) {
+          if (i < g.rank) {
+            int64_t li, mi;
+            if (g.inter[i]) {
+              const uint32_t q = fdiv(static_cast<uint32_t>(j[i]), g.ediv[i]);
+              li = j[i] - static_cast<int64_t>(q) * g.ext[i];
+              mi = q;
+            } else {
+              const uint32_t q = fdiv(static_cast<uint32_t>(j[i]), g.tdiv[i]);
+              li = q;
+              mi = j[i] - static_cast<int64_t>(q) * g.t[i];
+            }
+            tile += li * g.estride[i];
+            h += mi * g.tstride[i];
+          }
+        }
+        dense[f + k] = __ldg(tiles + tile * g.s + h);
+        // odometer step
+#pragma unroll
+        for (int i = RK - 1; i >= 0; --i) {
+          if (i < g.rank) {
+            if (++j[i] < g.n[i]) break;
+            j[i] = 0;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---- clean_unknowns: multiply by the 0/1 used indicator ---------------------------
+
+template <int RK>
+__global__ void __launch_bounds__(256) clean_kernel(const __grid_constant__ Geo g,
+                                                     const double* __restrict__ in,
+                                                     double* __restrict__ out,
+                                                     FastDiv64 quads_div) {
+  const uint64_t total = static_cast<uint64_t>(g.n_tiles) * quads_div.d;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t flat = fdiv(w, quads_div);
+    const uint32_t h0 = static_cast<uint32_t>((w - flat * quads_div.d) * 4);
+    uint32_t l[RK];
+    tile_coords<RK>(g, static_cast<uint32_t>(flat), l);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t h = h0 + k;
+      if (h < g.s) {
+        const double mask = slot_source<RK>(g, l, h) >= 0 ? 1.0 : 0.0;
+        const uint64_t o = flat * g.s + h;
+        out[o] = dmul(in[o], mask);  // Session::mask_mul backend.hpp:145
+      }
+    }
+  }
+}
+
+// ---- elementwise with external broadcast ------------------------------------------
+
+struct EwParams {
+  int rank;
+  int64_t s;
+  int64_t n_tiles;
+  FastDiv32 ediv[R];      // out external extents
+  int64_t a_stride[R];    // tile-index stride of A along dim i, 0 where A broadcasts
+  int64_t b_stride[R];
+};
+
+template <int OP, bool VEC>
+__global__ void __launch_bounds__(256) elementwise_kernel(const __grid_constant__ EwParams p,
+                                                           const double* __restrict__ a,
+                                                           const double* __restrict__ b,
+                                                           double* __restrict__ out,
+                                                           FastDiv64 quads_div) {
+  const uint64_t total = static_cast<uint64_t>(p.n_tiles) * quads_div.d;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t flat = fdiv(w, quads_div);
+    const uint32_t h0 = static_cast<uint32_t>((w - flat * quads_div.d) * 4);
+    uint32_t rem = static_cast<uint32_t>(flat);
+    int64_t fa = 0, fb = 0;
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      if (i < p.rank) {
+        const uint32_t q = fdiv(rem, p.ediv[i]);
+        const int64_t li = rem - q * p.ediv[i].d;
+        rem = q;
+        fa += li * p.a_stride[i];
+        fb += li * p.b_stride[i];
+      }
+    }
+    const double* pa = a + fa * p.s + h0;
+    const double* pb = b + fb * p.s + h0;
+    double* po = out + flat * p.s + h0;
+    if (VEC && h0 + 4 <= p.s) {
+      const double2 a0 = __ldg(reinterpret_cast<const double2*>(pa));
+      const double2 a1 = __ldg(reinterpret_cast<const double2*>(pa) + 1);
+      const double2 b0 = __ldg(reinterpret_cast<const double2*>(pb));
+      const double2 b1 = __ldg(reinterpret_cast<const double2*>(pb) + 1);
+      double2 o0, o1;
+      if (OP == TT_OP_ADD) {
+        o0 = make_double2(dadd(a0.x, b0.x), dadd(a0.y, b0.y));
+        o1 = make_double2(dadd(a1.x, b1.x), dadd(a1.y, b1.y));
+      } else {
+        o0 = make_double2(dmul(a0.x, b0.x), dmul(a0.y, b0.y));
+        o1 = make_double2(dmul(a1.x, b1.x), dmul(a1.y, b1.y));
+      }
+      reinterpret_cast<double2*>(po)[0] = o0;
+      reinterpret_cast<double2*>(po)[1] = o1;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (h0 + k < p.s)
+          po[k] = OP == TT_OP_ADD ? dadd(pa[k], pb[k]) : dmul(pa[k], pb[k]);
+    }
+  }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(256) binary_flat_kernel(const double* __restrict__ a,
+                                                           const double* __restrict__ b,
+                                                           double* __restrict__ out,
+                                                           uint64_t count) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = OP == TT_OP_ADD ? dadd(a[i], b[i]) : dmul(a[i], b[i]);
+}
+
+__global__ void __launch_bounds__(256) rotate_kernel(const double* __restrict__ in,
+                                                      double* __restrict__ out, uint64_t s,
+                                                      uint64_t r, uint64_t total,
+                                                      FastDiv64 sdiv) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t tile = fdiv(i, sdiv);
+    uint64_t j = i - tile * s + r;
+    if (j >= s) j -= s;
+    out[i] = in[tile * s + j];
+  }
+}
+
+// ---- group programs (reductions) ---------------------------------------------------
+
+struct GroupParams {
+  GroupSpec g;
+  FastDiv64 gdiv[R];  // divide by g.ext[i]
+  int64_t s;
+  int nops;
+  int nbuf;           // logical scratch tiles
+  int use_smem;       // scratch tiles live in dynamic shared memory
+  int nlevels;        // simple_pow2: number of in-place ROTADD levels
+  int64_t rots[64];   // simple_pow2: rotation of each level
+  GOp ops[kMaxOps];
+};
+
+struct GroupBase {
+  int64_t out, a, b;
+};
+
+__device__ __forceinline__ GroupBase group_base(const GroupParams& p, uint64_t v) {
+  GroupBase gb{0, 0, 0};
+#pragma unroll
+  for (int i = R - 1; i >= 0; --i) {
+    if (i < p.g.nd) {
+      const uint64_t q = fdiv(v, p.gdiv[i]);
+      const int64_t c = static_cast<int64_t>(v - q * p.gdiv[i].d);
+      v = q;
+      gb.out += c * p.g.out_stride[i];
+      gb.a += c * p.g.a_stride[i];
+      gb.b += c * p.g.b_stride[i];
+    }
+  }
+  return gb;
+}
+
+// FOLD for one pair of slots (j, j+1) when VEC, else one slot j:
+//   acc = P[first]; acc = acc + P[first+1]; ...   P[l] = A[l] (* B[l]).
+template <bool HAS_B, bool VEC>
+__device__ __forceinline__ void fold_slots(const GroupParams& p, const GroupBase& gb,
+                                           const double* __restrict__ A,
+                                           const double* __restrict__ B, int64_t first,
+                                           int64_t count, int64_t j, double* dst) {
+  const int64_t s = p.s;
+  const double* pa = A + (gb.a + first * p.g.astep) * s + j;
+  const int64_t sa = p.g.astep * s;
+  const double* pb = HAS_B ? B + (gb.b + first * p.g.bstep) * s + j : nullptr;
+  const int64_t sb = p.g.bstep * s;
+  if (VEC) {
+    double2 x = __ldg(reinterpret_cast<const double2*>(pa));
+    double2 acc;
+    double2 w;
+    if (HAS_B) {
+      w = __ldg(reinterpret_cast<const double2*>(pb));
+      acc = make_double2(dmul(x.x, w.x), dmul(x.y, w.y));
+    } else {
+      acc = x;
+    }
+    if (HAS_B && sb == 0) {  // broadcast B along the summed dim: load once
+#pragma unroll 8
+      for (int64_t c = 1; c < count; ++c) {
+        x = __ldg(reinterpret_cast<const double2*>(pa + c * sa));
+        acc.x = dadd(acc.x, dmul(x.x, w.x));
+        acc.y = dadd(acc.y, dmul(x.y, w.y));
+      }
+    } else {
+#pragma unroll 4
+      for (int64_t c = 1; c < count; ++c) {
+        x = __ldg(reinterpret_cast<const double2*>(pa + c * sa));
+        if (HAS_B) {
+          const double2 y = __ldg(reinterpret_cast<const double2*>(pb + c * sb));
+          acc.x = dadd(acc.x, dmul(x.x, y.x));
+          acc.y = dadd(acc.y, dmul(x.y, y.y));
+        } else {
+          acc.x = dadd(acc.x, x.x);
+          acc.y = dadd(acc.y, x.y);
+        }
+      }
+    }
+    *reinterpret_cast<double2*>(dst) = acc;
+  } else {
+    double acc = HAS_B ? dmul(__ldg(pa), __ldg(pb)) : __ldg(pa);
+#pragma unroll 4
+    for (int64_t c = 1; c < count; ++c) {
+      const double x = __ldg(pa + c * sa);
+      acc = dadd(acc, HAS_B ? dmul(x, __ldg(pb + c * sb)) : x);
+    }
+    *dst = acc;
+  }
+}
+
+// Fast path: FOLD into one shared tile, then `nlevels` in-place rotate-adds
+// (the power-of-two schedule, rotate_sum.hpp:51-56), the last into the output
+// tile.  Each thread owns slots j = i*T + tid; a level reads the partner
+// slot from shared memory into registers, barriers, then writes.
+template <int VMAX, bool HAS_B, bool VEC>
+__global__ void __launch_bounds__(512, 1) group_pow2_kernel(const __grid_constant__ GroupParams p,
+                                                            const double* __restrict__ A,
+                                                            const double* __restrict__ B,
+                                                            double* __restrict__ OUT) {
+  extern __shared__ __align__(16) double sbuf[];
+  const int T = blockDim.x;
+  const int tid = threadIdx.x;
+  const int s = static_cast<int>(p.s);
+  const int64_t first = p.ops[0].x;
+  const int64_t count = p.ops[0].y;
+  for (uint64_t v = blockIdx.x; v < static_cast<uint64_t>(p.g.groups); v += gridDim.x) {
+    const GroupBase gb = group_base(p, v);
+    if (VEC) {
+      for (int q = tid; 2 * q < s; q += T)
+        fold_slots<HAS_B, true>(p, gb, A, B, first, count, 2 * q, sbuf + 2 * q);
+    } else {
+      for (int j = tid; j < s; j += T) fold_slots<HAS_B, false>(p, gb, A, B, first, count, j, sbuf + j);
+    }
+    __syncthreads();
+    double val[VMAX];
+#pragma unroll
+    for (int i = 0; i < VMAX; ++i) {
+      const int j = i * T + tid;
+      if (j < s) val[i] = sbuf[j];
+    }
+    for (int lv = 0; lv < p.nlevels; ++lv) {
+      const int r = static_cast<int>(p.rots[lv]);
+#pragma unroll
+      for (int i = 0; i < VMAX; ++i) {
+        const int j = i * T + tid;
+        if (j < s) {
+          int jj = j + r;
+          if (jj >= s) jj -= s;
+          val[i] = dadd(val[i], sbuf[jj]);
+        }
+      }
+      __syncthreads();
+      if (lv + 1 < p.nlevels) {
+#pragma unroll
+        for (int i = 0; i < VMAX; ++i) {
+          const int j = i * T + tid;
+          if (j < s) sbuf[j] = val[i];
+        }
+        __syncthreads();
+      }
+    }
+    double* out = OUT + gb.out * p.s;
+#pragma unroll
+    for (int i = 0; i < VMAX; ++i) {
+      const int j = i * T + tid;
+      if (j < s) out[j] = val[i];
+    }
+    // The last level's reads completed before its barrier, so the next
+    // group's FOLD may overwrite sbuf without another barrier.
+  }
+}
+
+// Generic interpreter: any program (ltr/rtl schedules, boundary split,
+// replication).  Logical buffers map onto nbuf+1 physical tiles; an in-place
+// ROTADD writes the spare tile and swaps it in, so one barrier per op.
+template <bool HAS_B>
+__global__ void __launch_bounds__(512) group_generic_kernel(const __grid_constant__ GroupParams p,
+                                                            const double* __restrict__ A,
+                                                            const double* __restrict__ B,
+                                                            double* __restrict__ OUT,
+                                                            double* __restrict__ scratch) {
+  extern __shared__ __align__(16) double sbuf[];
+  const int T = blockDim.x;
+  const int tid = threadIdx.x;
+  const int64_t s = p.s;
+  double* base = p.use_smem ? sbuf : scratch + static_cast<int64_t>(blockIdx.x) * (p.nbuf + 1) * s;
+  for (uint64_t v = blockIdx.x; v < static_cast<uint64_t>(p.g.groups); v += gridDim.x) {
+    const GroupBase gb = group_base(p, v);
+    double* out = OUT + gb.out * s;
+    int map[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) map[i] = i;
+    int spare = p.nbuf;
+    for (int k = 0; k < p.nops; ++k) {
+      const GOp op = p.ops[k];
+      double* dst;
+      bool swap = false;
+      if (op.dst == BUF_OUT) {
+        dst = out;
+      } else if (op.inplace) {
+        dst = base + static_cast<int64_t>(spare) * s;
+        swap = true;
+      } else {
+        dst = base + static_cast<int64_t>(map[op.dst]) * s;
+      }
+      if (op.kind == GOP_FOLD) {
+        for (int64_t j = tid; j < s; j += T)
+          fold_slots<HAS_B, false>(p, gb, A, B, op.x, op.y, j, dst + j);
+      } else {
+        const double* a = base + static_cast<int64_t>(map[op.a]) * s;
+        const double* b = base + static_cast<int64_t>(map[op.b]) * s;
+        const int64_t r = op.x;
+        if (op.kind == GOP_ROTADD) {
+          for (int64_t j = tid; j < s; j += T) {
+            int64_t jj = j + r;
+            if (jj >= s) jj -= s;
+            dst[j] = dadd(a[j], b[jj]);
+          }
+        } else {
+          for (int64_t j = tid; j < s; j += T) dst[j] = a[j];
+        }
+      }
+      if (swap) {
+        const int old = map[op.dst];
+        map[op.dst] = spare;
+        spare = old;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Split fold: (group, 4-slot quad) work items over the whole grid, writing the
+// folded tile straight into OUT.  Used when a reduction has no in-tile
+// schedule (t == 1) or has too few groups to fill the GPU (phase 1 of 2).
+template <bool HAS_B, bool VEC>
+__global__ void __launch_bounds__(256) fold_kernel(const __grid_constant__ GroupParams p,
+                                                    const double* __restrict__ A,
+                                                    const double* __restrict__ B,
+                                                    double* __restrict__ OUT,
+                                                    FastDiv64 quads_div) {
+  const uint64_t total = static_cast<uint64_t>(p.g.groups) * quads_div.d;
+  const int64_t first = p.ops[0].x;
+  const int64_t count = p.ops[0].y;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t v = fdiv(w, quads_div);
+    const int64_t j0 = static_cast<int64_t>(w - v * quads_div.d) * 4;
+    const GroupBase gb = group_base(p, v);
+    double* dst = OUT + gb.out * p.s;
+    if (VEC && j0 + 4 <= p.s) {
+      fold_slots<HAS_B, true>(p, gb, A, B, first, count, j0, dst + j0);
+      fold_slots<HAS_B, true>(p, gb, A, B, first, count, j0 + 2, dst + j0 + 2);
+    } else {
+      for (int k = 0; k < 4; ++k)
+        if (j0 + k < p.s) fold_slots<HAS_B, false>(p, gb, A, B, first, count, j0 + k, dst + j0 + k);
+    }
+  }
+}
+
+// ---- synthetic input generator (== or_fill_uniform in oracle/tt_oracle.c) ------------
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void fill_uniform_kernel(double* out, uint64_t count, uint64_t key, uint64_t offset,
+                                    double lo, double span) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t u = splitmix64(key ^ (offset + i));
+    out[i] = dadd(lo, dmul(span, dmul(static_cast<double>(u >> 11), 0x1.0p-53)));
+  }
+}
+
+uint64_t host_splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+// ---- launchers ------------------------------------------------------------------
+
+#define TT_RANK_SWITCH(rank, RKV, ...)          \
+  switch (rank) {                               \
+    case 1: { constexpr int RKV = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int RKV = 2; __VA_ARGS__; } break; \
+    case 3: { constexpr int RKV = 3; __VA_ARGS__; } break; \
+    case 4: { constexpr int RKV = 4; __VA_ARGS__; } break; \
+    default: { constexpr int RKV = R; __VA_ARGS__; } break; \
+  }
+
+void launch_pack(const LaunchCtx& c, const Shape& shape, int64_t s, const double* dense,
+                 double* tiles) {
+  const Geo g = make_geo(shape, s);
+  if (g.n_tiles == 0) return;
+  const uint64_t quads = static_cast<uint64_t>((s + 3) / 4);
+  const FastDiv64 qd = make_div64(quads);
+  const int64_t work = (g.n_tiles * static_cast<int64_t>(quads) + 255) / 256;
+  const bool vec = (s % 2 == 0) && aligned16(tiles);
+  TT_RANK_SWITCH(g.rank, RK, {
+    const void* k = vec ? (const void*)pack_kernel<RK, true> : (const void*)pack_kernel<RK, false>;
+    const int grid = grid_for(c, k, 256, 0, work);
+    if (vec)
+      pack_kernel<RK, true><<<grid, 256, 0, c.stream>>>(g, dense, tiles, qd);
+    else
+      pack_kernel<RK, false><<<grid, 256, 0, c.stream>>>(g, dense, tiles, qd);
+  });
+  post_launch(c, "pack kernel");
+}
+
+void launch_unpack(const LaunchCtx& c, const Shape& shape, int64_t s, const double* tiles,
+                   double* dense) {
+  const Geo g = make_geo(shape, s);
+  const uint64_t total = static_cast<uint64_t>(shape.dense_count());
+  if (total == 0) return;
+  const int64_t work = static_cast<int64_t>((total + 1023) / 1024);
+  TT_RANK_SWITCH(g.rank, RK, {
+    const int grid = grid_for(c, (const void*)unpack_kernel<RK>, 256, 0, work);
+    unpack_kernel<RK><<<grid, 256, 0, c.stream>>>(g, tiles, dense, total);
+  });
+  post_launch(c, "unpack kernel");
+}
+
+void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const double* in,
+                  double* out) {
+  const Geo g = make_geo(shape, s);
+  const uint64_t quads = static_cast<uint64_t>((s + 3) / 4);
+  const FastDiv64 qd = make_div64(quads);
+  const int64_t work = (g.n_tiles * static_cast<int64_t>(quads) + 255) / 256;
+  TT_RANK_SWITCH(g.rank, RK, {
+    const int grid = grid_for(c, (const void*)clean_kernel<RK>, 256, 0, work);
+    clean_kernel<RK><<<grid, 256, 0, c.stream>>>(g, in, out, qd);
+  });
+  post_launch(c, "clean_unknowns kernel");
+}
+
+void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shape& a,
+                        const Shape& b, int64_t s, const double* ta, const double* tb,
+                        double* tout) {
+  EwParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.rank = out.rank();
+  p.s = s;
+  p.n_tiles = out.tile_count();
+  const auto eo = out.external();
+  const auto ea = a.external();
+  const auto eb = b.external();
+  const auto sa = row_major_strides(ea);
+  const auto sb = row_major_strides(eb);
+  for (int i = 0; i < p.rank; ++i) {
+    p.ediv[i] = make_div32(static_cast<uint32_t>(eo[i]));
+    // l mod e_a is l when e_a == e_out and 0 when e_a == 1 (the only cases
+    // compatible shapes allow, shape.hpp:306-308).
+    p.a_stride[i] = ea[i] == 1 ? 0 : sa[i];
+    p.b_stride[i] = eb[i] == 1 ? 0 : sb[i];
+  }
+  if (p.n_tiles == 0) return;
+  const uint64_t quads = static_cast<uint64_t>((s + 3) / 4);
+  const FastDiv64 qd = make_div64(quads);
+  const bool vec = (s % 2 == 0) && aligned16(ta) && aligned16(tb) && aligned16(tout);
+  const int64_t work = (p.n_tiles * static_cast<int64_t>(quads) + 255) / 256;
+#define TT_EW(OPV, VECV)                                                                  \
+  {                                                                                       \
+    const int grid = grid_for(c, (const void*)elementwise_kernel<OPV, VECV>, 256, 0, work); \
+    elementwise_kernel<OPV, VECV><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout, qd);       \
+  }
+  if (op == TT_OP_ADD) {
+    if (vec) TT_EW(TT_OP_ADD, true) else TT_EW(TT_OP_ADD, false)
+  } else {
+    if (vec) TT_EW(TT_OP_MUL, true) else TT_EW(TT_OP_MUL, false)
+  }
+#undef TT_EW
+  post_launch(c, "elementwise kernel");
+}
+
+void launch_binary_flat(const LaunchCtx& c, int op, const double* a, const double* b, double* out,
+                        int64_t count) {
+  if (count <= 0) return;
+  const int64_t work = (count + 255) / 256;
+  if (op == TT_OP_ADD) {
+    const int grid = grid_for(c, (const void*)binary_flat_kernel<TT_OP_ADD>, 256, 0, work);
+    binary_flat_kernel<TT_OP_ADD><<<grid, 256, 0, c.stream>>>(a, b, out, count);
+  } else {
+    const int grid = grid_for(c, (const void*)binary_flat_kernel<TT_OP_MUL>, 256, 0, work);
+    binary_flat_kernel<TT_OP_MUL><<<grid, 256, 0, c.stream>>>(a, b, out, count);
+  }
+  post_launch(c, "binary kernel");
+}
+
+void launch_rotate(const LaunchCtx& c, const double* in, double* out, int64_t s, int64_t r,
+                   int64_t n_tiles) {
+  const uint64_t total = static_cast<uint64_t>(s) * n_tiles;
+  if (total == 0) return;
+  const int grid = grid_for(c, (const void*)rotate_kernel, 256, 0, (total + 255) / 256);
+  rotate_kernel<<<grid, 256, 0, c.stream>>>(in, out, s, r, total, make_div64(s));
+  post_launch(c, "rotate kernel");
+}
+
+void launch_fill_uniform(const LaunchCtx& c, double* out, int64_t count, uint64_t seed,
+                         int64_t offset, double lo, double hi) {
+  if (count <= 0) return;
+  const int grid = grid_for(c, (const void*)fill_uniform_kernel, 256, 0, (count + 255) / 256);
+  fill_uniform_kernel<<<grid, 256, 0, c.stream>>>(out, count, host_splitmix64(seed), offset, lo,
+                                                  hi - lo);
+  post_launch(c, "fill kernel");
+}
+
+namespace {
+
+GroupParams make_group_params(const Program& prog, const GroupSpec& g, int64_t s) {
+  GroupParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.g = g;
+  for (int i = 0; i < g.nd; ++i) p.gdiv[i] = make_div64(static_cast<uint64_t>(g.ext[i]));
+  p.s = s;
+  p.nops = static_cast<int>(prog.ops.size());
+  p.nbuf = prog.nbuf;
+  for (size_t i = 0; i < prog.ops.size(); ++i) p.ops[i] = prog.ops[i];
+  return p;
+}
+
+template <bool HAS_B>
+void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
+                 double* tout) {
+  const int64_t s = p.s;
+  const uint64_t quads = static_cast<uint64_t>((s + 3) / 4);
+  const FastDiv64 qd = make_div64(quads);
+  const bool vec = (s % 2 == 0) && aligned16(ta) && (!HAS_B || aligned16(tb)) && aligned16(tout);
+  const int64_t work = (p.g.groups * static_cast<int64_t>(quads) + 255) / 256;
+  if (vec) {
+    const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, true>, 256, 0, work);
+    fold_kernel<HAS_B, true><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout, qd);
+  } else {
+    const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, false>, 256, 0, work);
+    fold_kernel<HAS_B, false><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout, qd);
+  }
+  post_launch(c, "fold kernel");
+}
+
+template <int VMAX, bool HAS_B, bool VEC>
+void run_pow2(const LaunchCtx& c, const GroupParams& p, int threads, size_t smem,
+              const double* ta, const double* tb, double* tout) {
+  auto k = group_pow2_kernel<VMAX, HAS_B, VEC>;
+  check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)),
+             "smem attribute");
+  const int grid = grid_for(c, (const void*)k, threads, smem, p.g.groups);
+  k<<<grid, threads, smem, c.stream>>>(p, ta, tb, tout);
+  post_launch(c, "group pow2 kernel");
+}
+
+template <bool HAS_B, bool VEC>
+void dispatch_pow2(const LaunchCtx& c, const GroupParams& p, int threads, int vmax, size_t smem,
+                   const double* ta, const double* tb, double* tout) {
+  switch (vmax) {
+    case 1: run_pow2<1, HAS_B, VEC>(c, p, threads, smem, ta, tb, tout); break;
+    case 2: run_pow2<2, HAS_B, VEC>(c, p, threads, smem, ta, tb, tout); break;
+    case 4: run_pow2<4, HAS_B, VEC>(c, p, threads, smem, ta, tb, tout); break;
+    case 8: run_pow2<8, HAS_B, VEC>(c, p, threads, smem, ta, tb, tout); break;
+    case 16: run_pow2<16, HAS_B, VEC>(c, p, threads, smem, ta, tb, tout); break;
+    default: run_pow2<32, HAS_B, VEC>(c, p, threads, smem, ta, tb, tout); break;
+  }
+}
+
+template <bool HAS_B>
+void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
+                         const double* ta, const double* tb, double* tout) {
+  GroupParams p = make_group_params(prog, g, s);
+  if (g.groups == 0) return;
+  const size_t tile_bytes = static_cast<size_t>(s) * sizeof(double);
+  // 1) No in-tile schedule: the fold is the whole program.
+  if (prog.ops.size() == 1 && prog.ops[0].kind == GOP_FOLD && prog.ops[0].dst == BUF_OUT) {
+    launch_fold<HAS_B>(c, p, ta, tb, tout);
+    return;
+  }
+  // 2) Fast path: fold + power-of-two rotate-and-sum in one pass.
+  const int threads = static_cast<int>(std::min<int64_t>(512, ((s + 31) / 32) * 32));
+  const int64_t v_needed = (s + threads - 1) / threads;
+  if (prog.simple_pow2 && tile_bytes <= c.smem_optin && v_needed <= 32) {
+    int vmax = 1;
+    while (vmax < v_needed) vmax *= 2;
+    p.nlevels = static_cast<int>(prog.ops.size()) - 1;
+    for (int i = 0; i < p.nlevels; ++i) p.rots[i] = prog.ops[i + 1].x;
+    const bool vec = (s % 2 == 0) && aligned16(ta) && (!HAS_B || aligned16(tb));
+    // Too few groups to occupy every SM: fold over the whole grid first
+    // (phase 1, into OUT), then run the schedule on OUT in place (phase 2).
+    const int64_t per_sm = std::max<int64_t>(1, static_cast<int64_t>(c.smem_optin / (tile_bytes + 1024)));
+    if (g.groups < static_cast<int64_t>(c.sm_count) * std::min<int64_t>(per_sm, 4) &&
+        prog.ops[0].y > 1) {
+      launch_fold<HAS_B>(c, p, ta, tb, tout);
+      GroupParams p2 = p;
+      p2.g.nd = 1;
+      p2.g.ext[0] = g.groups;
+      p2.gdiv[0] = make_div64(static_cast<uint64_t>(g.groups));
+      p2.g.out_stride[0] = 0;
+      p2.g.a_stride[0] = 0;
+      p2.g.b_stride[0] = 0;
+      // phase 2 addresses its group's tile through `out`: remap so that
+      // out = a = original out tile index.
+      p2.g.nd = g.nd;
+      for (int i = 0; i < g.nd; ++i) {
+        p2.g.ext[i] = g.ext[i];
+        p2.gdiv[i] = p.gdiv[i];
+        p2.g.out_stride[i] = g.out_stride[i];
+        p2.g.a_stride[i] = g.out_stride[i];
+        p2.g.b_stride[i] = 0;
+      }
+      p2.g.astep = 0;
+      p2.g.bstep = 0;
+      p2.ops[0].x = 0;
+      p2.ops[0].y = 1;
+      const bool vec2 = (s % 2 == 0) && aligned16(tout);
+      if (vec2)
+        dispatch_pow2<false, true>(c, p2, threads, vmax, tile_bytes, tout, nullptr, tout);
+      else
+        dispatch_pow2<false, false>(c, p2, threads, vmax, tile_bytes, tout, nullptr, tout);
+      return;
+    }
+    if (vec)
+      dispatch_pow2<HAS_B, true>(c, p, threads, vmax, tile_bytes, ta, tb, tout);
+    else
+      dispatch_pow2<HAS_B, false>(c, p, threads, vmax, tile_bytes, ta, tb, tout);
+    return;
+  }
+  // 3) Generic interpreter.
+  const int gthreads = static_cast<int>(std::min<int64_t>(512, ((s + 31) / 32) * 32));
+  const size_t phys = static_cast<size_t>(prog.nbuf + 1) * tile_bytes;
+  if (prog.nbuf + 1 > 16) invalid_argument("reduction schedule needs too many scratch tiles");
+  double* scratch = nullptr;
+  size_t smem = 0;
+  auto k = group_generic_kernel<HAS_B>;
+  if (phys <= c.smem_optin) {
+    p.use_smem = 1;
+    smem = phys;
+    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)),
+               "smem attribute");
+  }
+  const int grid = grid_for(c, (const void*)k, gthreads, smem, g.groups);
+  if (!p.use_smem) scratch = c.scratch(c.scratch_owner, phys * static_cast<size_t>(grid));
+  k<<<grid, gthreads, smem, c.stream>>>(p, ta, tb, tout, scratch);
+  post_launch(c, "group generic kernel");
+}
+
+}  // namespace
+
+void launch_group_program(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
+                          const double* ta, const double* tb, double* tout) {
+  if (tb != nullptr)
+    launch_program_impl<true>(c, prog, g, s, ta, tb, tout);
+  else
+    launch_program_impl<false>(c, prog, g, s, ta, tb, tout);
+}
+
+}  // namespace ttb

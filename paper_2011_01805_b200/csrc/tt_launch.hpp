@@ -1,0 +1,64 @@
+// tt_launch.hpp -- host-side launch API of the sm_100a kernels (tt_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tt_internal.hpp"
+
+namespace ttb {
+
+struct LaunchCtx {
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int sm_count = 148;
+  size_t smem_optin = 227 * 1024;  // max dynamic smem per block
+  uint64_t* launches = nullptr;    // incremented per kernel launch
+  // Session-owned device scratch; (re)sized by the caller via `need`.
+  double* (*scratch)(void* owner, size_t bytes) = nullptr;
+  void* scratch_owner = nullptr;
+};
+
+// Group grid of a reduction: output tile ("group") g is addressed by
+// coordinates c_0..c_{nd-1} in iteration order (outermost first); its output
+// tile index and the operands' base tile indices are linear in c.  Along the
+// summed dim, operand tile indices advance by astep/bstep per fold step.
+struct GroupSpec {
+  int nd = 0;
+  int64_t ext[TT_MAX_RANK] = {};
+  int64_t out_stride[TT_MAX_RANK] = {};
+  int64_t a_stride[TT_MAX_RANK] = {};
+  int64_t b_stride[TT_MAX_RANK] = {};
+  int64_t astep = 0;
+  int64_t bstep = 0;
+  int64_t groups = 1;
+};
+
+void launch_pack(const LaunchCtx& c, const Shape& shape, int64_t s, const double* dense,
+                 double* tiles);
+void launch_unpack(const LaunchCtx& c, const Shape& shape, int64_t s, const double* tiles,
+                   double* dense);
+// out tile l = A[l mod ea] (op) B[l mod eb]   (tile_tensor.hpp:259-270)
+void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shape& a,
+                        const Shape& b, int64_t s, const double* ta, const double* tb,
+                        double* tout);
+// out[i] = a[i] (op) b[i] over `count` slots; op 2 = a * mask (same as mul)
+void launch_binary_flat(const LaunchCtx& c, int op, const double* a, const double* b, double* out,
+                        int64_t count);
+// out[t][j] = in[t][(j + r) mod s]   (backend.hpp:157-159), r in [1, s)
+void launch_rotate(const LaunchCtx& c, const double* in, double* out, int64_t s, int64_t r,
+                   int64_t n_tiles);
+// out = in * used-mask(shape)   (tile_tensor.hpp:364-380)
+void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const double* in,
+                  double* out);
+// Runs `prog` for every group of `g`; `tb` may be null (no fused multiply).
+void launch_group_program(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
+                          const double* ta, const double* tb, double* tout);
+// Synthetic input generator shared with oracle/tt_oracle.c or_fill_uniform.
+void launch_fill_uniform(const LaunchCtx& c, double* out, int64_t count, uint64_t seed,
+                         int64_t offset, double lo, double hi);
+
+void check_cuda(cudaError_t e, const char* what);
+
+}  // namespace ttb

@@ -1,0 +1,662 @@
+"""Python mirror of the reference tile-tensor API over the B200 C-ABI.
+
+Same names, argument meaning and error behaviour as the reference's
+``namespace tiletensor`` (/root/reference/proj/include/tiletensor/*.hpp), so
+tests read like the reference's own.  Every operator calls
+``libtiletensor_b200.so`` (include/tiletensor_b200.h) through ctypes; slot
+arithmetic runs only in the sm_100a kernels.  There is no CPU path: importing
+works without a GPU (the shape algebra is host code in the library), but
+creating a :class:`Session` raises :class:`NoDeviceError` when no CUDA device
+is present, and every op fails loudly if the native library is missing.
+
+Device memory is held in ``torch`` CUDA tensors (plumbing only): a
+:class:`TileTensor` owns one ``float64`` tensor of shape ``[tile_count, s]``.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import TT_MAX_RANK, CCost, CShape, lib
+
+# ---- errors (shape.hpp:21-35, backend.hpp:18-21) -------------------------------
+
+
+class ShapeError(RuntimeError):
+    pass
+
+
+class ShapeParseError(ShapeError):
+    def __init__(self, msg: str, position: int):
+        super().__init__(msg)
+        self._position = position
+
+    def position(self) -> int:
+        return self._position
+
+
+class DepthExhaustedError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class NoDeviceError(RuntimeError):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().tt_last_error().decode()
+    if rc == 1:
+        raise ShapeError(msg)
+    if rc == 2:
+        raise ShapeParseError(msg, int(lib().tt_last_error_position()))
+    if rc == 3:
+        raise DepthExhaustedError(msg)
+    if rc == 4:
+        raise ValueError(msg)  # std::invalid_argument
+    if rc == 5:
+        raise IndexError(msg)  # std::out_of_range
+    if rc == 7:
+        raise CudaError(msg)
+    if rc == 8:
+        raise NoDeviceError(msg)
+    raise RuntimeError(msg)
+
+
+# ---- shapes (shape.hpp:37-138) ---------------------------------------------------
+
+
+class OpKind(enum.IntEnum):
+    add = 0
+    mul = 1
+
+
+class SumVariant(enum.IntEnum):
+    left_to_right = 0
+    right_to_left = 1
+    power_of_two = 2
+
+
+@dataclass(frozen=True)
+class DimSpec:
+    n: int = 1
+    d: int = 1
+    t: int = 1
+    unknown: bool = False
+    interleaved: bool = False  # the builder's `~` extension
+
+    def used(self) -> int:
+        return self.n * self.d
+
+    def fully_replicated(self) -> bool:
+        return self.n == 1 and self.d == self.t
+
+
+def _ceil_div(a: int, b: int) -> int:
+    return (a + b - 1) // b
+
+
+class TileTensorShape:
+    """TileTensorShape shape.hpp:72-138 (validated by the native library)."""
+
+    __slots__ = ("_dims", "_relaxed")
+
+    def __init__(self, dims: Sequence[DimSpec], relaxed: bool = False):
+        self._dims = tuple(dims)
+        self._relaxed = bool(relaxed)
+        _check(lib().tt_shape_check(ctypes.byref(self.to_c())))
+
+    # construction helpers
+    def to_c(self) -> CShape:
+        c = CShape()
+        c.rank = len(self._dims)
+        c.relaxed = 1 if self._relaxed else 0
+        if c.rank > TT_MAX_RANK:
+            raise ShapeError(f"rank {c.rank} exceeds the supported maximum {TT_MAX_RANK}")
+        for i, d in enumerate(self._dims):
+            c.dims[i].n, c.dims[i].d, c.dims[i].t = d.n, d.d, d.t
+            c.dims[i].unknown = 1 if d.unknown else 0
+            c.dims[i].interleaved = 1 if d.interleaved else 0
+        return c
+
+    @classmethod
+    def from_c(cls, c: CShape) -> "TileTensorShape":
+        obj = cls.__new__(cls)
+        obj._dims = tuple(
+            DimSpec(c.dims[i].n, c.dims[i].d, c.dims[i].t, bool(c.dims[i].unknown),
+                    bool(c.dims[i].interleaved)) for i in range(c.rank))
+        obj._relaxed = bool(c.relaxed)
+        return obj
+
+    def rank(self) -> int:
+        return len(self._dims)
+
+    def dims(self) -> tuple:
+        return self._dims
+
+    def dim(self, i: int) -> DimSpec:
+        return self._dims[i]
+
+    def relaxed(self) -> bool:
+        return self._relaxed
+
+    def tile_slots(self) -> int:
+        p = 1
+        for d in self._dims:
+            p *= d.t
+        return p
+
+    def tensor_extents(self) -> list:
+        return [d.n for d in self._dims]
+
+    def external_extents(self) -> list:
+        return [_ceil_div(d.used(), d.t) for d in self._dims]
+
+    def tile_count(self) -> int:
+        p = 1
+        for e in self.external_extents():
+            p *= e
+        return p
+
+    def used_slots(self) -> int:
+        p = 1
+        for d in self._dims:
+            p *= d.used()
+        return p
+
+    def total_slots(self) -> int:
+        return self.tile_count() * self.tile_slots()
+
+    def has_unknown(self) -> bool:
+        return any(d.unknown for d in self._dims)
+
+    def with_dim(self, i: int, ds: DimSpec) -> "TileTensorShape":
+        dims = list(self._dims)
+        dims[i] = ds
+        return TileTensorShape(dims, self._relaxed)
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, TileTensorShape) and self._dims == other._dims
+                and self._relaxed == other._relaxed)
+
+    def __hash__(self):
+        return hash((self._dims, self._relaxed))
+
+    def __repr__(self) -> str:
+        return f"TileTensorShape({format_shape(self)}{', relaxed' if self._relaxed else ''})"
+
+
+def parse_shape(text: str) -> TileTensorShape:  # shape.hpp:250
+    c = CShape()
+    _check(lib().tt_shape_parse(text.encode(), ctypes.byref(c)))
+    return TileTensorShape.from_c(c)
+
+
+def format_shape(shape: TileTensorShape) -> str:  # shape.hpp:256
+    buf = ctypes.create_string_buffer(64 * TT_MAX_RANK + 64)
+    _check(lib().tt_shape_format(ctypes.byref(shape.to_c()), buf, len(buf)))
+    return buf.value.decode()
+
+
+def external_shape(shape: TileTensorShape) -> list:  # shape.hpp:280
+    return shape.external_extents()
+
+
+def elementwise_result_shape(a: TileTensorShape, b: TileTensorShape, op) -> TileTensorShape:
+    out = CShape()
+    _check(lib().tt_shape_elementwise_result(ctypes.byref(a.to_c()), ctypes.byref(b.to_c()),
+                                             int(op), ctypes.byref(out)))
+    return TileTensorShape.from_c(out)
+
+
+def sum_result_shape(shape: TileTensorShape, dim: int) -> TileTensorShape:
+    out = CShape()
+    _check(lib().tt_shape_sum_result(ctypes.byref(shape.to_c()), int(dim), ctypes.byref(out)))
+    return TileTensorShape.from_c(out)
+
+
+def logical_indices(shape: TileTensorShape, tile_index: Sequence[int], h: int) -> list:
+    if len(tile_index) != shape.rank():
+        raise ShapeError("tile index rank mismatch")
+    ti = (ctypes.c_int64 * TT_MAX_RANK)(*tile_index)
+    j = (ctypes.c_int64 * TT_MAX_RANK)()
+    _check(lib().tt_logical_indices(ctypes.byref(shape.to_c()), ti, int(h), j))
+    return [j[i] for i in range(shape.rank())]
+
+
+def slot_of(shape: TileTensorShape, j: Sequence[int]):
+    if len(j) != shape.rank():
+        raise ShapeError("logical index rank mismatch")
+    jj = (ctypes.c_int64 * TT_MAX_RANK)(*j)
+    l = (ctypes.c_int64 * TT_MAX_RANK)()
+    h = ctypes.c_int64()
+    _check(lib().tt_slot_of(ctypes.byref(shape.to_c()), jj, l, ctypes.byref(h)))
+    return [l[i] for i in range(shape.rank())], h.value
+
+
+def rotations_left_to_right(n: int) -> int:
+    return int(lib().tt_rotations_left_to_right(n))
+
+
+def rotations_right_to_left(n: int) -> int:
+    return int(lib().tt_rotations_right_to_left(n))
+
+
+# ---- cost report (backend.hpp:28-63) ---------------------------------------------
+
+
+@dataclass
+class CostReport:
+    additions: int = 0
+    multiplications: int = 0
+    mask_multiplications: int = 0
+    rotations: int = 0
+    bootstraps: int = 0
+    power_of_two_rotations: int = 0
+
+    def to_text(self, extended: bool = False) -> str:
+        out = (f"additions={self.additions}\nmultiplications={self.multiplications}\n"
+               f"mask_multiplications={self.mask_multiplications}\nrotations={self.rotations}\n"
+               f"bootstraps={self.bootstraps}\n")
+        if extended:
+            out += f"power_of_two_rotations={self.power_of_two_rotations}\n"
+        return out
+
+    def since(self, base: "CostReport") -> "CostReport":
+        return CostReport(*(getattr(self, f) - getattr(base, f) for f in _COST_FIELDS))
+
+    def total_ops(self) -> int:
+        return (self.additions + self.multiplications + self.mask_multiplications +
+                self.rotations + self.bootstraps)
+
+
+_COST_FIELDS = ("additions", "multiplications", "mask_multiplications", "rotations", "bootstraps",
+                "power_of_two_rotations")
+
+# ---- session ------------------------------------------------------------------------
+
+
+def _torch():
+    import torch  # plumbing: device memory + streams
+    return torch
+
+
+class Session:
+    """Session backend.hpp:83-204, bound to one CUDA device.
+
+    Ops run on torch's current stream of that device at call time, so they are
+    ordered with the torch allocations that hold their operands.
+    """
+
+    def __init__(self, slot_count: int, max_chain_index: int, device: int = 0):
+        self._ptr = ctypes.c_void_p()
+        _check(lib().tt_session_create(int(slot_count), int(max_chain_index), int(device),
+                                       ctypes.byref(self._ptr)))
+        self._slots = int(slot_count)
+        self._depth = int(max_chain_index)
+        self._device = int(device)
+
+    def __del__(self):
+        p = getattr(self, "_ptr", None)
+        if p and p.value:
+            try:
+                lib().tt_session_destroy(p)
+            except Exception:
+                pass
+            self._ptr = None
+
+    @property
+    def handle(self):
+        torch = _torch()
+        stream = torch.cuda.current_stream(self._device).cuda_stream
+        _check(lib().tt_session_set_stream(self._ptr, ctypes.c_void_p(stream)))
+        return self._ptr
+
+    def slot_count(self) -> int:
+        return self._slots
+
+    def max_chain_index(self) -> int:
+        return self._depth
+
+    def device(self):
+        return _torch().device("cuda", self._device)
+
+    def cost_report(self) -> CostReport:
+        c = CCost()
+        lib().tt_session_cost(self._ptr, ctypes.byref(c))
+        return CostReport(*(getattr(c, f) for f in _COST_FIELDS))
+
+    def reset_counters(self) -> None:
+        lib().tt_session_reset_counters(self._ptr)
+
+    def launches(self) -> int:
+        return int(lib().tt_session_launches(self._ptr))
+
+    def synchronize(self) -> None:
+        _torch().cuda.synchronize(self._device)
+
+    def count_bootstraps(self, n: int) -> None:
+        lib().tt_session_count_bootstraps(self._ptr, int(n))
+
+    # allocation helper
+    def empty_tiles(self, count: int):
+        torch = _torch()
+        return torch.empty((int(count), self._slots), dtype=torch.float64, device=self.device())
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _as_device(x, session: Session):
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=session.device(), dtype=torch.float64)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).to(
+            session.device())
+    return t.contiguous()
+
+
+# ---- tile tensors (tile_tensor.hpp:130-165) -------------------------------------------
+
+
+class TileTensor:
+    """Shape + one device array [tile_count, s] + Session + chain index."""
+
+    def __init__(self, shape: TileTensorShape, tiles, session: Session, chain: Optional[int] = None):
+        torch = _torch()
+        if not isinstance(tiles, torch.Tensor) or tiles.device.type != "cuda":
+            tiles = _as_device(tiles, session)
+        tiles = tiles.reshape(-1, session.slot_count()) if tiles.numel() else tiles.reshape(
+            0, session.slot_count())
+        if tiles.shape[0] != shape.tile_count():
+            raise ShapeError("tile count does not match external shape")
+        self._shape = shape
+        self._tiles = tiles.contiguous()
+        self._session = session
+        self._chain = session.max_chain_index() if chain is None else int(chain)
+
+    def shape(self) -> TileTensorShape:
+        return self._shape
+
+    def session(self) -> Session:
+        return self._session
+
+    def tile_count(self) -> int:
+        return self._shape.tile_count()
+
+    def data(self):
+        """The device array [tile_count, s] (torch float64)."""
+        return self._tiles
+
+    def tiles(self) -> np.ndarray:
+        """Host copy of every tile, [tile_count, s] (TileTensor::tiles)."""
+        return self._tiles.detach().cpu().numpy()
+
+    def tile_at(self, flat: int) -> np.ndarray:
+        return self._tiles[flat].detach().cpu().numpy()
+
+    def chain_index(self) -> int:
+        return self._chain
+
+
+def with_leading_unit_dim(t: TileTensor) -> TileTensor:  # tile_tensor.hpp:158-165
+    dims = [DimSpec()] + list(t.shape().dims())
+    return TileTensor(TileTensorShape(dims, t.shape().relaxed()), t.data(), t.session(),
+                      t.chain_index())
+
+
+def _same_session(a: TileTensor, b: TileTensor) -> Session:
+    if a.session() is not b.session():
+        raise ValueError("operands belong to different sessions")  # tile_tensor.hpp:245-246
+    return a.session()
+
+
+def pack(tensor, shape: TileTensorShape, session: Session) -> TileTensor:
+    """pack tile_tensor.hpp:167-220; `tensor` is a numpy array or torch tensor
+    whose element count equals prod(n_i) (reshaped like the reference)."""
+    arr = tensor
+    want = 1
+    for e in shape.tensor_extents():
+        want *= e
+    size = int(np.prod(arr.shape)) if hasattr(arr, "shape") else len(arr)
+    if shape.has_unknown():
+        raise ShapeError("pack target shape may not contain '?': " + format_shape(shape))
+    if size != want:
+        raise ShapeError(f"tensor of {size} values cannot pack into {format_shape(shape)}")
+    dense = _as_device(arr, session).reshape(-1)
+    out = session.empty_tiles(shape.tile_count())
+    _check(lib().tt_pack(session.handle, _ptr(dense), ctypes.byref(shape.to_c()), _ptr(out)))
+    return TileTensor(shape, out, session)
+
+
+def unpack_device(t: TileTensor):
+    """unpack onto the device (torch tensor of the shape's n_i)."""
+    torch = _torch()
+    s = t.session()
+    ext = t.shape().tensor_extents()
+    out = torch.empty(ext, dtype=torch.float64, device=s.device())
+    _check(lib().tt_unpack(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()), _ptr(out)))
+    return out
+
+
+def unpack(t: TileTensor) -> np.ndarray:
+    """unpack tile_tensor.hpp:222-242 -> host numpy array."""
+    return unpack_device(t).cpu().numpy()
+
+
+def tt_elementwise(a: TileTensor, b: TileTensor, op) -> TileTensor:
+    s = _same_session(a, b)
+    so = CShape()
+    chain = ctypes.c_int64()
+    res_shape = elementwise_result_shape(a.shape(), b.shape(), op)
+    out = s.empty_tiles(res_shape.tile_count())
+    _check(lib().tt_elementwise(s.handle, int(op), ctypes.byref(a.shape().to_c()), _ptr(a.data()),
+                                a.chain_index(), ctypes.byref(b.shape().to_c()), _ptr(b.data()),
+                                b.chain_index(), ctypes.byref(so), _ptr(out), ctypes.byref(chain)))
+    return TileTensor(TileTensorShape.from_c(so), out, s, chain.value)
+
+
+def tt_add(a: TileTensor, b: TileTensor) -> TileTensor:
+    return tt_elementwise(a, b, OpKind.add)
+
+
+def tt_mul(a: TileTensor, b: TileTensor) -> TileTensor:
+    return tt_elementwise(a, b, OpKind.mul)
+
+
+def _variant(v) -> int:
+    return -1 if v is None else int(v)
+
+
+def tt_sum(t: TileTensor, dim: int, variant: Optional[SumVariant] = None) -> TileTensor:
+    """tt_sum tile_tensor.hpp:286-347."""
+    s = t.session()
+    res_shape = sum_result_shape(t.shape(), dim)
+    out = s.empty_tiles(res_shape.tile_count())
+    so = CShape()
+    _check(lib().tt_sum(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()), int(dim),
+                        _variant(variant), ctypes.byref(so), _ptr(out)))
+    return TileTensor(TileTensorShape.from_c(so), out, s, t.chain_index())
+
+
+def tt_mul_sum(a: TileTensor, b: TileTensor, dim: int,
+               variant: Optional[SumVariant] = None) -> TileTensor:
+    """tt_sum(tt_mul(a, b), dim) fused: one pass, product never stored."""
+    s = _same_session(a, b)
+    prod = elementwise_result_shape(a.shape(), b.shape(), OpKind.mul)
+    res_shape = sum_result_shape(prod, dim)
+    out = s.empty_tiles(res_shape.tile_count())
+    so = CShape()
+    chain = ctypes.c_int64()
+    _check(lib().tt_mul_sum(s.handle, ctypes.byref(a.shape().to_c()), _ptr(a.data()),
+                            a.chain_index(), ctypes.byref(b.shape().to_c()), _ptr(b.data()),
+                            b.chain_index(), int(dim), _variant(variant), ctypes.byref(so),
+                            _ptr(out), ctypes.byref(chain)))
+    return TileTensor(TileTensorShape.from_c(so), out, s, chain.value)
+
+
+def _product(which: int, a: TileTensor, b: TileTensor, variant) -> TileTensor:
+    s = _same_session(a, b)
+    so = CShape()
+    chain = ctypes.c_int64()
+    # allocate from the worst case (the product's summed shape) after validation
+    try:
+        prod = elementwise_result_shape(a.shape(), b.shape(), OpKind.mul)
+        dim = 2 if which in (0, 2) else 1
+        n_out = sum_result_shape(prod, dim).tile_count()
+    except ShapeError:
+        n_out = 0
+    out = s.empty_tiles(max(n_out, 1))
+    _check(lib().tt_linalg_product(s.handle, which, ctypes.byref(a.shape().to_c()),
+                                   _ptr(a.data()), a.chain_index(),
+                                   ctypes.byref(b.shape().to_c()), _ptr(b.data()),
+                                   b.chain_index(), _variant(variant), ctypes.byref(so),
+                                   _ptr(out), ctypes.byref(chain)))
+    shape = TileTensorShape.from_c(so)
+    return TileTensor(shape, out[:shape.tile_count()], s, chain.value)
+
+
+def matvec_a(m: TileTensor, v: TileTensor, variant=None) -> TileTensor:  # linalg.hpp:41
+    return _product(0, m, v, variant)
+
+
+def matvec_b(m_transposed: TileTensor, v: TileTensor, variant=None) -> TileTensor:  # :49
+    return _product(1, m_transposed, v, variant)
+
+
+def matmul_a(m1: TileTensor, m2: TileTensor, variant=None) -> TileTensor:  # :57
+    return _product(2, m1, m2, variant)
+
+
+def matmul_b(m1_transposed: TileTensor, m2: TileTensor, variant=None) -> TileTensor:  # :66
+    return _product(3, m1_transposed, m2, variant)
+
+
+def clean_unknowns(t: TileTensor) -> TileTensor:  # tile_tensor.hpp:352-386
+    s = t.session()
+    out = s.empty_tiles(t.tile_count())
+    so = CShape()
+    chain = ctypes.c_int64()
+    _check(lib().tt_clean_unknowns(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()),
+                                   t.chain_index(), ctypes.byref(so), _ptr(out),
+                                   ctypes.byref(chain)))
+    return TileTensor(TileTensorShape.from_c(so), out, s, chain.value)
+
+
+def replicate_dim(t: TileTensor, dim: int) -> TileTensor:  # tile_tensor.hpp:391-420
+    s = t.session()
+    out = s.empty_tiles(t.tile_count())
+    so = CShape()
+    _check(lib().tt_replicate_dim(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()),
+                                  int(dim), ctypes.byref(so), _ptr(out)))
+    return TileTensor(TileTensorShape.from_c(so), out, s, t.chain_index())
+
+
+# ---- tile-level primitives over [n, s] device arrays (backend.hpp / rotate_sum.hpp) ----
+
+
+def _tiles_arg(session: Session, tiles):
+    t = _as_device(tiles, session)
+    return t.reshape(-1, session.slot_count())
+
+
+def tiles_rotate(session: Session, tiles, offset: int):
+    """Session::rotate backend.hpp:152-163 on every row of `tiles`."""
+    src = _tiles_arg(session, tiles)
+    out = session.empty_tiles(src.shape[0])
+    _check(lib().tt_tiles_rotate(session.handle, _ptr(src), int(offset), _ptr(out), src.shape[0]))
+    return out
+
+
+def tiles_binary(session: Session, op, a, b):
+    """Session::add / Session::mul backend.hpp:117-136 row by row."""
+    ta, tb = _tiles_arg(session, a), _tiles_arg(session, b)
+    out = session.empty_tiles(ta.shape[0])
+    _check(lib().tt_tiles_binary(session.handle, int(op), _ptr(ta), _ptr(tb), _ptr(out),
+                                 ta.shape[0], None, None, None))
+    return out
+
+
+def tiles_mask_mul(session: Session, a, mask):
+    """Session::mask_mul backend.hpp:138-148 (one mask row per tile)."""
+    ta, tm = _tiles_arg(session, a), _tiles_arg(session, mask)
+    if tm.shape != ta.shape:
+        raise ValueError("mask length does not match slot count")
+    out = session.empty_tiles(ta.shape[0])
+    _check(lib().tt_tiles_mask_mul(session.handle, _ptr(ta), _ptr(tm), _ptr(out), ta.shape[0],
+                                   None, None))
+    return out
+
+
+def sum_tile_strided(session: Session, tiles, n: int, stride: int, variant) -> object:
+    """sum_tile_strided rotate_sum.hpp:44-90 on every row."""
+    src = _tiles_arg(session, tiles)
+    out = session.empty_tiles(src.shape[0])
+    _check(lib().tt_sum_tile_strided(session.handle, _ptr(src), int(n), int(stride),
+                                     _variant(variant), _ptr(out), src.shape[0]))
+    return out
+
+
+def sum_tile_flat(session: Session, tiles, n: int, variant) -> object:  # rotate_sum.hpp:92
+    return sum_tile_strided(session, tiles, n, 1, variant)
+
+
+def sum_tile_dim(session: Session, tiles, tile_extents: Sequence[int], dim: int,
+                 variant: Optional[SumVariant] = None):
+    src = _tiles_arg(session, tiles)
+    out = session.empty_tiles(src.shape[0])
+    ext = (ctypes.c_int64 * len(tile_extents))(*tile_extents)
+    _check(lib().tt_sum_tile_dim(session.handle, _ptr(src), ext, len(tile_extents), int(dim),
+                                 _variant(variant), _ptr(out), src.shape[0]))
+    return out
+
+
+def replicate_tile_dim(session: Session, tiles, tile_extents: Sequence[int], dim: int):
+    src = _tiles_arg(session, tiles)
+    out = session.empty_tiles(src.shape[0])
+    ext = (ctypes.c_int64 * len(tile_extents))(*tile_extents)
+    _check(lib().tt_replicate_tile_dim(session.handle, _ptr(src), ext, len(tile_extents),
+                                       int(dim), _ptr(out), src.shape[0]))
+    return out
+
+
+def auto_variant(n: int) -> SumVariant:  # rotate_sum.hpp:99-101
+    return SumVariant.power_of_two if n > 0 and n & (n - 1) == 0 else SumVariant.right_to_left
+
+
+def fill_uniform(session: Session, out, seed: int, lo: float, hi: float, offset: int = 0):
+    """Device generator, bit-identical to oracle or_fill_uniform."""
+    _check(lib().tt_fill_uniform(session.handle, _ptr(out), out.numel(), ctypes.c_uint64(seed),
+                                 int(offset), float(lo), float(hi)))
+    return out
+
+
+def shard_plan(shape: TileTensorShape, shard_dim: int, world: int, rank: int):
+    """Block partition of external dim `shard_dim` (1-based): (begin, end, local shape)."""
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    out = CShape()
+    _check(lib().tt_shard_plan(ctypes.byref(shape.to_c()), int(shard_dim), int(world), int(rank),
+                               ctypes.byref(b), ctypes.byref(e), ctypes.byref(out)))
+    return b.value, e.value, TileTensorShape.from_c(out)
+
+
+def device_count() -> int:
+    n = ctypes.c_int()
+    lib().tt_device_count(ctypes.byref(n))
+    return n.value
+
+
+__all__ = [n for n in dir() if not n.startswith("_")]

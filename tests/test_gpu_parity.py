@@ -1,0 +1,284 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) vs the CPU oracle.
+
+Bit-exact for every slot of every tile (including '?' crossover garbage and
+replicas) and identical cost counters -- the bar of SURVEY 8(c).  Inputs are
+seeded; tile contents are random over ALL slots (not just packed data) so
+the kernels must reproduce the reference's full-tile semantics.
+"""
+import random
+
+import numpy as np
+import pytest
+
+import paper_2011_01805_b200 as tt
+from paper_2011_01805_b200 import DimSpec, TileTensor, TileTensorShape, parse_shape, format_shape
+from shapes import (fuzz_unknown_regions, partner_shape, random_pack_shape, random_tensor,
+                    used_mask)
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(x):
+    return np.ascontiguousarray(x, dtype=np.float64).view(np.uint64)
+
+
+def assert_bitwise(got, want, what=""):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    assert got.shape == want.shape, f"{what}: shape {got.shape} vs {want.shape}"
+    g, w = bits(got), bits(want)
+    if not np.array_equal(g, w):
+        idx = np.argwhere(g != w)
+        first = tuple(idx[0])
+        raise AssertionError(f"{what}: {len(idx)} slots differ, first at {first}: "
+                             f"{got[first]!r} vs {want[first]!r}")
+
+
+def same_cost(a: tt.CostReport, b) -> bool:
+    return (a.additions, a.multiplications, a.mask_multiplications, a.rotations,
+            a.power_of_two_rotations) == (b.additions, b.multiplications, b.mask_multiplications,
+                                          b.rotations, b.power_of_two_rotations)
+
+
+_SESSIONS = {}
+
+
+def session(s, depth=8):
+    key = (s, depth)
+    if key not in _SESSIONS:
+        _SESSIONS[key] = tt.Session(s, depth)
+    return _SESSIONS[key]
+
+
+def test_pack_unpack_random_shapes(gpu, oracle):
+    rng = random.Random(4004)
+    nrng = np.random.default_rng(4004)
+    for it in range(300):
+        s = rng.choice([8, 16, 32, 64])
+        S = session(s)
+        shape = random_pack_shape(rng, s, rng.randint(1, 4))
+        a = random_tensor(nrng, shape.tensor_extents())
+        t = tt.pack(a, shape, S)
+        assert_bitwise(t.tiles(), oracle.pack(a, shape, s), f"pack {format_shape(shape)}")
+        assert_bitwise(tt.unpack(t), a, f"unpack {format_shape(shape)}")
+
+
+def test_unpack_ignores_unused_slots(gpu, oracle):
+    rng = random.Random(71)
+    nrng = np.random.default_rng(71)
+    for it in range(100):
+        s = rng.choice([8, 16, 32, 64])
+        S = session(s)
+        shape = random_pack_shape(rng, s, rng.randint(1, 4))
+        a = random_tensor(nrng, shape.tensor_extents())
+        tiles = oracle.pack(a, shape, s)
+        # garbage everywhere outside the used box; replicas keep their values
+        garbage = ~used_mask(shape, s)
+        tiles[garbage] = nrng.uniform(-100, 100, size=int(garbage.sum()))
+        t = TileTensor(shape, tiles, S)
+        assert_bitwise(tt.unpack(t), a, f"unpack fuzzed {format_shape(shape)}")
+
+
+@pytest.mark.parametrize("op", [tt.OpKind.add, tt.OpKind.mul])
+def test_elementwise_random(gpu, oracle, op):
+    rng = random.Random(73 + int(op))
+    nrng = np.random.default_rng(73 + int(op))
+    done = 0
+    while done < 150:
+        s = 1 << rng.randint(2, 5)
+        S = session(s)
+        sa = random_pack_shape(rng, s, rng.randint(1, 3))
+        sb = partner_shape(rng, sa)
+        try:
+            want_shape = oracle.elementwise_result_shape(sa, sb, int(op))
+        except Exception:
+            with pytest.raises(tt.ShapeError):
+                tt.elementwise_result_shape(sa, sb, op)
+            continue
+        ta = nrng.uniform(-3, 3, size=(sa.tile_count(), s))
+        tb = nrng.uniform(-3, 3, size=(sb.tile_count(), s))
+        S.reset_counters()
+        got = tt.tt_elementwise(TileTensor(sa, ta, S), TileTensor(sb, tb, S), op)
+        ws, wt, wc = oracle.elementwise(int(op), sa, ta, sb, tb, s)
+        assert got.shape() == ws
+        assert_bitwise(got.tiles(), wt, f"ew {format_shape(sa)} {format_shape(sb)}")
+        assert same_cost(S.cost_report(), wc)
+        done += 1
+
+
+def test_sum_every_dim_every_variant(gpu, oracle):
+    rng = random.Random(89)
+    nrng = np.random.default_rng(89)
+    for it in range(120):
+        s = 1 << rng.randint(2, 6)
+        S = session(s)
+        rank = rng.randint(1, 3)
+        shape = random_pack_shape(rng, s, rank)
+        tiles = nrng.uniform(-5, 5, size=(shape.tile_count(), s))
+        T = TileTensor(shape, tiles, S)
+        for dim in range(1, rank + 1):
+            for variant in (None, tt.SumVariant.left_to_right, tt.SumVariant.right_to_left,
+                            tt.SumVariant.power_of_two):
+                v = -1 if variant is None else int(variant)
+                try:
+                    ws, wt, wc = oracle.sum(shape, tiles, s, dim, v)
+                except Exception:
+                    with pytest.raises(ValueError):
+                        tt.tt_sum(T, dim, variant)
+                    continue
+                S.reset_counters()
+                got = tt.tt_sum(T, dim, variant)
+                assert got.shape() == ws
+                assert_bitwise(got.tiles(), wt, f"sum {format_shape(shape)} dim {dim} v {v}")
+                assert same_cost(S.cost_report(), wc), (S.cost_report(), wc)
+
+
+def test_sum_boundary_split(gpu, oracle):
+    """'?' dims whose used extent is not a multiple of t (tile_tensor.hpp:302-343)."""
+    nrng = np.random.default_rng(97)
+    cases = ["[18?/8,1]", "[5/2,1?/4]", "[13?/4,3/2]", "[7?/8]", "[3,11?/4]", "[2/2,9?/4,1]",
+             "[1?/8]", "[29?/32]", "[6/2,5?/4]"]
+    for text in cases:
+        shape = parse_shape(text)
+        s = shape.tile_slots()
+        S = session(s)
+        tiles = nrng.uniform(-5, 5, size=(shape.tile_count(), s))
+        for dim in range(1, shape.rank() + 1):
+            for v in (-1, 0, 1):
+                ws, wt, wc = oracle.sum(shape, tiles, s, dim, v)
+                S.reset_counters()
+                got = tt.tt_sum(TileTensor(shape, tiles, S), dim,
+                                None if v < 0 else tt.SumVariant(v))
+                assert got.shape() == ws
+                assert_bitwise(got.tiles(), wt, f"split {text} dim {dim} v {v}")
+                assert same_cost(S.cost_report(), wc)
+
+
+def test_mul_sum_matches_composition(gpu, oracle):
+    """Fused tt_sum(tt_mul(a,b)) == the two-step oracle, incl. counters."""
+    rng = random.Random(6006)
+    nrng = np.random.default_rng(6006)
+    for s in (8, 16, 32):
+        S = session(s)
+        t1 = 1
+        while t1 <= s:
+            t2 = 1
+            while t1 * t2 <= s:
+                t3 = s // (t1 * t2)
+                a, b, c = rng.randint(1, 9), rng.randint(1, 9), rng.randint(1, 9)
+                forms = [
+                    (TileTensorShape([DimSpec(a, 1, t1), DimSpec(b, 1, t2), DimSpec(1, t3, t3)]),
+                     TileTensorShape([DimSpec(1, t1, t1), DimSpec(b, 1, t2), DimSpec(c, 1, t3)]), 2),
+                    (TileTensorShape([DimSpec(b, 1, t1), DimSpec(a, 1, t2), DimSpec(1, t3, t3)]),
+                     TileTensorShape([DimSpec(b, 1, t1), DimSpec(1, t2, t2), DimSpec(c, 1, t3)]), 1),
+                ]
+                for sa, sb, dim in forms:
+                    ta = nrng.uniform(-2, 2, size=(sa.tile_count(), s))
+                    tb = nrng.uniform(-2, 2, size=(sb.tile_count(), s))
+                    ws, wt, wc = oracle.mul_sum(sa, ta, sb, tb, s, dim)
+                    S.reset_counters()
+                    got = tt.tt_mul_sum(TileTensor(sa, ta, S), TileTensor(sb, tb, S), dim)
+                    assert got.shape() == ws
+                    assert_bitwise(got.tiles(), wt, f"mulsum {format_shape(sa)}x{format_shape(sb)}")
+                    assert same_cost(S.cost_report(), wc)
+                t2 *= 2
+            t1 *= 2
+
+
+def test_clean_and_replicate(gpu, oracle):
+    nrng = np.random.default_rng(107)
+    for text, s in [("[5/2,1?/4]", 8), ("[18?/8,4/16]", 128), ("[3?/4,2/2,7?/4]", 32),
+                    ("[1?/8,3/4]", 32)]:
+        shape = parse_shape(text)
+        S = session(s)
+        tiles = nrng.uniform(-5, 5, size=(shape.tile_count(), s))
+        ws, wt, wc = oracle.clean_unknowns(shape, tiles, s)
+        S.reset_counters()
+        got = tt.clean_unknowns(TileTensor(shape, tiles, S))
+        assert got.shape() == ws
+        assert_bitwise(got.tiles(), wt, f"clean {text}")
+        assert same_cost(S.cost_report(), wc)
+        assert got.chain_index() == S.max_chain_index() - 1
+    for text, s, dim in [("[5/2,1/4]", 8, 2), ("[7/4,1/8]", 32, 2), ("[1/8,3/4]", 32, 1),
+                         ("[3/2,1/6,2/2]", 24, 2), ("[4,1/16,5/32]", 512, 2)]:
+        shape = parse_shape(text)
+        S = session(s)
+        tiles = nrng.uniform(-5, 5, size=(shape.tile_count(), s))
+        ws, wt, wc = oracle.replicate_dim(shape, tiles, s, dim)
+        S.reset_counters()
+        got = tt.replicate_dim(TileTensor(shape, tiles, S), dim)
+        assert got.shape() == ws
+        assert_bitwise(got.tiles(), wt, f"replicate {text}")
+        assert same_cost(S.cost_report(), wc)
+
+
+def test_tile_primitives(gpu, oracle):
+    nrng = np.random.default_rng(41)
+    for s in (16, 64, 256, 4096):
+        S = session(s, 2)
+        tile = nrng.integers(-50, 51, size=s).astype(np.float64)
+        for n in sorted({1, 2, 3, 7, s // 2, s, min(s, 1190)} | {int(x) for x in nrng.integers(1, s + 1, 6)}):
+            for v in (0, 1, 2):
+                if v == 2 and n & (n - 1):
+                    with pytest.raises(ValueError):
+                        tt.sum_tile_flat(S, tile, n, tt.SumVariant(v))
+                    continue
+                want, wc = oracle.sum_tile_strided(tile, n, 1, v)
+                S.reset_counters()
+                got = tt.sum_tile_flat(S, tile, n, tt.SumVariant(v)).cpu().numpy()[0]
+                assert_bitwise(got, want, f"flat sum s={s} n={n} v={v}")
+                assert same_cost(S.cost_report(), wc)
+        for off in (1, -1, 5, s - 1, 3 * s + 2, -8 * s):
+            want, wc = oracle.rotate(tile, off)
+            S.reset_counters()
+            got = tt.tiles_rotate(S, tile, off).cpu().numpy()[0]
+            assert_bitwise(got, want, f"rotate {off}")
+            assert same_cost(S.cost_report(), wc)
+
+
+def test_kat_backend_rotate(gpu):
+    """tests/test_backend.cpp:32-45 (reference KAT)."""
+    S = tt.Session(4, 3)
+    t = np.array([1.0, 2, 3, 4])
+    assert list(tt.tiles_rotate(S, t, 1).cpu().numpy()[0]) == [2, 3, 4, 1]
+    assert list(tt.tiles_rotate(S, t, -1).cpu().numpy()[0]) == [4, 1, 2, 3]
+    assert list(tt.tiles_rotate(S, t, 5).cpu().numpy()[0]) == [2, 3, 4, 1]
+    assert S.cost_report().rotations == 3
+    for off in (0, 4, -8):
+        assert list(tt.tiles_rotate(S, t, off).cpu().numpy()[0]) == [1, 2, 3, 4]
+    assert S.cost_report().rotations == 3
+
+
+def test_kat_pack_figures(gpu):
+    """tests/test_tile_tensor.cpp:152-181 (reference KAT)."""
+    S = tt.Session(8, 4)
+    v = np.array([1.0, 2, 3, 4, 5])
+    tv = tt.pack(v, parse_shape("[5/2,*/4]"), S)
+    assert tv.tile_count() == 3
+    assert tv.tiles().tolist() == [[1, 1, 1, 1, 2, 2, 2, 2], [3, 3, 3, 3, 4, 4, 4, 4],
+                                   [5, 5, 5, 5, 0, 0, 0, 0]]
+    assert tt.pack(v, parse_shape("[5/2,*3/4]"), S).tile_at(0).tolist() == [1, 1, 1, 0, 2, 2, 2, 0]
+    with pytest.raises(tt.ShapeError):
+        tt.pack(v, parse_shape("[5/2,1?/4]"), S)
+    with pytest.raises(tt.ShapeError):
+        tt.pack(v, parse_shape("[5/2]"), S)
+    with pytest.raises(tt.ShapeError):
+        tt.pack(np.zeros(6), parse_shape("[5/2,*/4]"), S)
+
+
+def test_kat_small_summation(gpu):
+    """tests/test_tile_tensor.cpp:500-507."""
+    S = tt.Session(4, 4)
+    ta = tt.pack(np.array([[1.0, 2], [3, 4]]), parse_shape("[2/2,2/2]"), S)
+    r = tt.tt_sum(ta, 2)
+    assert format_shape(r.shape()) == "[2/2,1?/2]"
+    assert tt.unpack(r).tolist() == [[3.0], [7.0]]
+
+
+def test_depth_exhaustion(gpu):
+    """tests/test_tile_tensor.cpp:478-485."""
+    S = tt.Session(4, 1)
+    ta = tt.pack(np.array([[1.0, 2], [3, 4]]), parse_shape("[2/2,2/2]"), S)
+    sq = tt.tt_mul(ta, ta)
+    with pytest.raises(tt.DepthExhaustedError):
+        tt.tt_mul(sq, sq)
