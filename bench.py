@@ -1,0 +1,459 @@
+"""Benchmark of the B200 tile-tensor hot path (driver contract: one JSON line).
+
+Workload (BASELINE.json config 5, the throughput sweep):
+  X = [2048/16,2048/32,512/32] (131072 tiles x 16384 fp64 slots, 16 GiB),
+  W = [*/16,2048/32,512/32] (replicated along dim 1, 1024 tiles, 128 MiB).
+  One step = tt_sum(tt_mul(X, W), k) for k = 1, 2, 3 in turn, each ONE fused
+  sm_100a launch (external left fold + in-tile rotate-and-sum, product never
+  stored).  value = streamed tile-slots per second = 3 * 2^31 per step per rank.
+
+Weak scaling (one process per GPU): rank r owns external tiles
+[128r, 128r+128) of dim 1 of a global [N*2048, 2048, 512] tensor (its own
+seeded slab); sums over dims 2 and 3 need no communication, the sum over
+dim 1 spans ranks and finishes with one NCCL all-reduce of the 128 MiB
+partial result.
+
+Inputs (16 GiB) exceed the 126 MB L2, so no flush is needed between steps.
+Timing: CUDA events on the launching stream, barrier + synchronize around the
+K timed steps, max over ranks.  `e2e` repeats the step through the public
+API from pinned HOST buffers (H2D of the dense input, pack, the three fused
+products, unpack, D2H of the results).  `--impl reference` times the
+reference's own CPU implementation (oracle/_ref, else the C restatement) on
+a bounded slab of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "tile-slots/sec and HBM GB/s (fraction of peak) for pack, mul+rotate-sum, matmul"
+S5 = 16384
+X_TILES = 131072
+W_TILES = 1024
+OUT_TILES = {1: 1024, 2: 2048, 3: 8192}
+GIB = 1 << 30
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_summary():
+    """Per-launch DRAM bytes from the committed ncu --set full summary, if any."""
+    for p in sorted((ROOT / "profiles").glob("r*_ncu_summary.json"), reverse=True):
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            continue
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- distributed plumbing -------------------------------------------------------------
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def init_dist(world, backend):
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return dist if world > 1 else None
+
+
+def max_over_ranks(x: float, dist, device) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---- CPU baseline (reference) ----------------------------------------------------------
+
+
+def cpu_slab_pipeline(slab_tiles: int, threads: int):
+    """Reference CPU path on X[0:16*slab_tiles] (+W): pack, tt_sum(tt_mul) per dim,
+    unpack.  Returns (kind, seconds dict, streamed tile-slots)."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2011_01805_b200 import configs, parse_shape
+    from paper_2011_01805_b200.tiletensor import DimSpec, TileTensorShape
+
+    rows = 16 * slab_tiles
+    x = np.ascontiguousarray(configs.c5_x_slab(slice(0, rows)))
+    w = np.ascontiguousarray(configs.c5_w())
+    sx = TileTensorShape([DimSpec(rows, 1, 16), DimSpec(2048, 1, 32), DimSpec(512, 1, 32)])
+    sw = parse_shape(configs.C5_W_SHAPE)
+    streamed = 3 * sx.tile_count() * S5
+    ref_lib = ROOT / "oracle" / "_ref" / "libttref.so"
+    if ref_lib.exists():
+        lib = ctypes.CDLL(str(ref_lib))
+        lib.ref_set_threads(int(threads))
+        dims = (ctypes.c_int * 3)(1, 2, 3)
+        secs = (ctypes.c_double * 4)()
+        dp = ctypes.POINTER(ctypes.c_double)
+        rc = lib.ref_bench_pipeline(x.ctypes.data_as(dp), ctypes.byref(sx.to_c()),
+                                    w.ctypes.data_as(dp), ctypes.byref(sw.to_c()),
+                                    ctypes.c_int64(S5), dims, 3, secs)
+        if rc != 0:
+            raise RuntimeError("reference pipeline failed")
+        return ("reference", int(lib.ref_thread_hint()),
+                {"pack": secs[0], "mul_sum": secs[1], "unpack": secs[2]}, streamed)
+    # fall back to the C restatement (single-threaded port)
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import Oracle
+    o = Oracle()
+    t0 = time.perf_counter()
+    tx = o.pack(x, sx, S5)
+    tw = o.pack(w, sw, S5)
+    t1 = time.perf_counter()
+    outs = [o.mul_sum(sx, tx, sw, tw, S5, k) for k in (1, 2, 3)]
+    t2 = time.perf_counter()
+    for so, ot, _ in outs:
+        o.unpack(so, S5, ot)
+    t3 = time.perf_counter()
+    return ("port", 1, {"pack": t1 - t0, "mul_sum": t2 - t1, "unpack": t3 - t2}, streamed)
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if world > 1 and rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    threads = min(64, os.cpu_count() or 1)
+    slab = args.ref_slab_tiles
+    for _ in range(args.warmup):
+        cpu_slab_pipeline(slab, threads)
+    times = []
+    kind, cores, streamed = "reference", threads, 0
+    for _ in range(args.steps):
+        kind, cores, secs, streamed = cpu_slab_pipeline(slab, threads)
+        times.append(secs["pack"] + secs["mul_sum"] + secs["unpack"])
+    total = sum(times)
+    value = streamed * len(times) / total
+    sample = (f"config-5 slab X[0:{16 * slab}] ({slab * 64 * 16} of 131072 tiles) + W: "
+              "pack, tt_sum(tt_mul(X,W),k) k=1,2,3, unpack, per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tile-slots/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 U[-1,1])",
+        "config": {"workload": "c5 [2048/16,2048/32,512/32] x [*/16,2048/32,512/32], sum dims 1,2,3 (CPU slab)",
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "tile-slots/s", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "tile-slots/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm ----------------------------------------------------------------------------
+
+
+def time_events(fn, reps, stream):
+    import torch
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(reps):
+        fn()
+    end.record(stream)
+    end.synchronize()
+    return start.elapsed_time(end) / 1e3 / reps
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2011_01805_b200 as tt
+    from paper_2011_01805_b200 import configs
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_dist(world, "nccl")
+    stream = torch.cuda.current_stream(dev)
+    hbm_peak, peak_src = peaks()
+
+    S = tt.Session(S5, 8, device=local)
+    sx = tt.parse_shape(configs.C5_X_SHAPE)
+    sw = tt.parse_shape(configs.C5_W_SHAPE)
+    # inputs generated on the device with the shared counter-based generator
+    x_dense = torch.empty(configs.C5_DIMS, dtype=torch.float64, device=dev)
+    w_dense = torch.empty((1, 2048, 512), dtype=torch.float64, device=dev)
+    rank_offset = rank * (2048 * 2048 * 512)
+    tt.fill_uniform(S, x_dense, configs.C5_SEED_X, -1.0, 1.0, offset=rank_offset)
+    tt.fill_uniform(S, w_dense, configs.C5_SEED_W, -1.0, 1.0)
+    X = tt.pack(x_dense, sx, S)
+    W = tt.pack(w_dense, sw, S)
+
+    def step():
+        outs = []
+        for k in (1, 2, 3):
+            r = tt.tt_mul_sum(X, W, k)
+            if k == 1 and dist is not None:
+                dist.all_reduce(r.data())  # dim 1 spans ranks: NCCL over NVLink
+            outs.append(r)
+        return outs
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+
+    # per-launch timing of the fused kernel (one launch per dim)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    per_dim = {1: [], 2: [], 3: []}
+    launches0 = S.launches()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for _ in range(args.steps):
+            ev[0].record(stream)
+            for k in (1, 2, 3):
+                r = tt.tt_mul_sum(X, W, k)
+                ev[k].record(stream)
+                if k == 1 and dist is not None:
+                    dist.all_reduce(r.data())
+            # the sync below is per step only to read the per-launch events
+            ev[3].synchronize()
+            per_dim[1].append(ev[0].elapsed_time(ev[1]) / 1e3)
+            per_dim[2].append(ev[1].elapsed_time(ev[2]) / 1e3)
+            per_dim[3].append(ev[2].elapsed_time(ev[3]) / 1e3)
+        t_end.record(stream)
+        t_end.synchronize()
+        elapsed = t_start.elapsed_time(t_end) / 1e3
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+    launches = S.launches() - launches0
+    elapsed_max = max_over_ranks(elapsed, dist, dev)
+    step_slots = 3 * X_TILES * S5
+    value = world * step_slots * args.steps / elapsed_max
+
+    # roofline of the dominant kernel (the fused group kernel, all three dims)
+    alg = {k: (X_TILES + W_TILES + OUT_TILES[k]) * S5 * 8 for k in (1, 2, 3)}
+    dur = {k: sum(v) / len(v) for k, v in per_dim.items()}
+    achieved = sum(alg.values()) / sum(dur.values()) / 1e9
+    traffic = traffic_summary()
+    tr = traffic.get("c5_mul_sum_bytes_per_launch")
+
+    ops = {}
+    for k in (1, 2, 3):
+        gbs = alg[k] / dur[k] / 1e9
+        ops[f"mul_sum_dim{k}"] = {"ms": dur[k] * 1e3, "GB/s": gbs, "frac": gbs / hbm_peak,
+                                  "frac_of_8TBps": gbs / 8000.0,
+                                  "tile_slots_per_s": X_TILES * S5 / dur[k],
+                                  "alg_bytes": alg[k]}
+
+    # pack (dense -> tiles), same tensor
+    if not args.skip_extra:
+        t = time_events(lambda: tt.pack(x_dense, sx, S), max(1, args.steps), stream)
+        pb = 2 * X_TILES * S5 * 8
+        ops["pack"] = {"ms": t * 1e3, "GB/s": pb / t / 1e9, "frac": pb / t / 1e9 / hbm_peak,
+                       "frac_of_8TBps": pb / t / 1e12 / 8.0, "tile_slots_per_s": X_TILES * S5 / t,
+                       "alg_bytes": pb}
+        del t
+        ops.update(bench_matmul(tt, configs, S, stream, hbm_peak, max(3, args.steps)))
+
+    # end to end from pinned host memory through the public API
+    e2e = None
+    if not args.skip_e2e:
+        host_x = x_dense.to("cpu").pin_memory() if args.e2e_pinned else x_dense.to("cpu")
+        host_w = w_dense.to("cpu").pin_memory()
+        del x_dense
+        torch.cuda.empty_cache()
+
+        def e2e_step():
+            Xh = tt.pack(host_x, sx, S)   # H2D of the dense input + pack kernel
+            Wh = tt.pack(host_w, sw, S)
+            d2h = 0
+            for k in (1, 2, 3):
+                r = tt.tt_mul_sum(Xh, Wh, k)
+                if k == 1 and dist is not None:
+                    dist.all_reduce(r.data())
+                res = tt.unpack(r)          # unpack kernel + D2H
+                d2h += res.nbytes
+            return d2h
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        reps = max(1, min(args.steps, args.e2e_steps))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            d2h = e2e_step()
+        torch.cuda.synchronize(dev)
+        e_el = max_over_ranks((time.perf_counter() - t0) / reps, dist, dev)
+        h2d = host_x.numel() * 8 + host_w.numel() * 8
+        e2e = {"value": world * step_slots / e_el, "unit": "tile-slots/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e_el * 1e3, "steps": reps, "host_buffers": "pinned" if args.e2e_pinned else "pageable"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        threads = min(64, os.cpu_count() or 1)
+        kind, cores, secs, streamed = cpu_slab_pipeline(args.cpu_slab_tiles, threads)
+        cpu = {"value": streamed / secs["mul_sum"], "unit": "tile-slots/s", "cores": cores,
+               "kind": kind,
+               "sample": (f"reference tt_sum(tt_mul(X,W),k) k=1,2,3 on the config-5 slab "
+                          f"X[0:{16 * args.cpu_slab_tiles}] ({args.cpu_slab_tiles * 1024} tiles), "
+                          f"{secs['mul_sum']:.2f} s; pack {secs['pack']:.2f} s, "
+                          f"unpack {secs['unpack']:.2f} s")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tile-slots/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded splitmix64 U[-1,1] generated on device; 16 GiB input > 126 MB L2 (no flush needed)",
+            "config": {"workload": "c5: tt_sum(tt_mul(X[2048/16,2048/32,512/32], W[*/16,2048/32,512/32]), k) for k=1,2,3",
+                       "slots": S5, "x_tiles_per_rank": X_TILES, "global_x": [2048 * world, 2048, 512],
+                       "parallelism": f"shard external dim 1 over {world} rank(s); NCCL all-reduce for the dim-1 sum",
+                       "l2": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "frac_of_8TBps": achieved / 8000.0,
+                         "peak_source": peak_src, "traffic": tr,
+                         "kernel": "group_pow2_kernel (fused fold + rotate-and-sum)",
+                         "alg_bytes_per_step": sum(alg.values())},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "ops": ops,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bench_matmul(tt, configs, S, stream, hbm_peak, reps):
+    """Config 3 ('3b': matmul_b then matmul_a, no repacking) on 8192-slot tiles."""
+    import torch
+    c3 = configs.config3()
+    S3 = tt.Session(8192, 8, device=torch.cuda.current_device())
+    T = {k: tt.pack(c3.tensors[k], tt.parse_shape(v), S3) for k, v in c3.shapes.items()
+         if k in ("A3", "Bt3", "C3")}
+
+    def chain():
+        s1 = tt.matmul_b(T["Bt3"], T["C3"])
+        return tt.matmul_a(T["A3"], s1)
+    chain()
+    torch.cuda.synchronize()
+    t = time_events(chain, reps, stream)
+    tile = 8192 * 8
+    # unique operand tiles + out tiles of both stages
+    alg = (1536 + 768 + 512 + 512 + 1024 + 512 + 512) * tile
+    prod_tiles = 24576 + 16384
+    return {"matmul_c3b": {"ms": t * 1e3, "GB/s": alg / t / 1e9, "frac": alg / t / 1e9 / hbm_peak,
+                           "tile_slots_per_s": prod_tiles * 8192 / t, "alg_bytes": alg,
+                           "note": "Bt3[768/16,1024/32,*/16] x C3[768/16,*/32,256/16] -> matmul_a(A3, .)"}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-extra", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-pinned", type=int, default=1)
+    ap.add_argument("--cpu-slab-tiles", type=int, default=8)
+    ap.add_argument("--ref-slab-tiles", type=int, default=2)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
