@@ -196,6 +196,14 @@ int tt_sum_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents
 int tt_replicate_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents, int rank,
                           int dim, double* out, int64_t n_tiles);     /* rotate_sum.hpp:128-152 */
 
+/* ---- diagnostics ------------------------------------------------------- */
+/* Force the reduction kernel path (tests / A-B measurement): 0 = best
+ * eligible (default), 1 = TMA-ring fused kernel, 2 = register-tree fused
+ * kernel, 3 = generic program interpreter.  Results are identical on every
+ * path; only speed differs. */
+int tt_set_kernel_path(int path);
+int tt_kernel_path(void);
+
 /* ---- sharding (north star item 5) -------------------------------------- */
 /* Block-partition external dim `shard_dim` (1-based) of `shape` over
  * `world` ranks; rank r owns external indices [*begin, *end).  Returns the

@@ -88,6 +88,8 @@ SIGNATURES = {
     "tt_sum_tile_strided": (_I, [_P, _P, _I64, _I64, _I, _P, _I64]),
     "tt_sum_tile_dim": (_I, [_P, _P, _I64P, _I, _I, _I, _P, _I64]),
     "tt_replicate_tile_dim": (_I, [_P, _P, _I64P, _I, _I, _P, _I64]),
+    "tt_set_kernel_path": (_I, [_I]),
+    "tt_kernel_path": (_I, []),
     "tt_shard_plan": (_I, [_SP, _I, _I, _I, _I64P, _I64P, _SP]),
 }
 

@@ -781,6 +781,17 @@ int tt_replicate_tile_dim(tt_session* s, const double* in, const int64_t* tile_e
   });
 }
 
+// ---- diagnostics --------------------------------------------------------------------
+
+int tt_set_kernel_path(int path) {
+  return guarded([&] {
+    if (path < 0 || path > 3) invalid_argument("kernel path must be 0..3");
+    set_kernel_path(path);
+  });
+}
+
+int tt_kernel_path(void) { return kernel_path(); }
+
 // ---- sharding ---------------------------------------------------------------------
 
 int tt_shard_plan(const tt_shape* shape, int shard_dim, int world, int rank, int64_t* begin,

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -116,6 +118,7 @@ struct Geo {
   int64_t estride[R];   // external (tile-index) stride of dim i
   int64_t dstride[R];   // dense stride of dim i, 0 when n_i == 1 (replication)
   int32_t inter[R];
+  int32_t quad_runs;
 };
 
 Geo make_geo(const Shape& sh, int64_t s) {
@@ -145,6 +148,8 @@ Geo make_geo(const Shape& sh, int64_t s) {
     g.dstride[i] = d.n == 1 ? 0 : ds[i];
     g.inter[i] = d.interleaved ? 1 : 0;
   }
+  const Dim& last = sh.dims[g.rank - 1];
+  g.quad_runs = (last.n > 1 && !last.interleaved && last.t % 4 == 0) ? 1 : 0;
   return g;
 }
 
@@ -182,37 +187,66 @@ __device__ __forceinline__ int64_t slot_source(const Geo& g, const uint32_t* l, 
 }
 
 // ---- pack ------------------------------------------------------------------------
-// One work item = 4 consecutive slots of one tile; a warp writes 1 KiB
-// contiguous with two 16-byte stores per lane, and gathers its sources in
-// runs of t_k contiguous dense elements.
+// A warp owns 256 consecutive slots of one tile; lane l fills the quads at
+// l*4 and 128 + l*4 (two 16-byte stores each, 1 KiB contiguous per warp
+// instruction).  When a quad's 4 sources are consecutive dense elements (the
+// common case: a run along the last dim) they are read with two 16-byte
+// loads, else slot by slot; padding slots are written as +0.0 without a read.
+
+template <int RK, bool VEC>
+__device__ __forceinline__ void pack_quad(const Geo& g, const uint32_t* l,
+                                          const double* __restrict__ dense, uint32_t h0,
+                                          double* out) {
+  double v[4];
+  const int64_t src0 = slot_source<RK>(g, l, h0);
+  // quad_runs (host): the last dim is a plain data dim (n > 1, not
+  // interleaved) with t % 4 == 0, so an aligned quad varies only along it and
+  // its sources are src0 .. src0+3 whenever the first and last are in range.
+  const bool run = VEC && g.quad_runs && h0 + 4 <= g.s && src0 >= 0 &&
+                   slot_source<RK>(g, l, h0 + 3) >= 0;
+  if (run && (src0 & 1) == 0) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(dense + src0));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(dense + src0) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  } else if (run) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldg(dense + src0 + k);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t src = k == 0 ? src0 : slot_source<RK>(g, l, h0 + k);
+      v[k] = src >= 0 ? __ldg(dense + src) : 0.0;
+    }
+  }
+  if (VEC && h0 + 4 <= g.s) {
+    reinterpret_cast<double2*>(out)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2*>(out)[1] = make_double2(v[2], v[3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (h0 + k < g.s) out[k] = v[k];
+  }
+}
 
 template <int RK, bool VEC>
 __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ Geo g,
                                                     const double* __restrict__ dense,
                                                     double* __restrict__ tiles,
-                                                    FastDiv64 quads_div) {
-  const uint64_t total = static_cast<uint64_t>(g.n_tiles) * quads_div.d;
-  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
-       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t flat = fdiv(w, quads_div);
-    const uint32_t h0 = static_cast<uint32_t>((w - flat * quads_div.d) * 4);
+                                                    FastDiv64 units_div) {
+  const uint64_t total = static_cast<uint64_t>(g.n_tiles) * units_div.d;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+       u < total; u += warps) {
+    const uint64_t flat = fdiv(u, units_div);
+    const uint32_t base = static_cast<uint32_t>((u - flat * units_div.d) * 256);
     uint32_t l[RK];
     tile_coords<RK>(g, static_cast<uint32_t>(flat), l);
-    double v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t src = slot_source<RK>(g, l, h0 + k);
-      v[k] = src >= 0 ? __ldg(dense + src) : 0.0;
-    }
-    double* out = tiles + flat * g.s + h0;
-    if (VEC && h0 + 4 <= g.s) {
-      reinterpret_cast<double2*>(out)[0] = make_double2(v[0], v[1]);
-      reinterpret_cast<double2*>(out)[1] = make_double2(v[2], v[3]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (h0 + k < g.s) out[k] = v[k];
-    }
+    double* tile = tiles + flat * g.s;
+    const uint32_t h0 = base + lane * 4;
+    const uint32_t h1 = h0 + 128;
+    if (h0 < g.s) pack_quad<RK, VEC>(g, l, dense, h0, tile + h0);
+    if (h1 < g.s) pack_quad<RK, VEC>(g, l, dense, h1, tile + h1);
   }
 }
 
@@ -473,6 +507,72 @@ __device__ __forceinline__ void fold_slots(const GroupParams& p, const GroupBase
   }
 }
 
+// FOLD for NP independent slot pairs at j0 + k*jstride (k < NP), all valid
+// and 16-byte aligned.  Each fold step issues NP (or 2*NP with a B operand)
+// independent 16-byte loads before any dependent arithmetic, so a thread
+// keeps NP*16 B (x2 with unroll) of HBM reads in flight -- the fold is
+// latency bound otherwise (one long-scoreboard stall per tile step).
+template <bool HAS_B, int NP>
+__device__ __forceinline__ void fold_pairs(const GroupParams& p, const GroupBase& gb,
+                                           const double* __restrict__ A,
+                                           const double* __restrict__ B, int64_t first,
+                                           int64_t count, int64_t j0, int64_t jstride,
+                                           double* dst, int64_t dst_stride) {
+  const int64_t s = p.s;
+  const double* pa = A + (gb.a + first * p.g.astep) * s + j0;
+  const int64_t sa = p.g.astep * s;
+  const double* pb = HAS_B ? B + (gb.b + first * p.g.bstep) * s + j0 : nullptr;
+  const int64_t sb = p.g.bstep * s;
+  double2 acc[NP];
+  double2 w[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(pa + k * jstride));
+    if (HAS_B) {
+      w[k] = __ldg(reinterpret_cast<const double2*>(pb + k * jstride));
+      acc[k] = make_double2(dmul(x.x, w[k].x), dmul(x.y, w[k].y));
+    } else {
+      acc[k] = x;
+    }
+  }
+  if (HAS_B && sb == 0) {  // B broadcast along the summed dim: its pairs stay in registers
+#pragma unroll 2
+    for (int64_t c = 1; c < count; ++c) {
+      double2 x[NP];
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        x[k] = __ldg(reinterpret_cast<const double2*>(pa + c * sa + k * jstride));
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        acc[k].x = dadd(acc[k].x, dmul(x[k].x, w[k].x));
+        acc[k].y = dadd(acc[k].y, dmul(x[k].y, w[k].y));
+      }
+    }
+  } else {
+#pragma unroll 2
+    for (int64_t c = 1; c < count; ++c) {
+      double2 x[NP], y[NP];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        x[k] = __ldg(reinterpret_cast<const double2*>(pa + c * sa + k * jstride));
+        if (HAS_B) y[k] = __ldg(reinterpret_cast<const double2*>(pb + c * sb + k * jstride));
+      }
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        if (HAS_B) {
+          acc[k].x = dadd(acc[k].x, dmul(x[k].x, y[k].x));
+          acc[k].y = dadd(acc[k].y, dmul(x[k].y, y[k].y));
+        } else {
+          acc[k].x = dadd(acc[k].x, x[k].x);
+          acc[k].y = dadd(acc[k].y, x[k].y);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) *reinterpret_cast<double2*>(dst + k * dst_stride) = acc[k];
+}
+
 // Fast path: FOLD into one shared tile, then `nlevels` in-place rotate-adds
 // (the power-of-two schedule, rotate_sum.hpp:51-56), the last into the output
 // tile.  Each thread owns slots j = i*T + tid; a level reads the partner
@@ -491,8 +591,15 @@ __global__ void __launch_bounds__(512, 1) group_pow2_kernel(const __grid_constan
   for (uint64_t v = blockIdx.x; v < static_cast<uint64_t>(p.g.groups); v += gridDim.x) {
     const GroupBase gb = group_base(p, v);
     if (VEC) {
-      for (int q = tid; 2 * q < s; q += T)
-        fold_slots<HAS_B, true>(p, gb, A, B, first, count, 2 * q, sbuf + 2 * q);
+      // pairs q = tid + i*T; batches of 4 pairs (i, i+1, i+2, i+3) per thread
+      // (2 pairs per batch when the tree's val[32] already claims 64 registers)
+      constexpr int NP = VMAX >= 32 ? 2 : 4;
+      const int npairs = s / 2;
+      int q = tid;
+      for (; q + (NP - 1) * T < npairs; q += NP * T)
+        fold_pairs<HAS_B, NP>(p, gb, A, B, first, count, 2 * q, 2 * T, sbuf + 2 * q, 2 * T);
+      for (; q < npairs; q += T)
+        fold_pairs<HAS_B, 1>(p, gb, A, B, first, count, 2 * q, 0, sbuf + 2 * q, 0);
     } else {
       for (int j = tid; j < s; j += T) fold_slots<HAS_B, false>(p, gb, A, B, first, count, j, sbuf + j);
     }
@@ -503,15 +610,24 @@ __global__ void __launch_bounds__(512, 1) group_pow2_kernel(const __grid_constan
       const int j = i * T + tid;
       if (j < s) val[i] = sbuf[j];
     }
+    const bool pow2_s = (s & (s - 1)) == 0;
     for (int lv = 0; lv < p.nlevels; ++lv) {
       const int r = static_cast<int>(p.rots[lv]);
+      if (pow2_s) {  // cyclic index by mask: no per-slot compare
+        const int mask = s - 1;
+        const int base = tid + r;
 #pragma unroll
-      for (int i = 0; i < VMAX; ++i) {
-        const int j = i * T + tid;
-        if (j < s) {
-          int jj = j + r;
-          if (jj >= s) jj -= s;
-          val[i] = dadd(val[i], sbuf[jj]);
+        for (int i = 0; i < VMAX; ++i)
+          if (i * T + tid < s) val[i] = dadd(val[i], sbuf[(base + i * T) & mask]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < VMAX; ++i) {
+          const int j = i * T + tid;
+          if (j < s) {
+            int jj = j + r;
+            if (jj >= s) jj -= s;
+            val[i] = dadd(val[i], sbuf[jj]);
+          }
         }
       }
       __syncthreads();
@@ -532,6 +648,207 @@ __global__ void __launch_bounds__(512, 1) group_pow2_kernel(const __grid_constan
     }
     // The last level's reads completed before its barrier, so the next
     // group's FOLD may overwrite sbuf without another barrier.
+  }
+}
+
+// ---- TMA-fed fused fold + power-of-two tree ---------------------------------------
+// The B200-native fast path.  One producer warp streams every fold operand
+// chunk (16 KiB of one tile, plus the matching chunk of B when B varies
+// along the summed dim) into a shared-memory ring with cp.async.bulk
+// (TMA bulk copies, SASS UBLKCP) completing on mbarriers; 16 consumer warps
+// fold each chunk from shared memory into registers and release the stage.
+// The ring keeps ~96 KiB of HBM reads in flight per SM independent of
+// register pressure, and the producer runs ahead into the next group while
+// the consumers execute the current group's rotate-and-sum tree.
+
+constexpr int kTmaConsumerWarps = 16;
+constexpr int kTmaConsumers = kTmaConsumerWarps * 32;
+constexpr int kTmaThreads = kTmaConsumers + 32;
+constexpr int kTmaPairsPerThread = 2;                         // per stage
+constexpr int kTmaChunk = 2 * kTmaConsumers * kTmaPairsPerThread;  // 2048 slots = 16 KiB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+}
+
+template <int VMAX, bool HAS_B>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    group_tma_kernel(const __grid_constant__ GroupParams p, const double* __restrict__ A,
+                     const double* __restrict__ B, double* __restrict__ OUT, int nstages) {
+  extern __shared__ __align__(128) double smem[];
+  const int s = static_cast<int>(p.s);
+  const bool b_stream = HAS_B && p.g.bstep != 0;
+  const int stage_doubles = kTmaChunk * (b_stream ? 2 : 1);
+  double* tile = smem;
+  double* ring = smem + s;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<int64_t>(nstages) * stage_doubles);
+  uint64_t* empty = full + nstages;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t first = p.ops[0].x;
+  const int64_t count = p.ops[0].y;
+  const int nchunks = s / kTmaChunk;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kTmaConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kTmaConsumerWarps) {  // ---- producer ----
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_first();  // streamed once
+      const uint64_t pol_b = policy_evict_last();   // shared by neighbouring groups
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t chunk_bytes = kTmaChunk * sizeof(double);
+      for (uint64_t v = blockIdx.x; v < static_cast<uint64_t>(p.g.groups); v += gridDim.x) {
+        const GroupBase gb = group_base(p, v);
+        for (int r = 0; r < nchunks; ++r) {
+          for (int64_t c = 0; c < count; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            double* dst = ring + static_cast<int64_t>(stage) * stage_doubles;
+            mbar_arrive_expect_tx(&full[stage], chunk_bytes * (b_stream ? 2 : 1));
+            const double* src = A + (gb.a + (first + c) * p.g.astep) * p.s + r * kTmaChunk;
+            bulk_g2s(dst, src, chunk_bytes, &full[stage], pol_a);
+            if (b_stream) {
+              const double* sb = B + (gb.b + (first + c) * p.g.bstep) * p.s + r * kTmaChunk;
+              bulk_g2s(dst + kTmaChunk, sb, chunk_bytes, &full[stage], pol_b);
+            }
+            if (++stage == nstages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  const int tid = threadIdx.x;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (uint64_t v = blockIdx.x; v < static_cast<uint64_t>(p.g.groups); v += gridDim.x) {
+    const GroupBase gb = group_base(p, v);
+    for (int r = 0; r < nchunks; ++r) {
+      double2 acc[kTmaPairsPerThread];
+      double2 w[kTmaPairsPerThread];
+      if (HAS_B && !b_stream) {  // B broadcast along the summed dim: one load per chunk
+        const double* pb = B + (gb.b + first * p.g.bstep) * p.s + r * kTmaChunk;
+#pragma unroll
+        for (int k = 0; k < kTmaPairsPerThread; ++k)
+          w[k] = __ldg(reinterpret_cast<const double2*>(pb) + tid + k * kTmaConsumers);
+      }
+      for (int64_t c = 0; c < count; ++c) {
+        mbar_wait(&full[stage], phase);
+        const double2* st = reinterpret_cast<const double2*>(ring + static_cast<int64_t>(stage) * stage_doubles);
+#pragma unroll
+        for (int k = 0; k < kTmaPairsPerThread; ++k) {
+          const double2 x = st[tid + k * kTmaConsumers];
+          double2 prod;
+          if (HAS_B) {
+            const double2 y = b_stream ? st[kTmaChunk / 2 + tid + k * kTmaConsumers] : w[k];
+            prod = make_double2(dmul(x.x, y.x), dmul(x.y, y.y));
+          } else {
+            prod = x;
+          }
+          if (c == 0) {
+            acc[k] = prod;
+          } else {
+            acc[k].x = dadd(acc[k].x, prod.x);
+            acc[k].y = dadd(acc[k].y, prod.y);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == nstages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      double2* dt = reinterpret_cast<double2*>(tile + r * kTmaChunk);
+#pragma unroll
+      for (int k = 0; k < kTmaPairsPerThread; ++k) dt[tid + k * kTmaConsumers] = acc[k];
+    }
+    consumer_sync();
+    // power-of-two rotate-and-sum on the folded tile (rotate_sum.hpp:51-56)
+    double val[VMAX];
+#pragma unroll
+    for (int i = 0; i < VMAX; ++i) {
+      const int j = i * kTmaConsumers + tid;
+      if (j < s) val[i] = tile[j];
+    }
+    const int mask = s - 1;  // s is a power of two on this path
+    for (int lv = 0; lv < p.nlevels; ++lv) {
+      const int base = tid + static_cast<int>(p.rots[lv]);
+#pragma unroll
+      for (int i = 0; i < VMAX; ++i)
+        if (i * kTmaConsumers + tid < s) val[i] = dadd(val[i], tile[(base + i * kTmaConsumers) & mask]);
+      consumer_sync();
+      if (lv + 1 < p.nlevels) {
+#pragma unroll
+        for (int i = 0; i < VMAX; ++i) {
+          const int j = i * kTmaConsumers + tid;
+          if (j < s) tile[j] = val[i];
+        }
+        consumer_sync();
+      }
+    }
+    double* out = OUT + gb.out * p.s;
+#pragma unroll
+    for (int i = 0; i < VMAX; ++i) {
+      const int j = i * kTmaConsumers + tid;
+      if (j < s) out[j] = val[i];
+    }
   }
 }
 
@@ -595,30 +912,47 @@ __global__ void __launch_bounds__(512) group_generic_kernel(const __grid_constan
   }
 }
 
-// Split fold: (group, 4-slot quad) work items over the whole grid, writing the
+// Split fold: the whole grid folds (group, chunk) work units and writes the
 // folded tile straight into OUT.  Used when a reduction has no in-tile
 // schedule (t == 1) or has too few groups to fill the GPU (phase 1 of 2).
+// VEC: a warp owns 128 slot pairs (256 slots) of one group; lane l folds the
+// pairs l, l+32, l+64, l+96 (fully coalesced 512-byte requests, 4 loads in
+// flight per operand).  Scalar mode: one slot per work item.
 template <bool HAS_B, bool VEC>
 __global__ void __launch_bounds__(256) fold_kernel(const __grid_constant__ GroupParams p,
                                                     const double* __restrict__ A,
                                                     const double* __restrict__ B,
                                                     double* __restrict__ OUT,
-                                                    FastDiv64 quads_div) {
-  const uint64_t total = static_cast<uint64_t>(p.g.groups) * quads_div.d;
+                                                    FastDiv64 units_div) {
   const int64_t first = p.ops[0].x;
   const int64_t count = p.ops[0].y;
-  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
-       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t v = fdiv(w, quads_div);
-    const int64_t j0 = static_cast<int64_t>(w - v * quads_div.d) * 4;
-    const GroupBase gb = group_base(p, v);
-    double* dst = OUT + gb.out * p.s;
-    if (VEC && j0 + 4 <= p.s) {
-      fold_slots<HAS_B, true>(p, gb, A, B, first, count, j0, dst + j0);
-      fold_slots<HAS_B, true>(p, gb, A, B, first, count, j0 + 2, dst + j0 + 2);
-    } else {
-      for (int k = 0; k < 4; ++k)
-        if (j0 + k < p.s) fold_slots<HAS_B, false>(p, gb, A, B, first, count, j0 + k, dst + j0 + k);
+  const int64_t s = p.s;
+  if (VEC) {
+    const uint64_t total = static_cast<uint64_t>(p.g.groups) * units_div.d;  // warp units
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+         u < total; u += warps) {
+      const uint64_t v = fdiv(u, units_div);
+      const int64_t q0 = static_cast<int64_t>(u - v * units_div.d) * 128;
+      const GroupBase gb = group_base(p, v);
+      double* dst = OUT + gb.out * s;
+      const int64_t npairs = s / 2;
+      if (q0 + 128 <= npairs) {
+        fold_pairs<HAS_B, 4>(p, gb, A, B, first, count, 2 * (q0 + lane), 64, dst + 2 * (q0 + lane), 64);
+      } else {
+        for (int64_t q = q0 + lane; q < npairs; q += 32)
+          fold_pairs<HAS_B, 1>(p, gb, A, B, first, count, 2 * q, 0, dst + 2 * q, 0);
+      }
+    }
+  } else {
+    const uint64_t total = static_cast<uint64_t>(p.g.groups) * units_div.d;  // slots
+    for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+      const uint64_t v = fdiv(w, units_div);
+      const int64_t j = static_cast<int64_t>(w - v * units_div.d);
+      const GroupBase gb = group_base(p, v);
+      fold_slots<HAS_B, false>(p, gb, A, B, first, count, j, OUT + gb.out * s + j);
     }
   }
 }
@@ -667,17 +1001,17 @@ void launch_pack(const LaunchCtx& c, const Shape& shape, int64_t s, const double
                  double* tiles) {
   const Geo g = make_geo(shape, s);
   if (g.n_tiles == 0) return;
-  const uint64_t quads = static_cast<uint64_t>((s + 3) / 4);
-  const FastDiv64 qd = make_div64(quads);
-  const int64_t work = (g.n_tiles * static_cast<int64_t>(quads) + 255) / 256;
-  const bool vec = (s % 2 == 0) && aligned16(tiles);
+  const uint64_t units = static_cast<uint64_t>((s + 255) / 256);
+  const FastDiv64 ud = make_div64(units);
+  const int64_t work = (g.n_tiles * static_cast<int64_t>(units) + 7) / 8;
+  const bool vec = (s % 2 == 0) && aligned16(tiles) && aligned16(dense);
   TT_RANK_SWITCH(g.rank, RK, {
     const void* k = vec ? (const void*)pack_kernel<RK, true> : (const void*)pack_kernel<RK, false>;
     const int grid = grid_for(c, k, 256, 0, work);
     if (vec)
-      pack_kernel<RK, true><<<grid, 256, 0, c.stream>>>(g, dense, tiles, qd);
+      pack_kernel<RK, true><<<grid, 256, 0, c.stream>>>(g, dense, tiles, ud);
     else
-      pack_kernel<RK, false><<<grid, 256, 0, c.stream>>>(g, dense, tiles, qd);
+      pack_kernel<RK, false><<<grid, 256, 0, c.stream>>>(g, dense, tiles, ud);
   });
   post_launch(c, "pack kernel");
 }
@@ -797,16 +1131,17 @@ template <bool HAS_B>
 void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
                  double* tout) {
   const int64_t s = p.s;
-  const uint64_t quads = static_cast<uint64_t>((s + 3) / 4);
-  const FastDiv64 qd = make_div64(quads);
   const bool vec = (s % 2 == 0) && aligned16(ta) && (!HAS_B || aligned16(tb)) && aligned16(tout);
-  const int64_t work = (p.g.groups * static_cast<int64_t>(quads) + 255) / 256;
   if (vec) {
+    const uint64_t units = static_cast<uint64_t>((s / 2 + 127) / 128);
+    const int64_t work = (p.g.groups * static_cast<int64_t>(units) + 7) / 8;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, true>, 256, 0, work);
-    fold_kernel<HAS_B, true><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout, qd);
+    fold_kernel<HAS_B, true><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout, make_div64(units));
   } else {
+    const int64_t work = (p.g.groups * s + 255) / 256;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, false>, 256, 0, work);
-    fold_kernel<HAS_B, false><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout, qd);
+    fold_kernel<HAS_B, false><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout,
+                                                           make_div64(static_cast<uint64_t>(s)));
   }
   post_launch(c, "fold kernel");
 }
@@ -836,6 +1171,54 @@ void dispatch_pow2(const LaunchCtx& c, const GroupParams& p, int threads, int vm
   }
 }
 
+template <int VMAX, bool HAS_B>
+void run_tma(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
+             double* tout) {
+  const bool b_stream = HAS_B && p.g.bstep != 0;
+  const size_t stage_bytes = static_cast<size_t>(kTmaChunk) * sizeof(double) * (b_stream ? 2 : 1);
+  const size_t tile_bytes = static_cast<size_t>(p.s) * sizeof(double);
+  const size_t avail = c.smem_optin - tile_bytes;
+  int nstages = static_cast<int>(avail / (stage_bytes + 16));
+  nstages = std::min(nstages, 12);
+  if (nstages < 2) invalid_argument("TMA path needs two ring stages");
+  const size_t smem = tile_bytes + nstages * (stage_bytes + 16);
+  auto k = group_tma_kernel<VMAX, HAS_B>;
+  check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)),
+             "smem attribute");
+  const int grid = grid_for(c, (const void*)k, kTmaThreads, smem, p.g.groups);
+  k<<<grid, kTmaThreads, smem, c.stream>>>(p, ta, tb, tout, nstages);
+  post_launch(c, "group tma kernel");
+}
+
+template <bool HAS_B>
+void dispatch_tma(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
+                  double* tout) {
+  const int64_t v = p.s / kTmaConsumers;
+  if (v <= 4)
+    run_tma<4, HAS_B>(c, p, ta, tb, tout);
+  else if (v <= 8)
+    run_tma<8, HAS_B>(c, p, ta, tb, tout);
+  else if (v <= 16)
+    run_tma<16, HAS_B>(c, p, ta, tb, tout);
+  else
+    run_tma<32, HAS_B>(c, p, ta, tb, tout);
+}
+
+// Kernel-path override for A/B measurement and tests (tt_set_kernel_path /
+// TT_KERNEL_PATH = tma | regs | generic); 0 = best eligible path.
+std::atomic<int> g_forced_path{-1};
+
+int forced_path() {
+  int v = g_forced_path.load(std::memory_order_relaxed);
+  if (v >= 0) return v;
+  const char* e = std::getenv("TT_KERNEL_PATH");
+  const std::string s(e ? e : "");
+  v = s == "tma" ? 1 : s == "regs" ? 2 : s == "generic" ? 3 : 0;
+  g_forced_path.store(v, std::memory_order_relaxed);
+  return v;
+}
+
 template <bool HAS_B>
 void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
                          const double* ta, const double* tb, double* tout) {
@@ -847,35 +1230,30 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
     launch_fold<HAS_B>(c, p, ta, tb, tout);
     return;
   }
-  // 2) Fast path: fold + power-of-two rotate-and-sum in one pass.
+  // 2) Fast paths: fold + power-of-two rotate-and-sum in one pass.
+  const int force = forced_path();
   const int threads = static_cast<int>(std::min<int64_t>(512, ((s + 31) / 32) * 32));
   const int64_t v_needed = (s + threads - 1) / threads;
-  if (prog.simple_pow2 && tile_bytes <= c.smem_optin && v_needed <= 32) {
+  const bool pow2_s = (s & (s - 1)) == 0;
+  if (prog.simple_pow2 && tile_bytes <= c.smem_optin && v_needed <= 32 && force != 3) {
     int vmax = 1;
     while (vmax < v_needed) vmax *= 2;
     p.nlevels = static_cast<int>(prog.ops.size()) - 1;
     for (int i = 0; i < p.nlevels; ++i) p.rots[i] = prog.ops[i + 1].x;
     const bool vec = (s % 2 == 0) && aligned16(ta) && (!HAS_B || aligned16(tb));
+    const bool tma_ok = pow2_s && s % kTmaChunk == 0 && s / kTmaConsumers <= 32 && aligned16(ta) &&
+                        (!HAS_B || aligned16(tb)) && aligned16(tout) &&
+                        tile_bytes + 2 * (2 * kTmaChunk * sizeof(double) + 16) <= c.smem_optin &&
+                        force != 2;
     // Too few groups to occupy every SM: fold over the whole grid first
     // (phase 1, into OUT), then run the schedule on OUT in place (phase 2).
     const int64_t per_sm = std::max<int64_t>(1, static_cast<int64_t>(c.smem_optin / (tile_bytes + 1024)));
     if (g.groups < static_cast<int64_t>(c.sm_count) * std::min<int64_t>(per_sm, 4) &&
         prog.ops[0].y > 1) {
       launch_fold<HAS_B>(c, p, ta, tb, tout);
+      // phase 2 reads its group's folded tile from OUT: a = out tile index
       GroupParams p2 = p;
-      p2.g.nd = 1;
-      p2.g.ext[0] = g.groups;
-      p2.gdiv[0] = make_div64(static_cast<uint64_t>(g.groups));
-      p2.g.out_stride[0] = 0;
-      p2.g.a_stride[0] = 0;
-      p2.g.b_stride[0] = 0;
-      // phase 2 addresses its group's tile through `out`: remap so that
-      // out = a = original out tile index.
-      p2.g.nd = g.nd;
       for (int i = 0; i < g.nd; ++i) {
-        p2.g.ext[i] = g.ext[i];
-        p2.gdiv[i] = p.gdiv[i];
-        p2.g.out_stride[i] = g.out_stride[i];
         p2.g.a_stride[i] = g.out_stride[i];
         p2.g.b_stride[i] = 0;
       }
@@ -883,14 +1261,17 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
       p2.g.bstep = 0;
       p2.ops[0].x = 0;
       p2.ops[0].y = 1;
-      const bool vec2 = (s % 2 == 0) && aligned16(tout);
-      if (vec2)
+      if (tma_ok)
+        dispatch_tma<false>(c, p2, tout, nullptr, tout);
+      else if (s % 2 == 0 && aligned16(tout))
         dispatch_pow2<false, true>(c, p2, threads, vmax, tile_bytes, tout, nullptr, tout);
       else
         dispatch_pow2<false, false>(c, p2, threads, vmax, tile_bytes, tout, nullptr, tout);
       return;
     }
-    if (vec)
+    if (tma_ok)
+      dispatch_tma<HAS_B>(c, p, ta, tb, tout);
+    else if (vec)
       dispatch_pow2<HAS_B, true>(c, p, threads, vmax, tile_bytes, ta, tb, tout);
     else
       dispatch_pow2<HAS_B, false>(c, p, threads, vmax, tile_bytes, ta, tb, tout);
@@ -917,6 +1298,9 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
 }
 
 }  // namespace
+
+void set_kernel_path(int path) { g_forced_path.store(path, std::memory_order_relaxed); }
+int kernel_path() { return forced_path(); }
 
 void launch_group_program(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
                           const double* ta, const double* tb, double* tout) {

@@ -60,5 +60,8 @@ void launch_fill_uniform(const LaunchCtx& c, double* out, int64_t count, uint64_
                          int64_t offset, double lo, double hi);
 
 void check_cuda(cudaError_t e, const char* what);
+// 0 = best eligible, 1 = TMA ring, 2 = register tree, 3 = generic interpreter.
+void set_kernel_path(int path);
+int kernel_path();
 
 }  // namespace ttb

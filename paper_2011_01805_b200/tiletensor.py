@@ -653,6 +653,19 @@ def shard_plan(shape: TileTensorShape, shard_dim: int, world: int, rank: int):
     return b.value, e.value, TileTensorShape.from_c(out)
 
 
+KERNEL_PATHS = {"auto": 0, "tma": 1, "regs": 2, "generic": 3}
+
+
+def set_kernel_path(path: str) -> None:
+    """Force the reduction kernel path (identical results, different speed)."""
+    _check(lib().tt_set_kernel_path(KERNEL_PATHS[path]))
+
+
+def kernel_path() -> str:
+    v = int(lib().tt_kernel_path())
+    return {b: a for a, b in KERNEL_PATHS.items()}[v]
+
+
 def device_count() -> int:
     n = ctypes.c_int()
     lib().tt_device_count(ctypes.byref(n))

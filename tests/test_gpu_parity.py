@@ -282,3 +282,37 @@ def test_depth_exhaustion(gpu):
     sq = tt.tt_mul(ta, ta)
     with pytest.raises(tt.DepthExhaustedError):
         tt.tt_mul(sq, sq)
+
+
+@pytest.mark.parametrize("path", ["auto", "tma", "regs", "generic"])
+def test_fused_large_tiles_every_path(gpu, oracle, path):
+    """Config-5-like tiles (s = 16384 and 8192): every reduction kernel path
+    (TMA ring, register tree, generic interpreter) and both group regimes
+    (few groups -> split fold + tree, many groups -> single pass), with B
+    broadcast along the summed dim (W-like) and not."""
+    nrng = np.random.default_rng(5005)
+    cases = [
+        ("[512/16,256/32,64/32]", "[*/16,256/32,64/32]", 16384),
+        ("[64/16,64/32,128/32]", "[64/16,64/32,*/32]", 16384),
+        ("[256/16,512/32,32/16]", "[*/16,512/32,32/16]", 8192),
+    ]
+    tt.set_kernel_path(path)
+    try:
+        for xa, xb, s in cases:
+            S = session(s)
+            sa, sb = parse_shape(xa), parse_shape(xb)
+            ta = nrng.uniform(-1, 1, size=(sa.tile_count(), s))
+            tb = nrng.uniform(-1, 1, size=(sb.tile_count(), s))
+            A, B = TileTensor(sa, ta, S), TileTensor(sb, tb, S)
+            for dim in (1, 2, 3):
+                ws, wt, wc = oracle.mul_sum(sa, ta, sb, tb, s, dim)
+                S.reset_counters()
+                got = tt.tt_mul_sum(A, B, dim)
+                assert got.shape() == ws
+                assert_bitwise(got.tiles(), wt, f"{path} {xa} x {xb} dim {dim}")
+                assert same_cost(S.cost_report(), wc)
+                # tt_sum alone on the same tensor
+                ws2, wt2, _ = oracle.sum(sa, ta, s, dim)
+                assert_bitwise(tt.tt_sum(A, dim).tiles(), wt2, f"{path} sum {xa} dim {dim}")
+    finally:
+        tt.set_kernel_path("auto")
