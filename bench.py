@@ -63,60 +63,55 @@ def traffic_summary():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled (NVML, every 10 ms) during the
+    timed region; falls back to nvidia-smi if pynvml is unavailable."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.sm, self.mx, self.reasons = [], [], set()
+        self._stop = threading.Event()
+        self.thread = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[self.index]) if vis else self.index
+            h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        self.mx.append(mx)
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for name, bit in self.REASONS.items():
+                            if r & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    self._stop.wait(0.01)
+            self.thread = threading.Thread(target=run, daemon=True)
             self.thread.start()
         except Exception:
-            self.proc = None
+            self.thread = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-            except ValueError:
-                continue
-            for name, flag in zip(names, parts[5:9]):
-                if flag.lower() == "active":
-                    reasons.add(name)
-        if not sm:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx),
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 # ---- distributed plumbing -------------------------------------------------------------
@@ -256,26 +251,31 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     hbm_peak, peak_src = peaks()
 
+    from paper_2011_01805_b200 import sharding
     S = tt.Session(S5, 8, device=local)
-    sx = tt.parse_shape(configs.C5_X_SHAPE)
+    # weak scaling: the global X is [2048*N, 2048, 512]; rank r owns external
+    # tiles [128r, 128r+128) of dim 1 (its own 16 GiB slab); W broadcasts.
+    sx_global = tt.TileTensorShape([tt.DimSpec(2048 * world, 1, 16), tt.DimSpec(2048, 1, 32),
+                                    tt.DimSpec(512, 1, 32)])
+    plan = sharding.plan(sx_global, 1, world, rank)
+    sx = plan.local_shape
     sw = tt.parse_shape(configs.C5_W_SHAPE)
+    assert sharding.operand_plan(sw, plan) is None and sx.tile_count() == X_TILES
     # inputs generated on the device with the shared counter-based generator
     x_dense = torch.empty(configs.C5_DIMS, dtype=torch.float64, device=dev)
     w_dense = torch.empty((1, 2048, 512), dtype=torch.float64, device=dev)
-    rank_offset = rank * (2048 * 2048 * 512)
+    rank_offset = plan.row_slice.start * (2048 * 512)
     tt.fill_uniform(S, x_dense, configs.C5_SEED_X, -1.0, 1.0, offset=rank_offset)
-    tt.fill_uniform(S, w_dense, configs.C5_SEED_W, -1.0, 1.0)
+    tt.fill_uniform(S, w_dense, configs.C5_SEED_W, -1.0, 1.0)  # same W on every rank
     X = tt.pack(x_dense, sx, S)
     W = tt.pack(w_dense, sw, S)
 
+    def mul_sum(a, b, k):
+        return tt.tt_mul_sum(a, b, k)
+
     def step():
-        outs = []
-        for k in (1, 2, 3):
-            r = tt.tt_mul_sum(X, W, k)
-            if k == 1 and dist is not None:
-                dist.all_reduce(r.data())  # dim 1 spans ranks: NCCL over NVLink
-            outs.append(r)
-        return outs
+        return [sharding.sharded_mul_sum(X, W, k, plan, mul_sum, lambda r: r.data())[0]
+                for k in (1, 2, 3)]
 
     for _ in range(args.warmup):
         step()
@@ -299,8 +299,8 @@ def run_ours(args):
             for k in (1, 2, 3):
                 r = tt.tt_mul_sum(X, W, k)
                 ev[k].record(stream)
-                if k == 1 and dist is not None:
-                    dist.all_reduce(r.data())
+                if k == plan.shard_dim and world > 1:
+                    sharding.allreduce_partial(r.data())  # NCCL over NVLink
             # the sync below is per step only to read the per-launch events
             ev[3].synchronize()
             per_dim[1].append(ev[0].elapsed_time(ev[1]) / 1e3)
@@ -355,9 +355,7 @@ def run_ours(args):
             Wh = tt.pack(host_w, sw, S)
             d2h = 0
             for k in (1, 2, 3):
-                r = tt.tt_mul_sum(Xh, Wh, k)
-                if k == 1 and dist is not None:
-                    dist.all_reduce(r.data())
+                r, _ = sharding.sharded_mul_sum(Xh, Wh, k, plan, mul_sum, lambda t: t.data())
                 res = tt.unpack(r)          # unpack kernel + D2H
                 d2h += res.nbytes
             return d2h

@@ -76,7 +76,7 @@ def build_host_tests(verbose: bool = False) -> Path:
             print("[build] g++ host_tests.cpp")
         _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", str(ROOT / "include"),
               "-I", str(PKG / "include"), str(src), "-o", str(HOST_TESTS), "-L", str(LIB_DIR),
-              "-ltiletensor_b200", f"-Wl,-rpath,{LIB_DIR}", "-pthread"])
+              "-ltiletensor_b200", "-Wl,-rpath,$ORIGIN", "-pthread"])
     return HOST_TESTS
 
 

@@ -1,0 +1,125 @@
+"""Sharding of external tile indices across GPUs (north-star item 5).
+
+One process per GPU.  A tile tensor is block-partitioned along one external
+dimension (`shard_dim`, 1-based): rank r owns external indices
+[begin_r, end_r) of that dim, i.e. the dense slab of rows
+[begin_r * t, min(n, end_r * t)).  Because every output tile of an
+elementwise op or of a sum over another dim depends only on operand tiles at
+the same external index (or the broadcast index l mod e,
+tile_tensor.hpp:260-265), those ops run locally with NO communication and
+the results stay sharded, bit-identical to the single-GPU result.
+
+Only a sum over `shard_dim` itself spans ranks: each rank runs the fused
+fold + rotate-and-sum on its slab and the partial results are summed with one
+NCCL all-reduce over NVLink (torch.distributed, backend "nccl").  The
+cross-rank addition re-associates the reference's left fold, so that result
+matches the single-device one within 1e-12 relative (north star), not
+bitwise.
+
+The compute backend is injectable (`ops`): on GPUs it is this package's
+CUDA path; the CPU gloo tests drive the same planning and collective logic
+with the oracle as compute.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Any, Callable, Optional
+
+from .tiletensor import DimSpec, TileTensorShape, shard_plan
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    global_shape: TileTensorShape
+    local_shape: TileTensorShape
+    shard_dim: int           # 1-based
+    world: int
+    rank: int
+    begin: int               # external tile index range [begin, end)
+    end: int
+
+    @property
+    def row_slice(self) -> slice:
+        """Dense rows of `shard_dim` this rank holds."""
+        d = self.global_shape.dim(self.shard_dim - 1)
+        lo = self.begin * d.t
+        return slice(lo, min(d.used(), self.end * d.t))
+
+    def dense_slices(self) -> tuple:
+        sl = [slice(None)] * self.global_shape.rank()
+        sl[self.shard_dim - 1] = self.row_slice
+        return tuple(sl)
+
+    def local_tiles(self) -> int:
+        return self.local_shape.tile_count()
+
+
+def plan(global_shape: TileTensorShape, shard_dim: int, world: int, rank: int) -> ShardPlan:
+    b, e, local = shard_plan(global_shape, shard_dim, world, rank)
+    return ShardPlan(global_shape, local, shard_dim, world, rank, b, e)
+
+
+def operand_plan(op_shape: TileTensorShape, x_plan: ShardPlan) -> Optional[ShardPlan]:
+    """How a second operand follows X's sharding: None when it broadcasts
+    (fully replicated, one external tile) along shard_dim -- then every rank
+    holds it whole -- else the same block partition."""
+    d = op_shape.dim(x_plan.shard_dim - 1)
+    if d.n == 1 and (d.d + d.t - 1) // d.t == 1:
+        return None
+    return plan(op_shape, x_plan.shard_dim, x_plan.world, x_plan.rank)
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+def allreduce_partial(data, group=None) -> None:
+    """Sum a rank-partial result over all ranks in place (NCCL on GPUs)."""
+    dist = _dist()
+    if dist is not None and dist.get_world_size(group) > 1:
+        dist.all_reduce(data, op=dist.ReduceOp.SUM, group=group)
+
+
+def broadcast_operand(data, src: int = 0, group=None) -> None:
+    """Replicate an operand that every rank needs whole (e.g. W)."""
+    dist = _dist()
+    if dist is not None and dist.get_world_size(group) > 1:
+        dist.broadcast(data, src=src, group=group)
+
+
+def sharded_mul_sum(x_local, w_local, dim: int, x_plan: ShardPlan,
+                    mul_sum: Callable[[Any, Any, int], Any],
+                    data_of: Callable[[Any], Any], group=None):
+    """tt_sum(tt_mul(X, W), dim) on a sharded X.
+
+    dim != shard_dim: local fused op, result sharded like X (no traffic).
+    dim == shard_dim: local fused op over the slab, then one all-reduce of
+    the partial result -- every rank ends with the full (replicated) result.
+    Returns (result, is_sharded).
+    """
+    r = mul_sum(x_local, w_local, dim)
+    if dim == x_plan.shard_dim:
+        allreduce_partial(data_of(r), group)
+        return r, False
+    return r, True
+
+
+def local_result_tile_range(x_plan: ShardPlan, result_shape: TileTensorShape):
+    """Tile rows [lo, hi) of the GLOBAL result that this rank's sharded result
+    holds (row-major external order, shard_dim outermost-relative slab)."""
+    ext = result_shape.external_extents()
+    k = x_plan.shard_dim - 1
+    inner = 1
+    for e in ext[k + 1:]:
+        inner *= e
+    outer = 1
+    for e in ext[:k]:
+        outer *= e
+    if outer != 1:
+        raise ValueError("contiguous tile range only when shard_dim is the outermost non-unit dim")
+    return x_plan.begin * inner, x_plan.end * inner
+
+
+__all__ = ["ShardPlan", "plan", "operand_plan", "allreduce_partial", "broadcast_operand",
+           "sharded_mul_sum", "local_result_tile_range"]
