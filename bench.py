@@ -227,6 +227,8 @@ def run_reference(args):
 
 def time_events(fn, reps, stream):
     import torch
+    fn()  # warm-up outside the timed region (allocator growth, first-launch setup)
+    torch.cuda.synchronize()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record(stream)
