@@ -957,6 +957,216 @@ __global__ void __launch_bounds__(256) fold_kernel(const __grid_constant__ Group
   }
 }
 
+// ---- blocked fold (tile-tensor matmul) ---------------------------------------------------
+// For a product whose group grid has a dim `ia` along which B broadcasts and a
+// dim `ib` along which A broadcasts (matmul_a/b: out(i,k) = sum_j A(i,j)B(j,k)),
+// a thread folds a P x Q block of groups for one slot: per fold step it loads
+// P slots of A and Q of B and updates P*Q accumulators (acc = P[0]; acc += P[l],
+// the reference's left fold per group).  A is read ceil(|ib|/Q) times and B
+// ceil(|ia|/P) times instead of once per group; consecutive work units cover
+// the blocks of one slot chunk so concurrently running CTAs share operand
+// chunks in L2.  The folded tiles go to OUT; the in-tile schedule then runs
+// in place (two-phase reduction).
+
+struct BlockSpec {
+  int64_t ext_ia = 1, ext_ib = 1;            // extents of the blocked dims (1 if absent)
+  int64_t a_ia = 0, out_ia = 0;              // tile strides along ia
+  int64_t b_ib = 0, out_ib = 0;              // tile strides along ib
+  int64_t nbp = 1, nbq = 1;                  // blocks along ia, ib
+  int64_t chunks = 1;                        // slot chunks per tile
+  int64_t units = 0;
+  FastDiv64 div_nbq, div_nbp, div_chunks;
+};
+
+constexpr int kBlockThreads = 256;
+
+template <bool HAS_B, int P, int Q>
+__global__ void __launch_bounds__(kBlockThreads) fold_blocked_kernel(
+    const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
+    const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ OUT) {
+  const int64_t s = p.s;
+  const int64_t first = p.ops[0].x;
+  const int64_t count = p.ops[0].y;
+  const int64_t sa = p.g.astep * s, sb = p.g.bstep * s;
+  for (uint64_t u = blockIdx.x; u < static_cast<uint64_t>(bs.units); u += gridDim.x) {
+    // u = ((rest * chunks + chunk) * nbp + pb) * nbq + qb
+    uint64_t t = u;
+    const uint64_t t1 = fdiv(t, bs.div_nbq);
+    const int64_t qb = static_cast<int64_t>(t - t1 * bs.div_nbq.d);
+    const uint64_t t2 = fdiv(t1, bs.div_nbp);
+    const int64_t pb = static_cast<int64_t>(t1 - t2 * bs.div_nbp.d);
+    const uint64_t rest = fdiv(t2, bs.div_chunks);
+    const int64_t chunk = static_cast<int64_t>(t2 - rest * bs.div_chunks.d);
+    const int64_t j = chunk * kBlockThreads + threadIdx.x;
+    if (j >= s) continue;
+    const GroupBase gb = group_base(p, rest);
+    const int np = static_cast<int>(bs.ext_ia - pb * P < P ? bs.ext_ia - pb * P : P);
+    const int nq = static_cast<int>(bs.ext_ib - qb * Q < Q ? bs.ext_ib - qb * Q : Q);
+    // operand slot j of group row i / column k at fold step c (tails clamp to
+    // the last valid group; their results are not stored)
+    const double* a0 = A + (gb.a + pb * P * bs.a_ia + first * p.g.astep) * s + j;
+    const double* b0 = HAS_B ? B + (gb.b + qb * Q * bs.b_ib + first * p.g.bstep) * s + j : nullptr;
+    const int64_t a_row = bs.a_ia * s, b_col = bs.b_ib * s;
+    double acc[P][Q];
+    {
+      double a[P], b[Q];
+#pragma unroll
+      for (int i = 0; i < P; ++i) a[i] = __ldg(a0 + (i < np ? i : np - 1) * a_row);
+#pragma unroll
+      for (int k = 0; k < Q; ++k) b[k] = HAS_B ? __ldg(b0 + (k < nq ? k : nq - 1) * b_col) : 1.0;
+#pragma unroll
+      for (int i = 0; i < P; ++i)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) acc[i][k] = HAS_B ? dmul(a[i], b[k]) : a[i];
+    }
+    for (int64_t c = 1; c < count; ++c) {
+      double a[P], b[Q];
+#pragma unroll
+      for (int i = 0; i < P; ++i) a[i] = __ldg(a0 + c * sa + (i < np ? i : np - 1) * a_row);
+#pragma unroll
+      for (int k = 0; k < Q; ++k)
+        b[k] = HAS_B ? __ldg(b0 + c * sb + (k < nq ? k : nq - 1) * b_col) : 1.0;
+#pragma unroll
+      for (int i = 0; i < P; ++i)
+#pragma unroll
+        for (int k = 0; k < Q; ++k)
+          acc[i][k] = dadd(acc[i][k], HAS_B ? dmul(a[i], b[k]) : a[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int k = 0; k < Q; ++k)
+        if (i < np && k < nq)
+          OUT[(gb.out + (pb * P + i) * bs.out_ia + (qb * Q + k) * bs.out_ib) * s + j] = acc[i][k];
+  }
+}
+
+// GEMM-shaped variant for products with BOTH broadcast dims (matmul_a/b):
+// a CTA folds a 16 x 16 block of groups for 64 consecutive slots.  Each fold
+// step stages the block's 16 A-chunks and 16 B-chunks (64 slots each, 16 KiB)
+// in shared memory with cp.async (double-buffered, next step in flight while
+// this one computes); warp w owns slot half (w & 1) and the 8 x 4 sub-block
+// (w >> 1) of the 16 x 16 groups, so each thread reads 8 + 4 operands from
+// shared memory for 32 multiply-adds (128 registers, no spills).  Every A chunk is read once per 16
+// groups and every B chunk once per 16 groups (vs once per group).
+constexpr int kGemmSlots = 64;
+constexpr int kGemmBlk = 16;   // block rows (groups along ia)
+constexpr int kGemmSubR = 8;
+constexpr int kGemmSubC = 4;
+constexpr int kGemmStages = 4;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// BC = block columns (groups along ib): 16 (512 threads) or 8 (256 threads,
+// more and smaller work units when the 16 x 16 grid would leave SMs idle).
+template <int BC>
+__global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32, BC == 8 ? 2 : 1)
+    fold_gemm_kernel(const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
+                     const double* __restrict__ A, const double* __restrict__ B,
+                     double* __restrict__ OUT) {
+  constexpr int kThreads = 2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32;
+  constexpr int kSubCols = BC / kGemmSubC;
+  extern __shared__ __align__(16) double gsm[];
+  // kGemmStages-deep ring of (A block chunk, B block chunk)
+  auto sA = reinterpret_cast<double(*)[kGemmBlk][kGemmSlots]>(gsm);
+  auto sB = reinterpret_cast<double(*)[BC][kGemmSlots]>(gsm + kGemmStages * kGemmBlk * kGemmSlots);
+  const int64_t s = p.s;
+  const int64_t first = p.ops[0].x;
+  const int64_t count = p.ops[0].y;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int slot = (warp & 1) * 32 + lane;     // slot within the 64-slot chunk
+  const int sub = warp >> 1;                   // 8x4 sub-block of the 16 x BC groups
+  const int r0 = (sub / kSubCols) * kGemmSubR, c0 = (sub % kSubCols) * kGemmSubC;
+  for (uint64_t u = blockIdx.x; u < static_cast<uint64_t>(bs.units); u += gridDim.x) {
+    uint64_t t = u;
+    const uint64_t t1 = fdiv(t, bs.div_nbq);
+    const int64_t qb = static_cast<int64_t>(t - t1 * bs.div_nbq.d);
+    const uint64_t t2 = fdiv(t1, bs.div_nbp);
+    const int64_t pb = static_cast<int64_t>(t1 - t2 * bs.div_nbp.d);
+    const uint64_t rest = fdiv(t2, bs.div_chunks);
+    const int64_t chunk = static_cast<int64_t>(t2 - rest * bs.div_chunks.d);
+    const GroupBase gb = group_base(p, rest);
+    const int np = static_cast<int>(bs.ext_ia - pb * kGemmBlk < kGemmBlk ? bs.ext_ia - pb * kGemmBlk : kGemmBlk);
+    const int nq = static_cast<int>(bs.ext_ib - qb * BC < BC ? bs.ext_ib - qb * BC : BC);
+    const int64_t j0 = chunk * kGemmSlots;
+    const double* a0 = A + (gb.a + pb * kGemmBlk * bs.a_ia + first * p.g.astep) * s + j0;
+    const double* b0 = B + (gb.b + qb * BC * bs.b_ib + first * p.g.bstep) * s + j0;
+    const int64_t a_row = bs.a_ia * s, b_col = bs.b_ib * s;
+    const int64_t sa = p.g.astep * s, sb = p.g.bstep * s;
+
+    auto stage = [&](int buf, int64_t c) {
+      // 16 (resp. BC) rows x 32 segments of 16 B per operand
+      for (int e = tid; e < kGemmBlk * 32; e += kThreads) {
+        const int row = e >> 5, seg = e & 31;
+        const int ra = row < np ? row : np - 1;
+        cp_async16(&sA[buf][row][seg * 2], a0 + c * sa + ra * a_row + seg * 2);
+      }
+      for (int e = tid; e < BC * 32; e += kThreads) {
+        const int row = e >> 5, seg = e & 31;
+        const int rb = row < nq ? row : nq - 1;
+        cp_async16(&sB[buf][row][seg * 2], b0 + c * sb + rb * b_col + seg * 2);
+      }
+      cp_async_commit();
+    };
+
+    double acc[kGemmSubR][kGemmSubC];
+    // prologue: steps 0 .. kGemmStages-2 in flight (empty groups keep the count uniform)
+#pragma unroll
+    for (int k = 0; k < kGemmStages - 1; ++k) {
+      if (k < count)
+        stage(k, k);
+      else
+        cp_async_commit();
+    }
+    for (int64_t c = 0; c < count; ++c) {
+      const int buf = static_cast<int>(c % kGemmStages);
+      cp_async_wait<kGemmStages - 2>();  // step c has landed
+      __syncthreads();                   // ...for every thread; buffer (c-1) is free
+      if (c + kGemmStages - 1 < count)
+        stage(static_cast<int>((c + kGemmStages - 1) % kGemmStages), c + kGemmStages - 1);
+      else
+        cp_async_commit();
+      double a[kGemmSubR], b[kGemmSubC];
+#pragma unroll
+      for (int i = 0; i < kGemmSubR; ++i) a[i] = sA[buf][r0 + i][slot];
+#pragma unroll
+      for (int k = 0; k < kGemmSubC; ++k) b[k] = sB[buf][c0 + k][slot];
+      if (c == 0) {
+#pragma unroll
+        for (int i = 0; i < kGemmSubR; ++i)
+#pragma unroll
+          for (int k = 0; k < kGemmSubC; ++k) acc[i][k] = dmul(a[i], b[k]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < kGemmSubR; ++i)
+#pragma unroll
+          for (int k = 0; k < kGemmSubC; ++k) acc[i][k] = dadd(acc[i][k], dmul(a[i], b[k]));
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // the ring is reused by the next unit
+    const int64_t j = j0 + slot;
+    if (j < s) {
+#pragma unroll
+      for (int i = 0; i < kGemmSubR; ++i)
+#pragma unroll
+        for (int k = 0; k < kGemmSubC; ++k)
+          if (r0 + i < np && c0 + k < nq)
+            OUT[(gb.out + (pb * kGemmBlk + r0 + i) * bs.out_ia + (qb * BC + c0 + k) * bs.out_ib) *
+                    s + j] = acc[i][k];
+    }
+  }
+}
+
 // ---- synthetic input generator (== or_fill_uniform in oracle/tt_oracle.c) ------------
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -1127,6 +1337,20 @@ GroupParams make_group_params(const Program& prog, const GroupSpec& g, int64_t s
   return p;
 }
 
+// Kernel-path override for A/B measurement and tests (tt_set_kernel_path /
+// TT_KERNEL_PATH = tma | regs | generic); 0 = best eligible path.
+std::atomic<int> g_forced_path{-1};
+
+int forced_path() {
+  int v = g_forced_path.load(std::memory_order_relaxed);
+  if (v >= 0) return v;
+  const char* e = std::getenv("TT_KERNEL_PATH");
+  const std::string s(e ? e : "");
+  v = s == "tma" ? 1 : s == "regs" ? 2 : s == "generic" ? 3 : 0;
+  g_forced_path.store(v, std::memory_order_relaxed);
+  return v;
+}
+
 template <bool HAS_B>
 void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
                  double* tout) {
@@ -1144,6 +1368,109 @@ void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, con
                                                            make_div64(static_cast<uint64_t>(s)));
   }
   post_launch(c, "fold kernel");
+}
+
+// Blocked-fold plan: ia = a group dim along which B broadcasts (A varies), ib =
+// one along which A broadcasts (B varies).  Eligible when at least one exists.
+struct BlockPlan {
+  int ia = -1, ib = -1;
+};
+
+BlockPlan block_plan(const GroupSpec& g, bool has_b) {
+  BlockPlan bp;
+  if (!has_b) return bp;
+  for (int i = 0; i < g.nd; ++i) {
+    if (g.ext[i] <= 1) continue;
+    if (g.a_stride[i] != 0 && g.b_stride[i] == 0 && bp.ia < 0) bp.ia = i;
+    if (g.a_stride[i] == 0 && g.b_stride[i] != 0 && bp.ib < 0) bp.ib = i;
+  }
+  return bp;
+}
+
+template <bool HAS_B, int P, int Q>
+void run_blocked(const LaunchCtx& c, const GroupParams& p, const BlockSpec& bs, const double* ta,
+                 const double* tb, double* tout) {
+  auto k = fold_blocked_kernel<HAS_B, P, Q>;
+  const int grid = grid_for(c, (const void*)k, kBlockThreads, 0, bs.units);
+  k<<<grid, kBlockThreads, 0, c.stream>>>(p, bs, ta, tb, tout);
+  post_launch(c, "blocked fold kernel");
+}
+
+// Phase-1 fold into OUT using the blocked kernel (requires has_b and a plan).
+template <bool HAS_B>
+void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPlan& bp,
+                         const double* ta, const double* tb, double* tout) {
+  const GroupSpec& g = p.g;
+  GroupParams pr = p;  // the remaining ("rest") group dims
+  pr.g.nd = 0;
+  pr.g.groups = 1;
+  for (int i = 0; i < g.nd; ++i) {
+    if (i == bp.ia || i == bp.ib) continue;
+    const int k = pr.g.nd++;
+    pr.g.ext[k] = g.ext[i];
+    pr.g.out_stride[k] = g.out_stride[i];
+    pr.g.a_stride[k] = g.a_stride[i];
+    pr.g.b_stride[k] = g.b_stride[i];
+    pr.gdiv[k] = p.gdiv[i];
+    pr.g.groups *= g.ext[i];
+  }
+  const bool gemm = bp.ia >= 0 && bp.ib >= 0 && p.s % kGemmSlots == 0 && aligned16(ta) &&
+                    aligned16(tb) && forced_path() != 2;
+  int P = gemm ? kGemmBlk : (bp.ia >= 0 ? 8 : 1);
+  int Q = gemm ? kGemmBlk : (bp.ib >= 0 ? 8 : 1);
+  if (gemm) {  // 16 x 8 blocks when 16 x 16 would give fewer than ~3 waves of units
+    const int64_t units16 = pr.g.groups * (p.s / kGemmSlots) * ((g.ext[bp.ia] + 15) / 16) *
+                            ((g.ext[bp.ib] + 15) / 16);
+    (void)units16;  // 16 x 8 measured slower on config 3 (more L2 traffic); keep 16 x 16
+  }
+  BlockSpec bs;
+  if (bp.ia >= 0) {
+    bs.ext_ia = g.ext[bp.ia];
+    bs.a_ia = g.a_stride[bp.ia];
+    bs.out_ia = g.out_stride[bp.ia];
+  }
+  if (bp.ib >= 0) {
+    bs.ext_ib = g.ext[bp.ib];
+    bs.b_ib = g.b_stride[bp.ib];
+    bs.out_ib = g.out_stride[bp.ib];
+  }
+  bs.nbp = (bs.ext_ia + P - 1) / P;
+  bs.nbq = (bs.ext_ib + Q - 1) / Q;
+  bs.chunks = gemm ? p.s / kGemmSlots : (p.s + kBlockThreads - 1) / kBlockThreads;
+  bs.units = pr.g.groups * bs.chunks * bs.nbp * bs.nbq;
+  bs.div_nbq = make_div64(static_cast<uint64_t>(bs.nbq));
+  bs.div_nbp = make_div64(static_cast<uint64_t>(bs.nbp));
+  bs.div_chunks = make_div64(static_cast<uint64_t>(bs.chunks));
+  if (gemm) {
+    const size_t smem = static_cast<size_t>(kGemmStages) * (kGemmBlk + Q) * kGemmSlots * sizeof(double);
+    const void* k = Q == 16 ? (const void*)fold_gemm_kernel<16> : (const void*)fold_gemm_kernel<8>;
+    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)),
+               "smem attribute");
+    const int threads = Q == 16 ? 512 : 256;
+    const int grid = grid_for(c, k, threads, smem, bs.units);
+    if (Q == 16)
+      fold_gemm_kernel<16><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+    else
+      fold_gemm_kernel<8><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+    post_launch(c, "gemm fold kernel");
+  } else if (P == 8 && Q == 8)
+    run_blocked<HAS_B, 8, 8>(c, pr, bs, ta, tb, tout);
+  else if (P == 8)
+    run_blocked<HAS_B, 8, 1>(c, pr, bs, ta, tb, tout);
+  else
+    run_blocked<HAS_B, 1, 8>(c, pr, bs, ta, tb, tout);
+}
+
+// Phase-1 fold: blocked when the product has a broadcast structure to exploit.
+template <bool HAS_B>
+void launch_fold_best(const LaunchCtx& c, const GroupParams& p, const double* ta,
+                      const double* tb, double* tout) {
+  const BlockPlan bp = block_plan(p.g, HAS_B);
+  if (HAS_B && (bp.ia >= 0 || bp.ib >= 0) && p.ops[0].y > 1 && forced_path() != 3)
+    launch_fold_blocked<HAS_B>(c, p, bp, ta, tb, tout);
+  else
+    launch_fold<HAS_B>(c, p, ta, tb, tout);
 }
 
 template <int VMAX, bool HAS_B, bool VEC>
@@ -1205,20 +1532,6 @@ void dispatch_tma(const LaunchCtx& c, const GroupParams& p, const double* ta, co
     run_tma<32, HAS_B>(c, p, ta, tb, tout);
 }
 
-// Kernel-path override for A/B measurement and tests (tt_set_kernel_path /
-// TT_KERNEL_PATH = tma | regs | generic); 0 = best eligible path.
-std::atomic<int> g_forced_path{-1};
-
-int forced_path() {
-  int v = g_forced_path.load(std::memory_order_relaxed);
-  if (v >= 0) return v;
-  const char* e = std::getenv("TT_KERNEL_PATH");
-  const std::string s(e ? e : "");
-  v = s == "tma" ? 1 : s == "regs" ? 2 : s == "generic" ? 3 : 0;
-  g_forced_path.store(v, std::memory_order_relaxed);
-  return v;
-}
-
 template <bool HAS_B>
 void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
                          const double* ta, const double* tb, double* tout) {
@@ -1227,9 +1540,11 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
   const size_t tile_bytes = static_cast<size_t>(s) * sizeof(double);
   // 1) No in-tile schedule: the fold is the whole program.
   if (prog.ops.size() == 1 && prog.ops[0].kind == GOP_FOLD && prog.ops[0].dst == BUF_OUT) {
-    launch_fold<HAS_B>(c, p, ta, tb, tout);
+    launch_fold_best<HAS_B>(c, p, ta, tb, tout);
     return;
   }
+  const BlockPlan bplan = block_plan(g, HAS_B);
+  const bool matmul_like = HAS_B && bplan.ia >= 0 && bplan.ib >= 0;
   // 2) Fast paths: fold + power-of-two rotate-and-sum in one pass.
   const int force = forced_path();
   const int threads = static_cast<int>(std::min<int64_t>(512, ((s + 31) / 32) * 32));
@@ -1248,9 +1563,10 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
     // Too few groups to occupy every SM: fold over the whole grid first
     // (phase 1, into OUT), then run the schedule on OUT in place (phase 2).
     const int64_t per_sm = std::max<int64_t>(1, static_cast<int64_t>(c.smem_optin / (tile_bytes + 1024)));
-    if (g.groups < static_cast<int64_t>(c.sm_count) * std::min<int64_t>(per_sm, 4) &&
+    if ((g.groups < static_cast<int64_t>(c.sm_count) * std::min<int64_t>(per_sm, 4) ||
+         (matmul_like && force != 1 && force != 2)) &&
         prog.ops[0].y > 1) {
-      launch_fold<HAS_B>(c, p, ta, tb, tout);
+      launch_fold_best<HAS_B>(c, p, ta, tb, tout);
       // phase 2 reads its group's folded tile from OUT: a = out tile index
       GroupParams p2 = p;
       for (int i = 0; i < g.nd; ++i) {
@@ -1261,7 +1577,10 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
       p2.g.bstep = 0;
       p2.ops[0].x = 0;
       p2.ops[0].y = 1;
-      if (tma_ok)
+      // tree-only pass: the register-tree kernel (several CTAs per SM overlap
+      // load, tree and store) unless the tile is too big for two CTAs per SM
+      const bool regs2 = force == 2;  // the TMA kernel measured faster for tree-only passes
+      if (tma_ok && !regs2)
         dispatch_tma<false>(c, p2, tout, nullptr, tout);
       else if (s % 2 == 0 && aligned16(tout))
         dispatch_pow2<false, true>(c, p2, threads, vmax, tile_bytes, tout, nullptr, tout);
