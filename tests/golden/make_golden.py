@@ -187,6 +187,48 @@ def main():
     add("config_digest", name="c2", so=so, digest=digest(out), cost=cost_vec(c),
         unpacked=ref.unpack(so, 8192, out))
 
+    # config 3 ('3b' chain and the literal '3a' chain), through the reference
+    c3 = configs.config3()
+    sh3 = {k: parse_shape(v) for k, v in c3.shapes.items()}
+    p3 = {k: ref.pack(c3.tensors[k], sh3[k], 8192) for k in sh3}
+    s1, o1, k1 = ref.linalg(3, sh3["Bt3"], p3["Bt3"], sh3["C3"], p3["C3"], 8192)
+    s2, o2, k2 = ref.linalg(2, sh3["A3"], p3["A3"], s1, o1, 8192)
+    add("config_digest", name="c3b_stage1", so=s1, digest=digest(o1), cost=cost_vec(k1))
+    add("config_digest", name="c3b", so=s2, digest=digest(o2), cost=cost_vec(k2),
+        unpacked=ref.unpack(s2, 8192, o2))
+    sa, oa, ka = ref.linalg(2, sh3["A3"], p3["A3"], sh3["B3"], p3["B3"], 8192)
+    sc, oc, _ = ref.clean_unknowns(sa, oa, 8192)
+    sr, orr, _ = ref.replicate_dim(sc, oc, 8192, 2)
+    s3, o3, _ = ref.mul_sum(sr, orr, sh3["Ct3"], p3["Ct3"], 8192, 3)
+    add("config_digest", name="c3a", so=s3, digest=digest(o3), cost=cost_vec(ka))
+    # config 4, composed FC -> square -> FC on the full batch
+    c4 = configs.config4(False)
+    sh4 = {k: parse_shape(v) for k, v in c4.shapes.items()}
+    p4 = {k: ref.pack(c4.tensors[k], sh4[k], 8192) for k in sh4}
+    h1, t1, _ = ref.mul_sum(sh4["W1t"], p4["W1t"], sh4["X"], p4["X"], 8192, 1)
+    h2, t2, _ = ref.elementwise(0, h1, t1, sh4["b1"], p4["b1"], 8192)
+    h3, t3, _ = ref.elementwise(1, h2, t2, h2, t2, 8192)
+    h4, t4, _ = ref.mul_sum(sh4["W2"], p4["W2"], h3, t3, 8192, 2)
+    h5, t5, _ = ref.elementwise(0, h4, t4, sh4["b2"], p4["b2"], 8192)
+    add("config_digest", name="c4", so=h5, digest=digest(t5), cost=np.zeros(6, dtype=np.int64),
+        unpacked=ref.unpack(h5, 8192, t5))
+    # config 5 slabs: X[0:32] (sums over dims 2, 3) and X[:, 0:32] (sum over dim 1)
+    s5 = configs.C5_SLOTS
+    sw = parse_shape(configs.C5_W_SHAPE)
+    pw = ref.pack(configs.c5_w(), sw, s5)
+    add("config_digest", name="c5_w_pack", so=sw, digest=digest(pw), cost=np.zeros(6, dtype=np.int64))
+    ss = TileTensorShape([DimSpec(32, 1, 16), DimSpec(2048, 1, 32), DimSpec(512, 1, 32)])
+    px = ref.pack(configs.c5_x_slab(slice(0, 32)), ss, s5)
+    add("config_digest", name="c5_x_pack_slab", so=ss, digest=digest(px), cost=np.zeros(6, dtype=np.int64))
+    for dim in (2, 3):
+        so, out, k = ref.mul_sum(ss, px, sw, pw, s5, dim)
+        add("config_digest", name=f"c5_dim{dim}_slab", so=so, digest=digest(out), cost=cost_vec(k))
+    ss2 = TileTensorShape([DimSpec(2048, 1, 16), DimSpec(32, 1, 32), DimSpec(512, 1, 32)])
+    sw2 = TileTensorShape([DimSpec(1, 16, 16), DimSpec(32, 1, 32), DimSpec(512, 1, 32)])
+    so, out, k = ref.mul_sum(ss2, ref.pack(configs.c5_x_slab(slice(None), slice(0, 32)), ss2, s5),
+                             sw2, ref.pack(configs.c5_w(slice(0, 32)), sw2, s5), s5, 1)
+    add("config_digest", name="c5_dim1_slab", so=so, digest=digest(out), cost=cost_vec(k))
+
     np.savez_compressed(HERE / "golden.npz", **arrays)
     (HERE / "golden_index.json").write_text(json.dumps(index, indent=0))
     print(f"wrote {len(index)} cases, {len(arrays)} arrays")

@@ -127,6 +127,10 @@ def test_config3_chains(gpu, oracle):
     so2, o2, c2 = oracle.mul_sum(parse_shape(case.shapes["A3"]), p["A3"], so1, o1, s, 2)
     assert bitwise_equal(r.tiles(), o2)
     assert cost_tuple(S.cost_report())[:4] == tuple(np.add(cost_tuple(c1), cost_tuple(c2)))[:4]
+    # pinned to the reference's own outputs (tests/golden, made by oracle/_ref)
+    gold = {c["name"]: c for c in load() if c["kind"] == "config_digest"}
+    assert digest(s1.tiles()) == gold["c3b_stage1"]["digest"]
+    assert digest(r.tiles()) == gold["c3b"]["digest"]
     abc = case.tensors["A"] @ case.tensors["B"] @ case.tensors["C"]
     got = tt.unpack(r).reshape(512, 256)
     assert oracle.max_rel_diff(got, abc) < 1e-12
@@ -136,6 +140,7 @@ def test_config3_chains(gpu, oracle):
     rep = tt.replicate_dim(tt.clean_unknowns(ra), 2)
     assert tt.format_shape(rep.shape()) == "[512/16,*/32,768/16]"
     r3a = tt.tt_mul_sum(rep, T["Ct3"], 3)
+    assert digest(r3a.tiles()) == gold["c3a"]["digest"]
     assert tt.format_shape(r3a.shape()) == "[512/16,256/32,1?/16]"
     assert oracle.max_rel_diff(tt.unpack(r3a).reshape(512, 256), abc) < 1e-12
     # bitwise against the oracle composition of the same chain
@@ -181,6 +186,8 @@ def test_config4_fc_square_fc(gpu, oracle, interleaved):
     assert bitwise_equal(logits, want)
     if not interleaved:
         assert bitwise_equal(y.tiles(), o5)
+        gold = next(c for c in load() if c["kind"] == "config_digest" and c["name"] == "c4")
+        assert digest(y.tiles()) == gold["digest"]
 
 
 @pytest.mark.slow
@@ -206,10 +213,15 @@ def test_config5_full_size_slabs(gpu, oracle):
     assert bitwise_equal(X.data()[:2048].cpu().numpy(), px)
     pw = oracle.pack(configs.c5_w(), sw, s)
     assert bitwise_equal(W.tiles(), pw)
+    gold = {c["name"]: c for c in load() if c["kind"] == "config_digest"}
+    assert digest(W.tiles()) == gold["c5_w_pack"]["digest"]
+    assert digest(X.data()[:2048].cpu().numpy()) == gold["c5_x_pack_slab"]["digest"]
     for dim, ntiles in ((2, 32), (3, 128)):
         r = tt.tt_mul_sum(X, W, dim)
         so, want, _ = oracle.mul_sum(ss, px, sw, pw, s, dim)
-        assert bitwise_equal(r.data()[:ntiles].cpu().numpy(), want), dim
+        got = r.data()[:ntiles].cpu().numpy()
+        assert bitwise_equal(got, want), dim
+        assert digest(got) == gold[f"c5_dim{dim}_slab"]["digest"]
     # dim 1 spans all of X: slab along dim 2 (external index l2 = 0)
     r1 = tt.tt_mul_sum(X, W, 1)
     xs2 = configs.c5_x_slab(slice(None), slice(0, 32))
@@ -219,6 +231,7 @@ def test_config5_full_size_slabs(gpu, oracle):
                                  oracle.pack(configs.c5_w(slice(0, 32)), sw2, s), s, 1)
     assert tt.format_shape(r1.shape()) == "[*/16,2048/32,512/32]"
     assert bitwise_equal(r1.data()[:16].cpu().numpy(), want)
+    assert digest(r1.data()[:16].cpu().numpy()) == gold["c5_dim1_slab"]["digest"]
     # the replicated result unpacks to the dense sum (1e-12)
     got = tt.unpack(r1)[0, :32, :]
     dense = (xs2 * configs.c5_w(slice(0, 32))).sum(axis=0)

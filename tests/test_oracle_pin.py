@@ -245,3 +245,41 @@ def test_live_against_reference(oracle, ref):
                 continue
             r1 = oracle.elementwise(op, sh, tiles, sb, tb, s)
             assert r1[0] == r2[0] and bitwise_equal(r1[1], r2[1])
+
+
+def _golden_digest(name):
+    return next(c for c in CASES if c["kind"] == "config_digest" and c["name"] == name)
+
+
+def test_golden_config3_and_4_full_size(oracle):
+    """Full-size configs 3 and 4: the oracle reproduces the reference's digests."""
+    c3 = configs.config3()
+    s = 8192
+    sh = {k: parse_shape(v) for k, v in c3.shapes.items()}
+    p = {k: oracle.pack(c3.tensors[k], sh[k], s) for k in sh}
+    s1, o1, _ = oracle.mul_sum(sh["Bt3"], p["Bt3"], sh["C3"], p["C3"], s, 1)
+    assert digest(o1) == _golden_digest("c3b_stage1")["digest"]
+    s2, o2, _ = oracle.mul_sum(sh["A3"], p["A3"], s1, o1, s, 2)
+    assert digest(o2) == _golden_digest("c3b")["digest"]
+    c4 = configs.config4(False)
+    sh4 = {k: parse_shape(v) for k, v in c4.shapes.items()}
+    p4 = {k: oracle.pack(c4.tensors[k], sh4[k], s) for k in sh4}
+    h1, t1, _ = oracle.mul_sum(sh4["W1t"], p4["W1t"], sh4["X"], p4["X"], s, 1)
+    h2, t2, _ = oracle.elementwise(0, h1, t1, sh4["b1"], p4["b1"], s)
+    h3, t3, _ = oracle.elementwise(1, h2, t2, h2, t2, s)
+    h4, t4, _ = oracle.mul_sum(sh4["W2"], p4["W2"], h3, t3, s, 2)
+    h5, t5, _ = oracle.elementwise(0, h4, t4, sh4["b2"], p4["b2"], s)
+    assert digest(t5) == _golden_digest("c4")["digest"]
+
+
+def test_golden_config5_slabs(oracle):
+    s5 = configs.C5_SLOTS
+    sw = parse_shape(configs.C5_W_SHAPE)
+    pw = oracle.pack(configs.c5_w(), sw, s5)
+    assert digest(pw) == _golden_digest("c5_w_pack")["digest"]
+    ss = TileTensorShape([DimSpec(32, 1, 16), DimSpec(2048, 1, 32), DimSpec(512, 1, 32)])
+    px = oracle.pack(configs.c5_x_slab(slice(0, 32)), ss, s5)
+    assert digest(px) == _golden_digest("c5_x_pack_slab")["digest"]
+    for dim in (2, 3):
+        _, out, _ = oracle.mul_sum(ss, px, sw, pw, s5, dim)
+        assert digest(out) == _golden_digest(f"c5_dim{dim}_slab")["digest"]
