@@ -198,9 +198,10 @@ int tt_replicate_tile_dim(tt_session* s, const double* in, const int64_t* tile_e
 
 /* ---- diagnostics ------------------------------------------------------- */
 /* Force the reduction kernel path (tests / A-B measurement): 0 = best
- * eligible (default), 1 = TMA-ring fused kernel, 2 = register-tree fused
- * kernel, 3 = generic program interpreter.  Results are identical on every
- * path; only speed differs. */
+ * eligible (default), 1 = TMA-ring fused kernel (whole-tile tree),
+ * 2 = register-tree fused kernel, 3 = generic program interpreter,
+ * 4 = TMA-ring sliding-window kernel.  Results are identical on every path;
+ * only speed differs. */
 int tt_set_kernel_path(int path);
 int tt_kernel_path(void);
 

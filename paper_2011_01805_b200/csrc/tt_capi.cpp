@@ -785,7 +785,7 @@ int tt_replicate_tile_dim(tt_session* s, const double* in, const int64_t* tile_e
 
 int tt_set_kernel_path(int path) {
   return guarded([&] {
-    if (path < 0 || path > 3) invalid_argument("kernel path must be 0..3");
+    if (path < 0 || path > 4) invalid_argument("kernel path must be 0..4");
     set_kernel_path(path);
   });
 }

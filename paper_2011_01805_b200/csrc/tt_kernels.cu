@@ -852,6 +852,183 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   }
 }
 
+// ---- sliding-window variant ---------------------------------------------------------
+// When the power-of-two schedule's reach H = (t-1)*stride is at most one
+// chunk (c5 dims 2 and 3: H = 992 and 31 slots), output slot j only depends on
+// folded slots j .. j+H (cyclic), so chunk r is finalised right after chunk
+// r+1 has been folded, from [chunk r | first H slots of chunk r+1] (the last
+// chunk wraps to a saved head of chunk 0).  Shared memory then holds two
+// folded chunks + two H-slot halos (~48 KiB) instead of the whole 128 KiB
+// tile, and the TMA ring gets the rest: ~2x the bytes in flight, and the tree
+// work is spread between the fold steps instead of stalling the SM per group.
+// Level k of the schedule runs on the shrinking range [0, CH + H - sum_{i<=k} d_i).
+
+constexpr int kWinVmax = 8;  // (CH + H) / consumers, rounded up: (2048 + 2047) / 512
+
+template <bool HAS_B>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    group_tma_win_kernel(const __grid_constant__ GroupParams p, const double* __restrict__ A,
+                         const double* __restrict__ B, double* __restrict__ OUT, int nstages,
+                         int halo) {
+  extern __shared__ __align__(128) double smem[];
+  const int s = static_cast<int>(p.s);
+  const bool b_stream = HAS_B && p.g.bstep != 0;
+  const int stage_doubles = kTmaChunk * (b_stream ? 2 : 1);
+  double* cbuf = smem;                         // 2 folded chunks (ping-pong)
+  double* work = smem + 2 * kTmaChunk;         // chunk r-1 copy + halo: CH + H
+  double* head = work + kTmaChunk + halo;      // first H slots of chunk 0
+  // TMA destinations must stay 16-byte aligned: start the ring on a 128 B line
+  double* ring = smem + 3 * kTmaChunk + ((2 * halo + 15) / 16) * 16;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<int64_t>(nstages) * stage_doubles);
+  uint64_t* empty = full + nstages;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t first = p.ops[0].x;
+  const int64_t count = p.ops[0].y;
+  const int nchunks = s / kTmaChunk;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kTmaConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kTmaConsumerWarps) {  // ---- producer (as in group_tma_kernel) ----
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_first();
+      const uint64_t pol_b = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t chunk_bytes = kTmaChunk * sizeof(double);
+      for (uint64_t v = blockIdx.x; v < static_cast<uint64_t>(p.g.groups); v += gridDim.x) {
+        const GroupBase gb = group_base(p, v);
+        for (int r = 0; r < nchunks; ++r) {
+          for (int64_t c = 0; c < count; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            double* dst = ring + static_cast<int64_t>(stage) * stage_doubles;
+            mbar_arrive_expect_tx(&full[stage], chunk_bytes * (b_stream ? 2 : 1));
+            bulk_g2s(dst, A + (gb.a + (first + c) * p.g.astep) * p.s + r * kTmaChunk, chunk_bytes,
+                     &full[stage], pol_a);
+            if (b_stream)
+              bulk_g2s(dst + kTmaChunk, B + (gb.b + (first + c) * p.g.bstep) * p.s + r * kTmaChunk,
+                       chunk_bytes, &full[stage], pol_b);
+            if (++stage == nstages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  const int tid = threadIdx.x;
+  int stage = 0;
+  uint32_t phase = 0;
+  // sum of the level offsets up to and including level k
+  int64_t reach[32];
+  {
+    int64_t acc = 0;
+    for (int lv = 0; lv < p.nlevels; ++lv) {
+      acc += p.rots[lv];
+      reach[lv] = acc;
+    }
+  }
+  // finalise chunk `rc` (folded values in `src`), halo = first H slots of `hal`
+  auto finalise = [&](int rc, const double* src, const double* hal, double* out) {
+    for (int j = tid; j < kTmaChunk; j += kTmaConsumers) work[j] = src[j];
+    for (int j = tid; j < halo; j += kTmaConsumers) work[kTmaChunk + j] = hal[j];
+    consumer_sync();
+    int range = kTmaChunk + halo;
+    for (int lv = 0; lv < p.nlevels; ++lv) {
+      const int d = static_cast<int>(p.rots[lv]);
+      const int nr = kTmaChunk + halo - static_cast<int>(reach[lv]);
+      double val[kWinVmax];
+#pragma unroll
+      for (int i = 0; i < kWinVmax; ++i) {
+        const int j = i * kTmaConsumers + tid;
+        if (j < nr) val[i] = dadd(work[j], work[j + d]);
+      }
+      consumer_sync();
+      if (lv + 1 < p.nlevels) {
+#pragma unroll
+        for (int i = 0; i < kWinVmax; ++i) {
+          const int j = i * kTmaConsumers + tid;
+          if (j < nr) work[j] = val[i];
+        }
+        consumer_sync();
+      } else {
+#pragma unroll
+        for (int i = 0; i < kWinVmax; ++i) {
+          const int j = i * kTmaConsumers + tid;
+          if (j < nr) out[static_cast<int64_t>(rc) * kTmaChunk + j] = val[i];
+        }
+      }
+      range = nr;
+    }
+    (void)range;
+  };
+
+  for (uint64_t v = blockIdx.x; v < static_cast<uint64_t>(p.g.groups); v += gridDim.x) {
+    const GroupBase gb = group_base(p, v);
+    double* out = OUT + gb.out * p.s;
+    for (int r = 0; r < nchunks; ++r) {
+      double2 acc[kTmaPairsPerThread];
+      double2 w[kTmaPairsPerThread];
+      if (HAS_B && !b_stream) {
+        const double* pb = B + (gb.b + first * p.g.bstep) * p.s + r * kTmaChunk;
+#pragma unroll
+        for (int k = 0; k < kTmaPairsPerThread; ++k)
+          w[k] = __ldg(reinterpret_cast<const double2*>(pb) + tid + k * kTmaConsumers);
+      }
+      for (int64_t c = 0; c < count; ++c) {
+        mbar_wait(&full[stage], phase);
+        const double2* st = reinterpret_cast<const double2*>(ring + static_cast<int64_t>(stage) * stage_doubles);
+#pragma unroll
+        for (int k = 0; k < kTmaPairsPerThread; ++k) {
+          const double2 x = st[tid + k * kTmaConsumers];
+          double2 prod;
+          if (HAS_B) {
+            const double2 y = b_stream ? st[kTmaChunk / 2 + tid + k * kTmaConsumers] : w[k];
+            prod = make_double2(dmul(x.x, y.x), dmul(x.y, y.y));
+          } else {
+            prod = x;
+          }
+          if (c == 0) {
+            acc[k] = prod;
+          } else {
+            acc[k].x = dadd(acc[k].x, prod.x);
+            acc[k].y = dadd(acc[k].y, prod.y);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == nstages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      double* cb = cbuf + (r & 1) * kTmaChunk;
+      double2* dt = reinterpret_cast<double2*>(cb);
+#pragma unroll
+      for (int k = 0; k < kTmaPairsPerThread; ++k) dt[tid + k * kTmaConsumers] = acc[k];
+      consumer_sync();
+      if (r == 0) {  // keep chunk 0's head for the cyclic wrap of the last chunk
+        for (int j = tid; j < halo; j += kTmaConsumers) head[j] = cb[j];
+      } else {
+        finalise(r - 1, cbuf + ((r - 1) & 1) * kTmaChunk, cb, out);
+      }
+      consumer_sync();
+    }
+    finalise(nchunks - 1, cbuf + ((nchunks - 1) & 1) * kTmaChunk, head, out);
+    consumer_sync();
+  }
+}
+
 // Generic interpreter: any program (ltr/rtl schedules, boundary split,
 // replication).  Logical buffers map onto nbuf+1 physical tiles; an in-place
 // ROTADD writes the spare tile and swaps it in, so one barrier per op.
@@ -1346,7 +1523,7 @@ int forced_path() {
   if (v >= 0) return v;
   const char* e = std::getenv("TT_KERNEL_PATH");
   const std::string s(e ? e : "");
-  v = s == "tma" ? 1 : s == "regs" ? 2 : s == "generic" ? 3 : 0;
+  v = s == "tma" ? 1 : s == "regs" ? 2 : s == "generic" ? 3 : s == "window" ? 4 : 0;
   g_forced_path.store(v, std::memory_order_relaxed);
   return v;
 }
@@ -1519,6 +1696,25 @@ void run_tma(const LaunchCtx& c, const GroupParams& p, const double* ta, const d
 }
 
 template <bool HAS_B>
+void run_tma_win(const LaunchCtx& c, const GroupParams& p, int halo, const double* ta,
+                 const double* tb, double* tout) {
+  const bool b_stream = HAS_B && p.g.bstep != 0;
+  const size_t stage_bytes = static_cast<size_t>(kTmaChunk) * sizeof(double) * (b_stream ? 2 : 1);
+  const size_t fixed = (3 * static_cast<size_t>(kTmaChunk) + ((2 * halo + 15) / 16) * 16) * sizeof(double);
+  int nstages = static_cast<int>((c.smem_optin - fixed) / (stage_bytes + 16));
+  nstages = std::min(nstages, 16);
+  if (nstages < 2) invalid_argument("window path needs two ring stages");
+  const size_t smem = fixed + nstages * (stage_bytes + 16);
+  auto k = group_tma_win_kernel<HAS_B>;
+  check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)),
+             "smem attribute");
+  const int grid = grid_for(c, (const void*)k, kTmaThreads, smem, p.g.groups);
+  k<<<grid, kTmaThreads, smem, c.stream>>>(p, ta, tb, tout, nstages, halo);
+  post_launch(c, "group tma window kernel");
+}
+
+template <bool HAS_B>
 void dispatch_tma(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
                   double* tout) {
   const int64_t v = p.s / kTmaConsumers;
@@ -1588,7 +1784,12 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
         dispatch_pow2<false, false>(c, p2, threads, vmax, tile_bytes, tout, nullptr, tout);
       return;
     }
-    if (tma_ok)
+    int64_t halo = 0;
+    for (int i = 0; i < p.nlevels; ++i) halo += p.rots[i];
+    const bool win_ok = tma_ok && halo <= kTmaChunk && (force == 0 || force == 4);
+    if (win_ok)
+      run_tma_win<HAS_B>(c, p, static_cast<int>(halo), ta, tb, tout);
+    else if (tma_ok)
       dispatch_tma<HAS_B>(c, p, ta, tb, tout);
     else if (vec)
       dispatch_pow2<HAS_B, true>(c, p, threads, vmax, tile_bytes, ta, tb, tout);

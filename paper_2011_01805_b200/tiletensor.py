@@ -653,7 +653,7 @@ def shard_plan(shape: TileTensorShape, shard_dim: int, world: int, rank: int):
     return b.value, e.value, TileTensorShape.from_c(out)
 
 
-KERNEL_PATHS = {"auto": 0, "tma": 1, "regs": 2, "generic": 3}
+KERNEL_PATHS = {"auto": 0, "tma": 1, "regs": 2, "generic": 3, "window": 4}
 
 
 def set_kernel_path(path: str) -> None:

@@ -284,7 +284,7 @@ def test_depth_exhaustion(gpu):
         tt.tt_mul(sq, sq)
 
 
-@pytest.mark.parametrize("path", ["auto", "tma", "regs", "generic"])
+@pytest.mark.parametrize("path", ["auto", "tma", "regs", "generic", "window"])
 def test_fused_large_tiles_every_path(gpu, oracle, path):
     """Config-5-like tiles (s = 16384 and 8192): every reduction kernel path
     (TMA ring, register tree, generic interpreter) and both group regimes
