@@ -938,8 +938,38 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       reach[lv] = acc;
     }
   }
+  // stride-1 schedules with reach < 32 (every offset < 32): warp w owns rows
+  // w*4 .. w*4+3 of 32 slots plus the next row as halo; all levels run in
+  // registers with shuffles (partner of (row i, lane l) at offset d is
+  // (i, l+d) or (i+1, l+d-32)), no barrier and no shared-memory round trip.
+  const bool shfl_tree = halo < 32;
+  auto finalise_shfl = [&](int rc, const double* src, const double* hal, double* out) {
+    const int w = tid >> 5;
+    double v[5];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = src[w * 128 + i * 32 + lane];
+    v[4] = (w + 1 < kTmaConsumerWarps) ? src[(w + 1) * 128 + lane] : (lane < halo ? hal[lane] : 0.0);
+    for (int lv = 0; lv < p.nlevels; ++lv) {
+      const int d = static_cast<int>(p.rots[lv]);
+      const int srcl = (lane + d) & 31;
+      const bool same_row = lane + d < 32;
+      double sh[5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) sh[i] = __shfl_sync(0xffffffffu, v[i], srcl);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = dadd(v[i], same_row ? sh[i] : sh[i + 1]);
+      v[4] = dadd(v[4], sh[4]);  // only its low lanes stay meaningful; never stored
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[static_cast<int64_t>(rc) * kTmaChunk + w * 128 + i * 32 + lane] = v[i];
+  };
+
   // finalise chunk `rc` (folded values in `src`), halo = first H slots of `hal`
   auto finalise = [&](int rc, const double* src, const double* hal, double* out) {
+    if (shfl_tree) {
+      finalise_shfl(rc, src, hal, out);
+      return;
+    }
     for (int j = tid; j < kTmaChunk; j += kTmaConsumers) work[j] = src[j];
     for (int j = tid; j < halo; j += kTmaConsumers) work[kTmaChunk + j] = hal[j];
     consumer_sync();
