@@ -472,7 +472,10 @@ int tt_pack(tt_session* s, const double* dense, const tt_shape* shape, double* t
     require_slots(s, sh, "pack");
     check_tiles_addressable(sh);
     std::lock_guard<std::mutex> lk(s->mu);
-    launch_pack(ctx_of(s), sh, s->slots, dense, tiles);
+    const LaunchCtx c = ctx_of(s);
+    const int path = kernel_path();  // 2 (regs) / 3 (generic) force the gather kernel
+    if ((path == 2 || path == 3) || !launch_pack_tma(c, sh, s->slots, dense, tiles))
+      launch_pack(c, sh, s->slots, dense, tiles);
   });
 }
 
@@ -483,7 +486,10 @@ int tt_unpack(tt_session* s, const tt_shape* shape, const double* tiles, double*
     require_slots(s, sh, "unpack");
     check_tiles_addressable(sh);
     std::lock_guard<std::mutex> lk(s->mu);
-    launch_unpack(ctx_of(s), sh, s->slots, tiles, dense);
+    const LaunchCtx c = ctx_of(s);
+    const int path = kernel_path();
+    if ((path == 2 || path == 3) || !launch_unpack_tma(c, sh, s->slots, tiles, dense))
+      launch_unpack(c, sh, s->slots, tiles, dense);
   });
 }
 

@@ -39,6 +39,12 @@ void launch_pack(const LaunchCtx& c, const Shape& shape, int64_t s, const double
                  double* tiles);
 void launch_unpack(const LaunchCtx& c, const Shape& shape, int64_t s, const double* tiles,
                    double* dense);
+// TMA tensor-map pack / unpack (tt_tma_pack.cu); return false when the shape
+// is not eligible (replication, `~`, relaxed, rank > 5, odd last extent...).
+bool launch_pack_tma(const LaunchCtx& c, const Shape& shape, int64_t s, const double* dense,
+                     double* tiles);
+bool launch_unpack_tma(const LaunchCtx& c, const Shape& shape, int64_t s, const double* tiles,
+                       double* dense);
 // out tile l = A[l mod ea] (op) B[l mod eb]   (tile_tensor.hpp:259-270)
 void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shape& a,
                         const Shape& b, int64_t s, const double* ta, const double* tb,

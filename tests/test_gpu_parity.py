@@ -316,3 +316,37 @@ def test_fused_large_tiles_every_path(gpu, oracle, path):
                 assert_bitwise(tt.tt_sum(A, dim).tiles(), wt2, f"{path} sum {xa} dim {dim}")
     finally:
         tt.set_kernel_path("auto")
+
+
+@pytest.mark.parametrize("path", ["auto", "regs"])
+def test_pack_unpack_plain_shapes_tma_and_gather(gpu, oracle, path):
+    """Plain shapes take the TMA tensor-map pack/unpack (auto); `regs` forces
+    the gather kernels.  Edge tiles exercise TMA out-of-bounds zero fill."""
+    rng = random.Random(1234)
+    nrng = np.random.default_rng(1234)
+    tt.set_kernel_path(path)
+    try:
+        for it in range(150):
+            s = rng.choice([16, 64, 256, 1024])
+            S = session(s)
+            rank = rng.randint(1, 4)
+            shape = random_pack_shape(rng, s, rank, allow_replication=False)
+            dims = list(shape.dims())
+            # make the innermost extent even half the time (TMA eligibility)
+            if rng.random() < 0.5 and dims[-1].n % 2:
+                dims[-1] = DimSpec(dims[-1].n + 1, 1, dims[-1].t)
+            shape = TileTensorShape(dims)
+            a = random_tensor(nrng, shape.tensor_extents())
+            t = tt.pack(a, shape, S)
+            assert_bitwise(t.tiles(), oracle.pack(a, shape, s), f"{path} pack {format_shape(shape)}")
+            assert_bitwise(tt.unpack(t), a, f"{path} unpack {format_shape(shape)}")
+        for text, s in [("[100/16,200/32]", 512), ("[1024/64,4096/128]", 8192),
+                        ("[50/16,20/2,255/32]", 1024), ("[13/4,30/8,6/2]", 64)]:
+            shape = parse_shape(text)
+            S = session(s)
+            a = random_tensor(nrng, shape.tensor_extents())
+            t = tt.pack(a, shape, S)
+            assert_bitwise(t.tiles(), oracle.pack(a, shape, s), f"{path} pack {text}")
+            assert_bitwise(tt.unpack(t), a, f"{path} unpack {text}")
+    finally:
+        tt.set_kernel_path("auto")
