@@ -1260,7 +1260,8 @@ constexpr int kGemmSlots = 64;
 constexpr int kGemmBlk = 16;   // block rows (groups along ia)
 constexpr int kGemmSubR = 8;
 constexpr int kGemmSubC = 4;
-constexpr int kGemmStages = 4;
+constexpr int kGemmStages = 3;  // super-stages in flight
+constexpr int kGemmPair = 2;    // fold steps per super-stage (one barrier per pair)
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
@@ -1281,10 +1282,9 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
                      double* __restrict__ OUT) {
   constexpr int kThreads = 2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32;
   constexpr int kSubCols = BC / kGemmSubC;
+  constexpr int kStep = kGemmBlk * kGemmSlots + BC * kGemmSlots;  // doubles per fold step
   extern __shared__ __align__(16) double gsm[];
-  // kGemmStages-deep ring of (A block chunk, B block chunk)
-  auto sA = reinterpret_cast<double(*)[kGemmBlk][kGemmSlots]>(gsm);
-  auto sB = reinterpret_cast<double(*)[BC][kGemmSlots]>(gsm + kGemmStages * kGemmBlk * kGemmSlots);
+  // ring of kGemmStages super-stages, each holding kGemmPair fold steps
   const int64_t s = p.s;
   const int64_t first = p.ops[0].x;
   const int64_t count = p.ops[0].y;
@@ -1293,6 +1293,7 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
   const int slot = (warp & 1) * 32 + lane;     // slot within the 64-slot chunk
   const int sub = warp >> 1;                   // 8x4 sub-block of the 16 x BC groups
   const int r0 = (sub / kSubCols) * kGemmSubR, c0 = (sub % kSubCols) * kGemmSubC;
+  const int64_t nsuper = (count + kGemmPair - 1) / kGemmPair;
   for (uint64_t u = blockIdx.x; u < static_cast<uint64_t>(bs.units); u += gridDim.x) {
     uint64_t t = u;
     const uint64_t t1 = fdiv(t, bs.div_nbq);
@@ -1310,53 +1311,66 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
     const int64_t a_row = bs.a_ia * s, b_col = bs.b_ib * s;
     const int64_t sa = p.g.astep * s, sb = p.g.bstep * s;
 
-    auto stage = [&](int buf, int64_t c) {
-      // 16 (resp. BC) rows x 32 segments of 16 B per operand
-      for (int e = tid; e < kGemmBlk * 32; e += kThreads) {
-        const int row = e >> 5, seg = e & 31;
-        const int ra = row < np ? row : np - 1;
-        cp_async16(&sA[buf][row][seg * 2], a0 + c * sa + ra * a_row + seg * 2);
-      }
-      for (int e = tid; e < BC * 32; e += kThreads) {
-        const int row = e >> 5, seg = e & 31;
-        const int rb = row < nq ? row : nq - 1;
-        cp_async16(&sB[buf][row][seg * 2], b0 + c * sb + rb * b_col + seg * 2);
+    auto stage = [&](int buf, int64_t sup) {
+#pragma unroll
+      for (int h = 0; h < kGemmPair; ++h) {
+        const int64_t c = sup * kGemmPair + h;
+        if (c < count) {
+          double* sA = gsm + (static_cast<int64_t>(buf) * kGemmPair + h) * kStep;
+          double* sB = sA + kGemmBlk * kGemmSlots;
+          for (int e = tid; e < kGemmBlk * 32; e += kThreads) {
+            const int row = e >> 5, seg = e & 31;
+            const int ra = row < np ? row : np - 1;
+            cp_async16(sA + row * kGemmSlots + seg * 2, a0 + c * sa + ra * a_row + seg * 2);
+          }
+          for (int e = tid; e < BC * 32; e += kThreads) {
+            const int row = e >> 5, seg = e & 31;
+            const int rb = row < nq ? row : nq - 1;
+            cp_async16(sB + row * kGemmSlots + seg * 2, b0 + c * sb + rb * b_col + seg * 2);
+          }
+        }
       }
       cp_async_commit();
     };
 
     double acc[kGemmSubR][kGemmSubC];
-    // prologue: steps 0 .. kGemmStages-2 in flight (empty groups keep the count uniform)
 #pragma unroll
     for (int k = 0; k < kGemmStages - 1; ++k) {
-      if (k < count)
+      if (k < nsuper)
         stage(k, k);
       else
         cp_async_commit();
     }
-    for (int64_t c = 0; c < count; ++c) {
-      const int buf = static_cast<int>(c % kGemmStages);
-      cp_async_wait<kGemmStages - 2>();  // step c has landed
-      __syncthreads();                   // ...for every thread; buffer (c-1) is free
-      if (c + kGemmStages - 1 < count)
-        stage(static_cast<int>((c + kGemmStages - 1) % kGemmStages), c + kGemmStages - 1);
+    for (int64_t sup = 0; sup < nsuper; ++sup) {
+      const int buf = static_cast<int>(sup % kGemmStages);
+      cp_async_wait<kGemmStages - 2>();  // super-stage `sup` has landed
+      __syncthreads();                   // ...for every thread; the previous buffer is free
+      if (sup + kGemmStages - 1 < nsuper)
+        stage(static_cast<int>((sup + kGemmStages - 1) % kGemmStages), sup + kGemmStages - 1);
       else
         cp_async_commit();
-      double a[kGemmSubR], b[kGemmSubC];
 #pragma unroll
-      for (int i = 0; i < kGemmSubR; ++i) a[i] = sA[buf][r0 + i][slot];
+      for (int h = 0; h < kGemmPair; ++h) {
+        const int64_t c = sup * kGemmPair + h;
+        if (c >= count) break;
+        const double* sA = gsm + (static_cast<int64_t>(buf) * kGemmPair + h) * kStep;
+        const double* sB = sA + kGemmBlk * kGemmSlots;
+        double a[kGemmSubR], b[kGemmSubC];
 #pragma unroll
-      for (int k = 0; k < kGemmSubC; ++k) b[k] = sB[buf][c0 + k][slot];
-      if (c == 0) {
+        for (int i = 0; i < kGemmSubR; ++i) a[i] = sA[(r0 + i) * kGemmSlots + slot];
 #pragma unroll
-        for (int i = 0; i < kGemmSubR; ++i)
+        for (int k = 0; k < kGemmSubC; ++k) b[k] = sB[(c0 + k) * kGemmSlots + slot];
+        if (c == 0) {
 #pragma unroll
-          for (int k = 0; k < kGemmSubC; ++k) acc[i][k] = dmul(a[i], b[k]);
-      } else {
+          for (int i = 0; i < kGemmSubR; ++i)
 #pragma unroll
-        for (int i = 0; i < kGemmSubR; ++i)
+            for (int k = 0; k < kGemmSubC; ++k) acc[i][k] = dmul(a[i], b[k]);
+        } else {
 #pragma unroll
-          for (int k = 0; k < kGemmSubC; ++k) acc[i][k] = dadd(acc[i][k], dmul(a[i], b[k]));
+          for (int i = 0; i < kGemmSubR; ++i)
+#pragma unroll
+            for (int k = 0; k < kGemmSubC; ++k) acc[i][k] = dadd(acc[i][k], dmul(a[i], b[k]));
+        }
       }
     }
     cp_async_wait<0>();
@@ -1371,6 +1385,104 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
             OUT[(gb.out + (pb * kGemmBlk + r0 + i) * bs.out_ia + (qb * BC + c0 + k) * bs.out_ib) *
                     s + j] = acc[i][k];
     }
+  }
+}
+
+// ---- tree-only passes (phase 2 of a two-phase reduction), in place on OUT ----------------
+// (A) column-local: the summed dim is the first (s == t * stride), so each
+// column c of the tile viewed as [t][stride] is one cyclic sequence of t
+// values; a thread loads its column, runs the power-of-two levels in
+// registers (v'[m] = v[m] + v[(m + e) mod t]), stores it back.  Coalesced
+// across threads (consecutive columns), no shared memory, no barrier.
+template <int T>
+__global__ void __launch_bounds__(256) col_tree_kernel(double* __restrict__ tiles, int64_t n_tiles,
+                                                       int64_t stride, int64_t s, FastDiv64 cdiv) {
+  const uint64_t total = static_cast<uint64_t>(n_tiles) * stride;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t tile = fdiv(w, cdiv);
+    const int64_t col = static_cast<int64_t>(w - tile * cdiv.d);
+    double* base = tiles + tile * s + col;
+    double v[T];
+#pragma unroll
+    for (int m = 0; m < T; ++m) v[m] = base[m * stride];
+#pragma unroll
+    for (int e = 1; e < T; e *= 2) {
+      double nv[T];
+#pragma unroll
+      for (int m = 0; m < T; ++m) nv[m] = dadd(v[m], v[(m + e) % T]);
+#pragma unroll
+      for (int m = 0; m < T; ++m) v[m] = nv[m];
+    }
+#pragma unroll
+    for (int m = 0; m < T; ++m) base[m * stride] = v[m];
+  }
+}
+
+// (B) row-shift: tile as rows of 32 slots; a warp finalises 16 rows and holds
+// HR more rows of halo (reach <= HR*32 slots), read straight from L2/HBM
+// (cyclic over the tile).  An offset d < 32 is a shuffle with carry into the
+// next row; an offset 32*D is a register row shift.  Rows are updated in
+// ascending order in place, so each update still reads the previous level's
+// value of the rows below.  Valid rows shrink by the level's reach.
+template <int NR>
+__device__ __forceinline__ void row_shift(double (&v)[NR], int D) {
+#pragma unroll
+  for (int i = 0; i < NR; ++i)
+    if (i + D < NR) v[i] = dadd(v[i], v[i + D]);
+}
+
+// Reads the folded tiles from `in` (scratch) and writes `out`: warps read
+// halo rows owned by other warps, so the pass cannot run in place.
+template <int HR>
+__global__ void __launch_bounds__(256) row_tree_kernel(const double* __restrict__ in,
+                                                       double* __restrict__ out, int64_t n_tiles,
+                                                       int64_t s, int nlevels, int4 lv0, int4 lv1) {
+  constexpr int R = 16;
+  constexpr int NR = R + HR;
+  const int lane = threadIdx.x & 31;
+  const int rows = static_cast<int>(s / 32);
+  const int blocks_per_tile = rows / R;
+  const uint64_t total = static_cast<uint64_t>(n_tiles) * blocks_per_tile;
+  const int lvl[8] = {lv0.x, lv0.y, lv0.z, lv0.w, lv1.x, lv1.y, lv1.z, lv1.w};
+  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+       u < total; u += static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5)) {
+    const uint64_t tile = u / blocks_per_tile;
+    const int rb = static_cast<int>(u - tile * blocks_per_tile) * R;
+    const double* t = in + tile * s;
+    double* o = out + tile * s;
+    double v[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      int row = rb + i;
+      if (row >= rows) row -= rows;  // cyclic halo
+      v[i] = __ldg(t + row * 32 + lane);
+    }
+    for (int k = 0; k < nlevels; ++k) {
+      const int d = lvl[k];
+      if (d < 32) {
+        const int src = (lane + d) & 31;
+        const bool same = lane + d < 32;
+        double cur = __shfl_sync(0xffffffffu, v[0], src);
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+          const double nxt = (i + 1 < NR) ? __shfl_sync(0xffffffffu, v[i + 1], src) : 0.0;
+          v[i] = dadd(v[i], same ? cur : nxt);
+          cur = nxt;
+        }
+      } else {
+        switch (d >> 5) {
+          case 1: row_shift<NR>(v, 1); break;
+          case 2: row_shift<NR>(v, 2); break;
+          case 4: row_shift<NR>(v, 4); break;
+          case 8: row_shift<NR>(v, 8); break;
+          case 16: row_shift<NR>(v, 16); break;
+          default: break;  // excluded by the host eligibility check
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) o[(rb + i) * 32 + lane] = v[i];
   }
 }
 
@@ -1649,7 +1761,8 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
   bs.div_nbp = make_div64(static_cast<uint64_t>(bs.nbp));
   bs.div_chunks = make_div64(static_cast<uint64_t>(bs.chunks));
   if (gemm) {
-    const size_t smem = static_cast<size_t>(kGemmStages) * (kGemmBlk + Q) * kGemmSlots * sizeof(double);
+    const size_t smem =
+        static_cast<size_t>(kGemmStages) * kGemmPair * (kGemmBlk + Q) * kGemmSlots * sizeof(double);
     const void* k = Q == 16 ? (const void*)fold_gemm_kernel<16> : (const void*)fold_gemm_kernel<8>;
     check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)),
@@ -1758,6 +1871,86 @@ void dispatch_tma(const LaunchCtx& c, const GroupParams& p, const double* ta, co
     run_tma<32, HAS_B>(c, p, ta, tb, tout);
 }
 
+// Tree-only passes (phase 2), register-resident.  kind 1 = column-local (in
+// place on OUT), kind 2 = row-shift (reads the folded tiles from a separate
+// buffer, writes OUT); 0 = none applies.
+struct TreePass {
+  int kind = 0;
+  int hr = 0;
+  int64_t stride0 = 0, t = 0;
+};
+
+TreePass plan_tree_pass(const GroupParams& p2, int64_t s) {
+  TreePass tp;
+  const int L = p2.nlevels;
+  if (L < 1 || L > 8) return tp;
+  const int64_t stride0 = p2.rots[0];
+  for (int i = 1; i < L; ++i)
+    if (p2.rots[i] != stride0 << i) return tp;
+  const int64_t t = int64_t{1} << L;
+  tp.stride0 = stride0;
+  tp.t = t;
+  if (t * stride0 == s && t <= 32) {
+    tp.kind = 1;
+    return tp;
+  }
+  if (s % (32 * 16) != 0) return tp;
+  int64_t reach = 0;
+  for (int i = 0; i < L; ++i) {
+    const int64_t d = p2.rots[i];
+    if (!(d < 32 || (d % 32 == 0 && d / 32 <= 16 && ((d / 32) & (d / 32 - 1)) == 0))) return tp;
+    reach += d;
+  }
+  const int hr = static_cast<int>((reach + 31) / 32);
+  if (hr > 16) return tp;
+  tp.kind = 2;
+  tp.hr = hr;
+  return tp;
+}
+
+void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2, int64_t n_tiles,
+                   int64_t s, const double* folded, double* tout) {
+  if (tp.kind == 1) {  // in place: folded == tout
+    const int64_t stride0 = tp.stride0;
+    const uint64_t total = static_cast<uint64_t>(n_tiles) * stride0;
+    const FastDiv64 cd = make_div64(static_cast<uint64_t>(stride0));
+    const int64_t work = static_cast<int64_t>((total + 255) / 256);
+#define TT_COL(TV)                                                                        \
+  {                                                                                      \
+    const int grid = grid_for(c, (const void*)col_tree_kernel<TV>, 256, 0, work);        \
+    col_tree_kernel<TV><<<grid, 256, 0, c.stream>>>(tout, n_tiles, stride0, s, cd);      \
+  }
+    switch (tp.t) {
+      case 2: TT_COL(2) break;
+      case 4: TT_COL(4) break;
+      case 8: TT_COL(8) break;
+      case 16: TT_COL(16) break;
+      default: TT_COL(32) break;
+    }
+#undef TT_COL
+    post_launch(c, "column tree pass");
+    return;
+  }
+  const int L = p2.nlevels;
+  int lv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < L; ++i) lv[i] = static_cast<int>(p2.rots[i]);
+  const int4 lv0 = make_int4(lv[0], lv[1], lv[2], lv[3]);
+  const int4 lv1 = make_int4(lv[4], lv[5], lv[6], lv[7]);
+  const int64_t warps = n_tiles * (s / 32 / 16);
+  const int64_t work = (warps + 7) / 8;
+  if (tp.hr <= 1) {
+    const int grid = grid_for(c, (const void*)row_tree_kernel<1>, 256, 0, work);
+    row_tree_kernel<1><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
+  } else if (tp.hr <= 8) {
+    const int grid = grid_for(c, (const void*)row_tree_kernel<8>, 256, 0, work);
+    row_tree_kernel<8><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
+  } else {
+    const int grid = grid_for(c, (const void*)row_tree_kernel<16>, 256, 0, work);
+    row_tree_kernel<16><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
+  }
+  post_launch(c, "row tree pass");
+}
+
 template <bool HAS_B>
 void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
                          const double* ta, const double* tb, double* tout) {
@@ -1792,6 +1985,18 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
     if ((g.groups < static_cast<int64_t>(c.sm_count) * std::min<int64_t>(per_sm, 4) ||
          (matmul_like && force != 1 && force != 2)) &&
         prog.ops[0].y > 1) {
+      // phase 2 plan first: the row-shift pass needs the folded tiles in a
+      // separate buffer, so phase 1 then folds into session scratch
+      TreePass tpass;
+      if (force == 0) tpass = plan_tree_pass(p, s);
+      double* fold_dst = tout;
+      if (tpass.kind == 2)
+        fold_dst = c.scratch(c.scratch_owner, static_cast<size_t>(g.groups) * tile_bytes);
+      if (tpass.kind != 0) {
+        launch_fold_best<HAS_B>(c, p, ta, tb, fold_dst);
+        run_tree_pass(c, tpass, p, g.groups, s, fold_dst, tout);
+        return;
+      }
       launch_fold_best<HAS_B>(c, p, ta, tb, tout);
       // phase 2 reads its group's folded tile from OUT: a = out tile index
       GroupParams p2 = p;
