@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <optional>
 #include <span>
 #include <string>
@@ -313,6 +314,42 @@ int ref_logical_indices(const tt_shape* sh, const int64_t* tile_index, int64_t h
 }
 
 // ---- timed CPU baseline helpers (bench.py) ----------------------------------
+// A persistent session holding W packed once (W is a fixed operand, like a
+// weight), so a timed step covers: pack X, tt_sum(tt_mul(X, W), k), unpack.
+namespace {
+std::unique_ptr<Session> g_bench_session;
+std::unique_ptr<TileTensor> g_bench_w;
+}  // namespace
+
+int ref_bench_prepare_w(const double* dense_w, const tt_shape* sw, int64_t slots) {
+  return guard([&] {
+    g_bench_w.reset();
+    g_bench_session = std::make_unique<Session>(slots, 8);
+    g_bench_w = std::make_unique<TileTensor>(pack(dense_of(dense_w, sw), to_ref(sw), *g_bench_session));
+  });
+}
+
+int ref_bench_step(const double* dense_x, const tt_shape* sx, const int* dims, int ndims,
+                   double* secs) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    if (!g_bench_w) throw std::logic_error("ref_bench_prepare_w first");
+    Session& session = *g_bench_session;
+    auto t0 = clk::now();
+    const TileTensor x = pack(dense_of(dense_x, sx), to_ref(sx), session);
+    auto t1 = clk::now();
+    std::vector<TileTensor> outs;
+    for (int k = 0; k < ndims; ++k) outs.push_back(tt_sum(tt_mul(x, *g_bench_w), dims[k]));
+    auto t2 = clk::now();
+    double sink = 0;
+    for (const auto& o : outs) sink += unpack(o).values()[0];
+    auto t3 = clk::now();
+    secs[0] = std::chrono::duration<double>(t1 - t0).count();
+    secs[1] = std::chrono::duration<double>(t2 - t1).count();
+    secs[2] = std::chrono::duration<double>(t3 - t2).count();
+    secs[3] = sink;
+  });
+}
 // One call = pack a seeded dense tensor, then tt_sum(tt_mul(X, W), dim) for each
 // dim in `dims`, then unpack each result, exactly through the reference API.
 // Returns wall seconds of each phase in secs[0..2] (pack, mul+sum, unpack).
