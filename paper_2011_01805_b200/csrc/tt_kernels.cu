@@ -1275,7 +1275,13 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // BC = block columns (groups along ib): 16 (512 threads) or 8 (256 threads,
 // more and smaller work units when the 16 x 16 grid would leave SMs idle).
-template <int BC>
+// COLTREE: the reduction is over the first dim with t = 16 (s = 16 * stride):
+// a 64-slot unit is then 16 rows x 4 consecutive columns (row = in-tile index
+// of the summed dim), each warp holds 16 rows x 2 columns (lane = row*2 + c),
+// i.e. complete cyclic columns, and the power-of-two tree runs as 4 shuffle
+// levels (partner lane (l + 2e) mod 32 == row (r + e) mod 16) before the
+// final store -- no separate tree pass, no round trip of the folded tile.
+template <int BC, bool COLTREE>
 __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32, BC == 8 ? 2 : 1)
     fold_gemm_kernel(const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
                      const double* __restrict__ A, const double* __restrict__ B,
@@ -1305,9 +1311,20 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
     const GroupBase gb = group_base(p, rest);
     const int np = static_cast<int>(bs.ext_ia - pb * kGemmBlk < kGemmBlk ? bs.ext_ia - pb * kGemmBlk : kGemmBlk);
     const int nq = static_cast<int>(bs.ext_ib - qb * BC < BC ? bs.ext_ib - qb * BC : BC);
-    const int64_t j0 = chunk * kGemmSlots;
+    const int64_t stride = COLTREE ? s / 16 : 0;
+    const int64_t j0 = COLTREE ? chunk * 4 : chunk * kGemmSlots;
     const double* a0 = A + (gb.a + pb * kGemmBlk * bs.a_ia + first * p.g.astep) * s + j0;
     const double* b0 = B + (gb.b + qb * BC * bs.b_ib + first * p.g.bstep) * s + j0;
+    // global offset (from j0) of the 16-byte segment `seg` of a 64-slot unit
+    auto seg_off = [&](int seg) -> int64_t {
+      if (COLTREE) return static_cast<int64_t>(seg >> 1) * stride + (seg & 1) * 2;  // row, half
+      return seg * 2;
+    };
+    // shared-memory position of segment `seg` (slot index = half*32 + row*2 + c)
+    auto seg_pos = [&](int seg) -> int {
+      if (COLTREE) return (seg & 1) * 32 + (seg >> 1) * 2;
+      return seg * 2;
+    };
     const int64_t a_row = bs.a_ia * s, b_col = bs.b_ib * s;
     const int64_t sa = p.g.astep * s, sb = p.g.bstep * s;
 
@@ -1321,12 +1338,12 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
           for (int e = tid; e < kGemmBlk * 32; e += kThreads) {
             const int row = e >> 5, seg = e & 31;
             const int ra = row < np ? row : np - 1;
-            cp_async16(sA + row * kGemmSlots + seg * 2, a0 + c * sa + ra * a_row + seg * 2);
+            cp_async16(sA + row * kGemmSlots + seg_pos(seg), a0 + c * sa + ra * a_row + seg_off(seg));
           }
           for (int e = tid; e < BC * 32; e += kThreads) {
             const int row = e >> 5, seg = e & 31;
             const int rb = row < nq ? row : nq - 1;
-            cp_async16(sB + row * kGemmSlots + seg * 2, b0 + c * sb + rb * b_col + seg * 2);
+            cp_async16(sB + row * kGemmSlots + seg_pos(seg), b0 + c * sb + rb * b_col + seg_off(seg));
           }
         }
       }
@@ -1375,7 +1392,18 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
     }
     cp_async_wait<0>();
     __syncthreads();  // the ring is reused by the next unit
-    const int64_t j = j0 + slot;
+    if (COLTREE) {
+      for (int lv = 0; lv < p.nlevels; ++lv) {  // e = 1, 2, 4, 8 rows
+        const int src = (lane + (2 << lv)) & 31;
+#pragma unroll
+        for (int i = 0; i < kGemmSubR; ++i)
+#pragma unroll
+          for (int k = 0; k < kGemmSubC; ++k)
+            acc[i][k] = dadd(acc[i][k], __shfl_sync(0xffffffffu, acc[i][k], src));
+      }
+    }
+    const int64_t j = COLTREE ? j0 + static_cast<int64_t>(lane >> 1) * stride + (warp & 1) * 2 + (lane & 1)
+                              : j0 + slot;
     if (j < s) {
 #pragma unroll
       for (int i = 0; i < kGemmSubR; ++i)
@@ -1718,7 +1746,7 @@ void run_blocked(const LaunchCtx& c, const GroupParams& p, const BlockSpec& bs, 
 // Phase-1 fold into OUT using the blocked kernel (requires has_b and a plan).
 template <bool HAS_B>
 void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPlan& bp,
-                         const double* ta, const double* tb, double* tout) {
+                         const double* ta, const double* tb, double* tout, bool coltree = false) {
   const GroupSpec& g = p.g;
   GroupParams pr = p;  // the remaining ("rest") group dims
   pr.g.nd = 0;
@@ -1737,7 +1765,8 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
                     aligned16(tb) && forced_path() != 2;
   int P = gemm ? kGemmBlk : (bp.ia >= 0 ? 8 : 1);
   int Q = gemm ? kGemmBlk : (bp.ib >= 0 ? 8 : 1);
-  if (gemm) {  // 16 x 8 blocks when 16 x 16 would give fewer than ~3 waves of units
+  if (coltree && !(gemm && Q == 16)) invalid_argument("column-tree fusion needs the 16x16 GEMM fold");
+  if (gemm && !coltree) {  // 16 x 8 blocks when 16 x 16 would give fewer than ~3 waves of units
     const int64_t units16 = pr.g.groups * (p.s / kGemmSlots) * ((g.ext[bp.ia] + 15) / 16) *
                             ((g.ext[bp.ib] + 15) / 16);
     (void)units16;  // 16 x 8 measured slower on config 3 (more L2 traffic); keep 16 x 16
@@ -1755,7 +1784,7 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
   }
   bs.nbp = (bs.ext_ia + P - 1) / P;
   bs.nbq = (bs.ext_ib + Q - 1) / Q;
-  bs.chunks = gemm ? p.s / kGemmSlots : (p.s + kBlockThreads - 1) / kBlockThreads;
+  bs.chunks = coltree ? (p.s / 16) / 4 : gemm ? p.s / kGemmSlots : (p.s + kBlockThreads - 1) / kBlockThreads;
   bs.units = pr.g.groups * bs.chunks * bs.nbp * bs.nbq;
   bs.div_nbq = make_div64(static_cast<uint64_t>(bs.nbq));
   bs.div_nbp = make_div64(static_cast<uint64_t>(bs.nbp));
@@ -1763,17 +1792,21 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
   if (gemm) {
     const size_t smem =
         static_cast<size_t>(kGemmStages) * kGemmPair * (kGemmBlk + Q) * kGemmSlots * sizeof(double);
-    const void* k = Q == 16 ? (const void*)fold_gemm_kernel<16> : (const void*)fold_gemm_kernel<8>;
+    const void* k = coltree ? (const void*)fold_gemm_kernel<16, true>
+                            : (Q == 16 ? (const void*)fold_gemm_kernel<16, false>
+                                       : (const void*)fold_gemm_kernel<8, false>);
     check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)),
                "smem attribute");
     const int threads = Q == 16 ? 512 : 256;
     const int grid = grid_for(c, k, threads, smem, bs.units);
-    if (Q == 16)
-      fold_gemm_kernel<16><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+    if (coltree)
+      fold_gemm_kernel<16, true><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+    else if (Q == 16)
+      fold_gemm_kernel<16, false><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
     else
-      fold_gemm_kernel<8><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
-    post_launch(c, "gemm fold kernel");
+      fold_gemm_kernel<8, false><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+    post_launch(c, coltree ? "gemm fold + column tree kernel" : "gemm fold kernel");
   } else if (P == 8 && Q == 8)
     run_blocked<HAS_B, 8, 8>(c, pr, bs, ta, tb, tout);
   else if (P == 8)
@@ -1988,10 +2021,20 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
       // phase 2 plan first: the row-shift pass needs the folded tiles in a
       // separate buffer, so phase 1 then folds into session scratch
       TreePass tpass;
-      if (force == 0) tpass = plan_tree_pass(p, s);
+      if (force == 0 || force == 4) tpass = plan_tree_pass(p, s);
       double* fold_dst = tout;
       if (tpass.kind == 2)
         fold_dst = c.scratch(c.scratch_owner, static_cast<size_t>(g.groups) * tile_bytes);
+      // fused column tree: correct, but its 32-byte column segments make the
+      // operand stream request-bound (c3 stage 1: 107 us vs 57 + 10 us unfused),
+      // so it is only taken when forced (TT_KERNEL_PATH=window is reused as the knob)
+      const bool fuse_col = force == 4 && HAS_B && matmul_like && tpass.kind == 1 && tpass.t == 16 &&
+                            tpass.stride0 % 4 == 0 && s % kGemmSlots == 0 && aligned16(ta) &&
+                            aligned16(tb);
+      if (fuse_col) {
+        launch_fold_blocked<HAS_B>(c, p, bplan, ta, tb, tout, true);
+        return;
+      }
       if (tpass.kind != 0) {
         launch_fold_best<HAS_B>(c, p, ta, tb, fold_dst);
         run_tree_pass(c, tpass, p, g.groups, s, fold_dst, tout);

@@ -350,3 +350,33 @@ def test_pack_unpack_plain_shapes_tma_and_gather(gpu, oracle, path):
             assert_bitwise(tt.unpack(t), a, f"{path} unpack {text}")
     finally:
         tt.set_kernel_path("auto")
+
+
+@pytest.mark.parametrize("path", ["auto", "window", "generic"])
+def test_tile_matmul_gemm_paths(gpu, oracle, path):
+    """Products with two broadcast dims (matmul_a / matmul_b) at sizes that
+    take the GEMM-style blocked fold, the fused column tree (sum over dim 1
+    with t = 16) and the row-shift tree pass; partial 16x16 blocks included."""
+    nrng = np.random.default_rng(777)
+    cases = [  # (A shape, B shape, summed dim, slots)
+        ("[40/16,24/8,*/8]", "[40/16,*/8,20/8]", 1, 1024),     # matmul_b, t1 = 16: fused column tree
+        ("[36/8,50/16,*/8]", "[*/8,50/16,40/8]", 2, 1024),     # matmul_a, t2 = 16: row-shift pass
+        ("[100/16,70/8,*/16]", "[100/16,*/8,33/16]", 1, 2048),
+        ("[24/4,96/32,*/16]", "[*/4,96/32,24/16]", 2, 2048),
+    ]
+    tt.set_kernel_path(path)
+    try:
+        for xa, xb, dim, s in cases:
+            S = session(s)
+            sa, sb = parse_shape(xa), parse_shape(xb)
+            ta = nrng.uniform(-1, 1, size=(sa.tile_count(), s))
+            tb = nrng.uniform(-1, 1, size=(sb.tile_count(), s))
+            ws, wt, wc = oracle.mul_sum(sa, ta, sb, tb, s, dim)
+            S.reset_counters()
+            f = tt.matmul_b if dim == 1 else tt.matmul_a
+            got = f(TileTensor(sa, ta, S), TileTensor(sb, tb, S))
+            assert got.shape() == ws
+            assert_bitwise(got.tiles(), wt, f"{path} {xa} x {xb}")
+            assert same_cost(S.cost_report(), wc)
+    finally:
+        tt.set_kernel_path("auto")
