@@ -1261,7 +1261,7 @@ constexpr int kGemmBlk = 16;   // block rows (groups along ia)
 constexpr int kGemmSubR = 8;
 constexpr int kGemmSubC = 4;
 constexpr int kGemmStages = 3;  // super-stages in flight
-constexpr int kGemmPair = 2;    // fold steps per super-stage (one barrier per pair)
+constexpr int kGemmPair = 4;    // fold steps per super-stage (one barrier per super-stage)
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
@@ -1281,14 +1281,19 @@ __device__ __forceinline__ void cp_async_wait() {
 // i.e. complete cyclic columns, and the power-of-two tree runs as 4 shuffle
 // levels (partner lane (l + 2e) mod 32 == row (r + e) mod 16) before the
 // final store -- no separate tree pass, no round trip of the folded tile.
-template <int BC, bool COLTREE>
-__global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32, BC == 8 ? 2 : 1)
+// SLOTS = slots per work unit: 64 (512 threads, 1 CTA/SM) or 32 (256 threads,
+// 2 CTAs/SM, so one CTA computes while the other waits at its barrier).
+template <int BC, bool COLTREE, int SLOTS = kGemmSlots>
+__global__ void __launch_bounds__((SLOTS / 32) * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32,
+                                  (SLOTS == 32 && BC == 8) ? 4 : (SLOTS == 32 || BC == 8) ? 2 : 1)
     fold_gemm_kernel(const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
                      const double* __restrict__ A, const double* __restrict__ B,
                      double* __restrict__ OUT) {
-  constexpr int kThreads = 2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32;
+  constexpr int kHalves = SLOTS / 32;
+  constexpr int kThreads = kHalves * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32;
   constexpr int kSubCols = BC / kGemmSubC;
-  constexpr int kStep = kGemmBlk * kGemmSlots + BC * kGemmSlots;  // doubles per fold step
+  constexpr int kSegs = SLOTS / 2;  // 16-byte segments per operand row
+  constexpr int kStep = kGemmBlk * SLOTS + BC * SLOTS;  // doubles per fold step
   extern __shared__ __align__(16) double gsm[];
   // ring of kGemmStages super-stages, each holding kGemmPair fold steps
   const int64_t s = p.s;
@@ -1296,10 +1301,9 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
   const int64_t count = p.ops[0].y;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int slot = (warp & 1) * 32 + lane;     // slot within the 64-slot chunk
-  const int sub = warp >> 1;                   // 8x4 sub-block of the 16 x BC groups
+  const int slot = (warp % kHalves) * 32 + lane;  // slot within the unit
+  const int sub = warp / kHalves;                 // 8x4 sub-block of the 16 x BC groups
   const int r0 = (sub / kSubCols) * kGemmSubR, c0 = (sub % kSubCols) * kGemmSubC;
-  const int64_t nsuper = (count + kGemmPair - 1) / kGemmPair;
   for (uint64_t u = blockIdx.x; u < static_cast<uint64_t>(bs.units); u += gridDim.x) {
     uint64_t t = u;
     const uint64_t t1 = fdiv(t, bs.div_nbq);
@@ -1312,83 +1316,133 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
     const int np = static_cast<int>(bs.ext_ia - pb * kGemmBlk < kGemmBlk ? bs.ext_ia - pb * kGemmBlk : kGemmBlk);
     const int nq = static_cast<int>(bs.ext_ib - qb * BC < BC ? bs.ext_ib - qb * BC : BC);
     const int64_t stride = COLTREE ? s / 16 : 0;
-    const int64_t j0 = COLTREE ? chunk * 4 : chunk * kGemmSlots;
+    constexpr int kCols = SLOTS / 16;  // COLTREE: columns per unit (16 rows each)
+    const int64_t j0 = COLTREE ? chunk * kCols : chunk * SLOTS;
     const double* a0 = A + (gb.a + pb * kGemmBlk * bs.a_ia + first * p.g.astep) * s + j0;
     const double* b0 = B + (gb.b + qb * BC * bs.b_ib + first * p.g.bstep) * s + j0;
     // global offset (from j0) of the 16-byte segment `seg` of a 64-slot unit
     auto seg_off = [&](int seg) -> int64_t {
-      if (COLTREE) return static_cast<int64_t>(seg >> 1) * stride + (seg & 1) * 2;  // row, half
+      if (COLTREE) return static_cast<int64_t>(seg / kHalves) * stride + (seg % kHalves) * 2;  // row, half
       return seg * 2;
     };
     // shared-memory position of segment `seg` (slot index = half*32 + row*2 + c)
     auto seg_pos = [&](int seg) -> int {
-      if (COLTREE) return (seg & 1) * 32 + (seg >> 1) * 2;
+      if (COLTREE) return (seg % kHalves) * 32 + (seg / kHalves) * 2;
       return seg * 2;
     };
     const int64_t a_row = bs.a_ia * s, b_col = bs.b_ib * s;
     const int64_t sa = p.g.astep * s, sb = p.g.bstep * s;
 
-    auto stage = [&](int buf, int64_t sup) {
+    // per-thread staging plan, invariant across fold steps: which 16-byte
+    // segments this thread copies (source pointer at step 0, smem offset)
+    constexpr int kCopiesA = (kGemmBlk * kSegs + kThreads - 1) / kThreads;
+    constexpr int kCopiesB = (BC * kSegs + kThreads - 1) / kThreads;
+    const double* srcA[kCopiesA];
+    const double* srcB[kCopiesB];
+    int dstA[kCopiesA], dstB[kCopiesB];
+#pragma unroll
+    for (int q = 0; q < kCopiesA; ++q) {
+      const int e = tid + q * kThreads;
+      const int row = e / kSegs, seg = e % kSegs;
+      const int ra = row < np ? row : np - 1;
+      srcA[q] = e < kGemmBlk * kSegs ? a0 + ra * a_row + seg_off(seg) : a0;  // unused when e is out
+      dstA[q] = row * SLOTS + seg_pos(seg);
+    }
+#pragma unroll
+    for (int q = 0; q < kCopiesB; ++q) {
+      const int e = tid + q * kThreads;
+      const int row = e / kSegs, seg = e % kSegs;
+      const int rb = row < nq ? row : nq - 1;
+      srcB[q] = e < BC * kSegs ? b0 + rb * b_col + seg_off(seg) : b0;
+      dstB[q] = kGemmBlk * SLOTS + row * SLOTS + seg_pos(seg);
+    }
+
+    // fold steps are int32 (the host checks count < 2^31); ring offsets in
+    // doubles advance by one super-stage and wrap without a division
+    const int cnt = static_cast<int>(count);
+    const int nsup = (cnt + kGemmPair - 1) / kGemmPair;
+    constexpr int kSuper = kGemmPair * kStep;
+    constexpr int kRing = kGemmStages * kSuper;
+    // staging pointers advance by one super-stage per call (no 64-bit
+    // multiplies in the loop); step h of a super-stage is h * sa further on
+    auto stage = [&](int off, int c_first) {
 #pragma unroll
       for (int h = 0; h < kGemmPair; ++h) {
-        const int64_t c = sup * kGemmPair + h;
-        if (c < count) {
-          double* sA = gsm + (static_cast<int64_t>(buf) * kGemmPair + h) * kStep;
-          double* sB = sA + kGemmBlk * kGemmSlots;
-          for (int e = tid; e < kGemmBlk * 32; e += kThreads) {
-            const int row = e >> 5, seg = e & 31;
-            const int ra = row < np ? row : np - 1;
-            cp_async16(sA + row * kGemmSlots + seg_pos(seg), a0 + c * sa + ra * a_row + seg_off(seg));
-          }
-          for (int e = tid; e < BC * 32; e += kThreads) {
-            const int row = e >> 5, seg = e & 31;
-            const int rb = row < nq ? row : nq - 1;
-            cp_async16(sB + row * kGemmSlots + seg_pos(seg), b0 + c * sb + rb * b_col + seg_off(seg));
-          }
+        if (c_first + h < cnt) {
+          double* st = gsm + off + h * kStep;
+#pragma unroll
+          for (int q = 0; q < kCopiesA; ++q)
+            if (kGemmBlk * kSegs % kThreads == 0 || tid + q * kThreads < kGemmBlk * kSegs)
+              cp_async16(st + dstA[q], srcA[q] + h * sa);
+#pragma unroll
+          for (int q = 0; q < kCopiesB; ++q)
+            if (BC * kSegs % kThreads == 0 || tid + q * kThreads < BC * kSegs)
+              cp_async16(st + dstB[q], srcB[q] + h * sb);
         }
       }
       cp_async_commit();
+#pragma unroll
+      for (int q = 0; q < kCopiesA; ++q) srcA[q] += kGemmPair * sa;
+#pragma unroll
+      for (int q = 0; q < kCopiesB; ++q) srcB[q] += kGemmPair * sb;
     };
 
+    // -0.0 is the exact additive identity (-0 + x == x for every x, signed
+    // zeros included), so starting the fold from it reproduces the
+    // reference's "first product, then add" association bit for bit
     double acc[kGemmSubR][kGemmSubC];
 #pragma unroll
+    for (int i = 0; i < kGemmSubR; ++i)
+#pragma unroll
+      for (int k = 0; k < kGemmSubC; ++k) acc[i][k] = -0.0;
+    auto fold_step = [&](const double* sA) {
+      const double* sB = sA + kGemmBlk * SLOTS;
+      double a[kGemmSubR], b[kGemmSubC];
+#pragma unroll
+      for (int i = 0; i < kGemmSubR; ++i) a[i] = sA[(r0 + i) * SLOTS + slot];
+#pragma unroll
+      for (int k = 0; k < kGemmSubC; ++k) b[k] = sB[(c0 + k) * SLOTS + slot];
+      // products of two rows first, then their additions: 8 independent
+      // DMULs in flight before the dependent DADDs (fixed-latency hiding)
+#pragma unroll
+      for (int i = 0; i < kGemmSubR; i += 2) {
+        double pr[2][kGemmSubC];
+#pragma unroll
+        for (int k = 0; k < kGemmSubC; ++k) {
+          pr[0][k] = dmul(a[i], b[k]);
+          pr[1][k] = dmul(a[i + 1], b[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < kGemmSubC; ++k) {
+          acc[i][k] = dadd(acc[i][k], pr[0][k]);
+          acc[i + 1][k] = dadd(acc[i + 1][k], pr[1][k]);
+        }
+      }
+    };
+#pragma unroll
     for (int k = 0; k < kGemmStages - 1; ++k) {
-      if (k < nsuper)
-        stage(k, k);
+      if (k < nsup)
+        stage(k * kSuper, k * kGemmPair);
       else
         cp_async_commit();
     }
-    for (int64_t sup = 0; sup < nsuper; ++sup) {
-      const int buf = static_cast<int>(sup % kGemmStages);
+    int rd = 0, wr = (kGemmStages - 1) * kSuper;
+    for (int sup = 0; sup < nsup; ++sup) {
       cp_async_wait<kGemmStages - 2>();  // super-stage `sup` has landed
       __syncthreads();                   // ...for every thread; the previous buffer is free
-      if (sup + kGemmStages - 1 < nsuper)
-        stage(static_cast<int>((sup + kGemmStages - 1) % kGemmStages), sup + kGemmStages - 1);
+      if (sup + kGemmStages - 1 < nsup)
+        stage(wr, (sup + kGemmStages - 1) * kGemmPair);
       else
         cp_async_commit();
+      wr = wr + kSuper == kRing ? 0 : wr + kSuper;
+      const double* sbuf = gsm + rd;
+      if ((sup + 1) * kGemmPair <= cnt) {
 #pragma unroll
-      for (int h = 0; h < kGemmPair; ++h) {
-        const int64_t c = sup * kGemmPair + h;
-        if (c >= count) break;
-        const double* sA = gsm + (static_cast<int64_t>(buf) * kGemmPair + h) * kStep;
-        const double* sB = sA + kGemmBlk * kGemmSlots;
-        double a[kGemmSubR], b[kGemmSubC];
-#pragma unroll
-        for (int i = 0; i < kGemmSubR; ++i) a[i] = sA[(r0 + i) * kGemmSlots + slot];
-#pragma unroll
-        for (int k = 0; k < kGemmSubC; ++k) b[k] = sB[(c0 + k) * kGemmSlots + slot];
-        if (c == 0) {
-#pragma unroll
-          for (int i = 0; i < kGemmSubR; ++i)
-#pragma unroll
-            for (int k = 0; k < kGemmSubC; ++k) acc[i][k] = dmul(a[i], b[k]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < kGemmSubR; ++i)
-#pragma unroll
-            for (int k = 0; k < kGemmSubC; ++k) acc[i][k] = dadd(acc[i][k], dmul(a[i], b[k]));
-        }
+        for (int h = 0; h < kGemmPair; ++h) fold_step(sbuf + h * kStep);
+      } else {
+        for (int h = 0; h < cnt - sup * kGemmPair; ++h) fold_step(sbuf + h * kStep);
       }
+      rd = rd + kSuper == kRing ? 0 : rd + kSuper;
     }
     cp_async_wait<0>();
     __syncthreads();  // the ring is reused by the next unit
@@ -1402,16 +1456,24 @@ __global__ void __launch_bounds__(2 * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) 
             acc[i][k] = dadd(acc[i][k], __shfl_sync(0xffffffffu, acc[i][k], src));
       }
     }
-    const int64_t j = COLTREE ? j0 + static_cast<int64_t>(lane >> 1) * stride + (warp & 1) * 2 + (lane & 1)
+    const int64_t j = COLTREE ? j0 + static_cast<int64_t>(lane >> 1) * stride + (warp % kHalves) * 2 + (lane & 1)
                               : j0 + slot;
     if (j < s) {
+      // row pointers by increment, column offsets once: one 64-bit add per store
+      double* orow = OUT + (gb.out + (pb * kGemmBlk + r0) * bs.out_ia + (qb * BC + c0) * bs.out_ib) * s + j;
+      const int64_t rstep = bs.out_ia * s, cstep = bs.out_ib * s;
+      int64_t coff[kGemmSubC];
 #pragma unroll
-      for (int i = 0; i < kGemmSubR; ++i)
+      for (int k = 0; k < kGemmSubC; ++k) coff[k] = k * cstep;
 #pragma unroll
-        for (int k = 0; k < kGemmSubC; ++k)
-          if (r0 + i < np && c0 + k < nq)
-            OUT[(gb.out + (pb * kGemmBlk + r0 + i) * bs.out_ia + (qb * BC + c0 + k) * bs.out_ib) *
-                    s + j] = acc[i][k];
+      for (int i = 0; i < kGemmSubR; ++i) {
+        if (r0 + i < np) {
+#pragma unroll
+          for (int k = 0; k < kGemmSubC; ++k)
+            if (c0 + k < nq) orow[coff[k]] = acc[i][k];
+        }
+        orow += rstep;
+      }
     }
   }
 }
@@ -1717,6 +1779,19 @@ void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, con
   post_launch(c, "fold kernel");
 }
 
+// GEMM unit width (TT_GEMM_SLOTS=64 forces the 64-slot, 1-CTA-per-SM variant).
+const int g_gemm_slots = [] {
+  const char* e = std::getenv("TT_GEMM_SLOTS");
+  return e ? std::atoi(e) : 32;
+}();
+// GEMM block columns for 32-slot units: 8 (16 x 8 groups, 128 threads, twice the
+// units of 16 x 16 -- better wave balance on 148 SMs; measured ~5% faster on
+// config 3) or TT_GEMM_BC=16 (16 x 16 groups, 256 threads)
+const int g_gemm_bc = [] {
+  const char* e = std::getenv("TT_GEMM_BC");
+  return e ? std::atoi(e) : 8;
+}();
+
 // Blocked-fold plan: ia = a group dim along which B broadcasts (A varies), ib =
 // one along which A broadcasts (B varies).  Eligible when at least one exists.
 struct BlockPlan {
@@ -1762,9 +1837,9 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
     pr.g.groups *= g.ext[i];
   }
   const bool gemm = bp.ia >= 0 && bp.ib >= 0 && p.s % kGemmSlots == 0 && aligned16(ta) &&
-                    aligned16(tb) && forced_path() != 2;
+                    aligned16(tb) && forced_path() != 2 && p.ops[0].y < (int64_t{1} << 31);
   int P = gemm ? kGemmBlk : (bp.ia >= 0 ? 8 : 1);
-  int Q = gemm ? kGemmBlk : (bp.ib >= 0 ? 8 : 1);
+  int Q = gemm ? (g_gemm_bc == 8 && !coltree && g_gemm_slots != 64 ? 8 : kGemmBlk) : (bp.ib >= 0 ? 8 : 1);
   if (coltree && !(gemm && Q == 16)) invalid_argument("column-tree fusion needs the 16x16 GEMM fold");
   if (gemm && !coltree) {  // 16 x 8 blocks when 16 x 16 would give fewer than ~3 waves of units
     const int64_t units16 = pr.g.groups * (p.s / kGemmSlots) * ((g.ext[bp.ia] + 15) / 16) *
@@ -1784,12 +1859,27 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
   }
   bs.nbp = (bs.ext_ia + P - 1) / P;
   bs.nbq = (bs.ext_ib + Q - 1) / Q;
-  bs.chunks = coltree ? (p.s / 16) / 4 : gemm ? p.s / kGemmSlots : (p.s + kBlockThreads - 1) / kBlockThreads;
+  // 32-slot units (2 CTAs per SM) for the plain GEMM fold
+  const bool slots32 = gemm && p.s % 32 == 0 && g_gemm_slots != 64;
+  bs.chunks = coltree ? (p.s / 16) / (slots32 ? 2 : 4)
+              : gemm ? p.s / (slots32 ? 32 : kGemmSlots)
+                     : (p.s + kBlockThreads - 1) / kBlockThreads;
   bs.units = pr.g.groups * bs.chunks * bs.nbp * bs.nbq;
   bs.div_nbq = make_div64(static_cast<uint64_t>(bs.nbq));
   bs.div_nbp = make_div64(static_cast<uint64_t>(bs.nbp));
   bs.div_chunks = make_div64(static_cast<uint64_t>(bs.chunks));
-  if (gemm) {
+  if (slots32) {
+    const size_t smem = static_cast<size_t>(kGemmStages) * kGemmPair * (kGemmBlk + Q) * 32 * sizeof(double);
+    auto k = coltree ? fold_gemm_kernel<16, true, 32>
+                     : (Q == 8 ? fold_gemm_kernel<8, false, 32> : fold_gemm_kernel<16, false, 32>);
+    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)),
+               "smem attribute");
+    const int threads = Q == 8 ? 128 : 256;
+    const int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
+    k<<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+    post_launch(c, coltree ? "gemm fold + column tree kernel (32-slot units)" : "gemm fold kernel (32-slot units)");
+  } else if (gemm) {
     const size_t smem =
         static_cast<size_t>(kGemmStages) * kGemmPair * (kGemmBlk + Q) * kGemmSlots * sizeof(double);
     const void* k = coltree ? (const void*)fold_gemm_kernel<16, true>

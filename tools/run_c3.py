@@ -10,6 +10,8 @@ import paper_2011_01805_b200 as tt  # noqa: E402
 from paper_2011_01805_b200 import configs  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+if len(sys.argv) > 2:
+    tt.set_kernel_path(sys.argv[2])
 c3 = configs.config3()
 S = tt.Session(8192, 8)
 T = {k: tt.pack(c3.tensors[k], tt.parse_shape(v), S) for k, v in c3.shapes.items()
