@@ -9,8 +9,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 
@@ -30,6 +33,11 @@ struct tt_session {
   size_t scratch_bytes = 0;
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;
+  // compiled rotate-and-sum schedules, keyed by (ext, t, stride, used,
+  // unknown, variant): a schedule depends only on these (slots are fixed per
+  // session), and rebuilding it per call costs more host time than a small
+  // op's kernels take on the GPU
+  std::map<std::array<int64_t, 6>, std::shared_ptr<const ttb::Program>> programs;
 };
 
 namespace {
@@ -160,8 +168,16 @@ void run_reduction(tt_session* s, const Shape& prod, int di, int variant, const 
     shape_error("sum over an unknown interleaved dimension requires clean_unknowns first");
   const auto ext = prod.external();
   const int64_t stride = tile_strides(prod)[di];
-  const Program prog =
-      build_sum_program(ext[di], ds.t, stride, s->slots, ds.used(), ds.unknown, variant);
+  const std::array<int64_t, 6> key{ext[di], ds.t, stride, ds.used(), ds.unknown ? 1 : 0, variant};
+  auto it = s->programs.find(key);
+  if (it == s->programs.end()) {
+    if (s->programs.size() >= 256) s->programs.clear();
+    it = s->programs
+             .emplace(key, std::make_shared<const Program>(build_sum_program(
+                               ext[di], ds.t, stride, s->slots, ds.used(), ds.unknown, variant)))
+             .first;
+  }
+  const Program& prog = *it->second;
   const GroupSpec g = make_group_spec(ext, di, a_st, b_st, tb != nullptr);
   add_cost(s, prog.per_group, static_cast<uint64_t>(g.groups));
   launch_group_program(ctx_of(s), prog, g, s->slots, ta, tb, out);

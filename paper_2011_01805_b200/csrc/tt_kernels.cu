@@ -13,13 +13,17 @@
 //    fold (tile_tensor.hpp:323-324) runs per slot in registers, and the
 //    in-tile rotate-and-sum schedule runs from shared memory without any HBM
 //    round trip per rotation (north-star item 3).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "tt_launch.hpp"
 
@@ -85,10 +89,48 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv32& f) {
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 
+// Host-side launch overhead matters for short ops (a c3 matmul stage is ~40
+// us of GPU work): occupancy answers and the dynamic-smem opt-in are cached
+// per (device, kernel, block shape) instead of queried on every launch.
+struct OccKey {
+  int device;
+  const void* kernel;
+  int threads;
+  size_t smem;
+  bool operator<(const OccKey& o) const {
+    return std::tie(device, kernel, threads, smem) < std::tie(o.device, o.kernel, o.threads, o.smem);
+  }
+};
+std::mutex g_launch_cache_mu;
+std::map<OccKey, int> g_occupancy;
+std::map<std::pair<int, const void*>, size_t> g_smem_attr;
+
+void set_smem_attr(const void* kernel, size_t smem) {
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_launch_cache_mu);
+  size_t& cur = g_smem_attr[{dev, kernel}];
+  if (smem <= cur) return;
+  check_cuda(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)),
+             "smem attribute");
+  cur = smem;
+}
+
 int grid_for(const LaunchCtx& c, const void* kernel, int threads, size_t smem, int64_t work) {
   int per_sm = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem),
-             "occupancy query");
+  {
+    std::lock_guard<std::mutex> lk(g_launch_cache_mu);
+    const OccKey key{c.device, kernel, threads, smem};
+    auto it = g_occupancy.find(key);
+    if (it != g_occupancy.end()) {
+      per_sm = it->second;
+    } else {
+      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem),
+                 "occupancy query");
+      g_occupancy[key] = per_sm;
+    }
+  }
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = static_cast<int64_t>(c.sm_count) * per_sm;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cap, work)));
@@ -711,6 +753,9 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy) : "memory");
 }
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
@@ -1478,6 +1523,218 @@ __global__ void __launch_bounds__((SLOTS / 32) * (kGemmBlk / kGemmSubR) * (BC / 
   }
 }
 
+// TMA-fed GEMM fold (the default for matmul-shaped products).  Same work
+// unit as fold_gemm_kernel -- a 16 x BC block of groups for 32 consecutive
+// slots -- but the operands arrive by tensor-map TMA: per stage, ONE 5-D box
+// load brings the block's A chunks ([kTgSteps fold steps][16 rows][32 slots])
+// and one the B chunks, both completing on the stage's mbarrier.  Lane 0 of
+// warp 0 issues them kTgStages-1 stages ahead, running on into the CTA's next
+// unit while the warps store the previous one, so no thread spends an
+// instruction on staging addresses.  There is no separate producer warp: with
+// ~200 registers per thread, 4-warp CTAs let two CTAs (2 warps per SM
+// sub-partition) share an SM, where a 5-warp CTA would fit only once.  Each
+// warp owns an 8 x 8 sub-block of the groups (16 shared-memory loads per 128
+// FP64 operations).  Tensor dims (innermost first): slot, block row, fold
+// step, up to two remaining group dims.  Out-of-range rows and steps are
+// zero-filled by the TMA unit: rows are never stored, steps never folded.
+// kTgSteps = fold steps per stage, kTgStages = ring stages (kTgStages - 1
+// loads in flight ahead), SC = columns of a thread's 8 x SC sub-block of groups
+
+struct TgSpec {
+  int nrest;
+  int chunk_major;  // unit order: chunk fastest (consecutive CTAs read adjacent slots)
+  int a_act[2], b_act[2];  // remaining group dim i is a tensor-map dim of A / B
+};
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+// SL = slots per unit: 32 (one slot per lane) or 16 (the two half-warps take
+// different 8-column halves of the block: twice the units, for wave balance)
+template <int BC, int SL, int SC>
+__host__ __device__ constexpr int tg_warps() {
+  return (kGemmBlk / 8) * (BC / SC) * SL / 32;
+}
+template <int BC, int SL, int kTgSteps, int kTgStages>
+__host__ __device__ constexpr size_t tg_smem_bytes() {
+  return static_cast<size_t>(kTgStages) * kTgSteps * (kGemmBlk + BC) * SL * sizeof(double) +
+         2 * kTgStages * sizeof(uint64_t);
+}
+
+struct TgUnit {
+  int64_t qb, pb, chunk;
+  uint64_t rest;
+};
+__device__ __forceinline__ TgUnit tg_decode(const BlockSpec& bs, uint64_t u, int chunk_major) {
+  TgUnit t;
+  if (chunk_major) {
+    const uint64_t t1 = fdiv(u, bs.div_chunks);
+    t.chunk = static_cast<int64_t>(u - t1 * bs.div_chunks.d);
+    const uint64_t t2 = fdiv(t1, bs.div_nbq);
+    t.qb = static_cast<int64_t>(t1 - t2 * bs.div_nbq.d);
+    t.rest = fdiv(t2, bs.div_nbp);
+    t.pb = static_cast<int64_t>(t2 - t.rest * bs.div_nbp.d);
+    return t;
+  }
+  const uint64_t t1 = fdiv(u, bs.div_nbq);
+  t.qb = static_cast<int64_t>(u - t1 * bs.div_nbq.d);
+  const uint64_t t2 = fdiv(t1, bs.div_nbp);
+  t.pb = static_cast<int64_t>(t1 - t2 * bs.div_nbp.d);
+  t.rest = fdiv(t2, bs.div_chunks);
+  t.chunk = static_cast<int64_t>(t2 - t.rest * bs.div_chunks.d);
+  return t;
+}
+
+template <int BC, int SL, int kTgSteps, int kTgStages, int SC>
+__global__ void __maxnreg__(SC == 8 ? 232 : 128)
+    fold_gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
+                         const __grid_constant__ CUtensorMap mapB,
+                         const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
+                         const __grid_constant__ TgSpec ts, double* __restrict__ OUT) {
+  constexpr int kW = tg_warps<BC, SL, SC>();
+  constexpr int kTgRows = 8 / SC;  // rows of products batched before their adds
+  constexpr int kA = kTgSteps * kGemmBlk * SL;  // doubles per stage
+  constexpr int kB = kTgSteps * BC * SL;
+  constexpr int kStage = kA + kB;
+  extern __shared__ __align__(1024) double tsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + kTgStages * kStage);
+  uint64_t* empty = full + kTgStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool issuer = threadIdx.x == 0;
+  if (issuer) {
+    for (int i = 0; i < kTgStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t s = p.s;
+  const int cnt = static_cast<int>(p.ops[0].y);
+  const int nst = (cnt + kTgSteps - 1) / kTgSteps;  // stages per unit
+  const uint64_t units = static_cast<uint64_t>(bs.units);
+
+  // load sequence of this CTA (issuer only): unit lu, stage k of that unit
+  uint64_t lu = blockIdx.x;
+  int lk = 0, lstage = 0;
+  uint32_t lphase = 0;
+  int rc[2] = {0, 0};
+  TgUnit lt{};
+  auto load_unit = [&]() {
+    lt = tg_decode(bs, lu, ts.chunk_major);
+    uint64_t v = lt.rest;
+#pragma unroll
+    for (int i = 1; i >= 0; --i) {
+      if (i < ts.nrest) {
+        const uint64_t q = fdiv(v, p.gdiv[i]);
+        rc[i] = static_cast<int>(v - q * p.gdiv[i].d);
+        v = q;
+      }
+    }
+  };
+  auto issue_next = [&]() {
+    if (lu >= units) return;
+    mbar_wait(&empty[lstage], lphase ^ 1);  // every warp has released this buffer
+    mbar_arrive_expect_tx(&full[lstage], kStage * sizeof(double));
+    double* st = tsm + lstage * kStage;
+    const int j0 = static_cast<int>(lt.chunk * SL);
+    tma_load_5d(st, &mapA, j0, static_cast<int>(lt.pb * kGemmBlk), lk * kTgSteps,
+                ts.a_act[0] ? rc[0] : 0, ts.a_act[1] ? rc[1] : 0, &full[lstage]);
+    tma_load_5d(st + kA, &mapB, j0, static_cast<int>(lt.qb * BC), lk * kTgSteps,
+                ts.b_act[0] ? rc[0] : 0, ts.b_act[1] ? rc[1] : 0, &full[lstage]);
+    if (++lstage == kTgStages) {
+      lstage = 0;
+      lphase ^= 1;
+    }
+    if (++lk == nst) {
+      lk = 0;
+      lu += gridDim.x;
+      if (lu < units) load_unit();
+    }
+  };
+  if (issuer && lu < units) {
+    load_unit();
+    for (int i = 0; i < kTgStages - 1; ++i) issue_next();
+  }
+
+  const int sub = warp * (32 / SL) + lane / SL, slot = lane % SL;
+  const int r0 = (sub / (BC / SC)) * 8, c0 = (sub % (BC / SC)) * SC;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const TgUnit t = tg_decode(bs, u, ts.chunk_major);
+    double acc[8][SC];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int k = 0; k < SC; ++k) acc[i][k] = -0.0;  // exact identity: -0 + x == x
+    auto fold_step = [&](const double* sA, const double* sB) {
+      double a[8], b[SC];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = sA[i * SL];
+#pragma unroll
+      for (int k = 0; k < SC; ++k) b[k] = sB[k * SL];
+      // per kTgRows rows: 8 * kTgRows independent products, then their additions
+#pragma unroll
+      for (int i = 0; i < 8; i += kTgRows) {
+        double pr[kTgRows][SC];
+#pragma unroll
+        for (int r = 0; r < kTgRows; ++r)
+#pragma unroll
+          for (int k = 0; k < SC; ++k) pr[r][k] = dmul(a[i + r], b[k]);
+#pragma unroll
+        for (int r = 0; r < kTgRows; ++r)
+#pragma unroll
+          for (int k = 0; k < SC; ++k) acc[i + r][k] = dadd(acc[i + r][k], pr[r][k]);
+      }
+    };
+    for (int k = 0; k < nst; ++k) {
+      if (issuer) issue_next();  // refills the buffer released one stage ago
+      __syncwarp();
+      mbar_wait(&full[stage], phase);
+      const double* sA = tsm + stage * kStage + r0 * SL + slot;
+      const double* sB = tsm + stage * kStage + kA + c0 * SL + slot;
+      const int nsteps = cnt - k * kTgSteps;
+      if (nsteps >= kTgSteps) {
+#pragma unroll
+        for (int h = 0; h < kTgSteps; ++h) fold_step(sA + h * kGemmBlk * SL, sB + h * BC * SL);
+      } else {
+        for (int h = 0; h < nsteps; ++h) fold_step(sA + h * kGemmBlk * SL, sB + h * BC * SL);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kTgStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    const GroupBase gb = group_base(p, t.rest);
+    const int np = static_cast<int>(bs.ext_ia - t.pb * kGemmBlk < kGemmBlk ? bs.ext_ia - t.pb * kGemmBlk : kGemmBlk);
+    const int nq = static_cast<int>(bs.ext_ib - t.qb * BC < BC ? bs.ext_ib - t.qb * BC : BC);
+    double* orow = OUT + (gb.out + (t.pb * kGemmBlk + r0) * bs.out_ia + (t.qb * BC + c0) * bs.out_ib) * s +
+                   t.chunk * SL + slot;
+    const int64_t rstep = bs.out_ia * s, cstep = bs.out_ib * s;
+    // the fold output is re-read at once by the tree pass: keep it in L2
+    const uint64_t keep = policy_evict_last();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (r0 + i < np) {
+#pragma unroll
+        for (int k = 0; k < SC; ++k)
+          if (c0 + k < nq) st_keep(orow + k * cstep, acc[i][k], keep);
+      }
+      orow += rstep;
+    }
+  }
+}
+
 // ---- tree-only passes (phase 2 of a two-phase reduction), in place on OUT ----------------
 // (A) column-local: the summed dim is the first (s == t * stride), so each
 // column c of the tile viewed as [t][stride] is one cyclic sequence of t
@@ -1792,6 +2049,12 @@ const int g_gemm_bc = [] {
   return e ? std::atoi(e) : 8;
 }();
 
+// TT_GEMM_TMA=0 disables the tensor-map-fed GEMM fold (cp.async variant instead)
+const int g_gemm_tma = [] {
+  const char* e = std::getenv("TT_GEMM_TMA");
+  return e ? std::atoi(e) : 1;
+}();
+
 // Blocked-fold plan: ia = a group dim along which B broadcasts (A varies), ib =
 // one along which A broadcasts (B varies).  Eligible when at least one exists.
 struct BlockPlan {
@@ -1807,6 +2070,90 @@ BlockPlan block_plan(const GroupSpec& g, bool has_b) {
     if (g.a_stride[i] == 0 && g.b_stride[i] != 0 && bp.ib < 0) bp.ib = i;
   }
   return bp;
+}
+
+// Launches fold_gemm_tma_kernel when both operands are expressible as 5-D
+// tensor maps (<= 2 remaining group dims, non-zero fold strides); false
+// otherwise (the caller falls back to the cp.async GEMM fold).
+const int g_gemm_order = [] {
+  const char* e = std::getenv("TT_GEMM_ORDER");
+  return e ? std::atoi(e) : 0;
+}();
+
+template <int SL, int kTgSteps, int kTgStages, int SC>
+bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupParams& pr,
+                        BlockSpec bs, const double* ta, const double* tb, double* tout) {
+  const GroupSpec& g = p.g;
+  const int64_t s = p.s;
+  const int64_t first = p.ops[0].x, count = p.ops[0].y;
+  if (pr.g.nd > 2 || g.astep == 0 || g.bstep == 0 || s % SL != 0 || count >= (int64_t{1} << 31))
+    return false;
+  if (s >= (int64_t{1} << 32) || bs.ext_ia >= (int64_t{1} << 31) || bs.ext_ib >= (int64_t{1} << 31))
+    return false;
+  constexpr int BC = 16;
+  TgSpec ts{};
+  ts.nrest = pr.g.nd;
+  ts.chunk_major = g_gemm_order;
+  alignas(64) unsigned char mapA[128], mapB[128];
+  const uint64_t eb = sizeof(double);
+  uint64_t dA[5] = {static_cast<uint64_t>(s), static_cast<uint64_t>(bs.ext_ia), static_cast<uint64_t>(count), 1, 1};
+  uint64_t dB[5] = {static_cast<uint64_t>(s), static_cast<uint64_t>(bs.ext_ib), static_cast<uint64_t>(count), 1, 1};
+  uint64_t sA[4] = {static_cast<uint64_t>(bs.a_ia * s) * eb, static_cast<uint64_t>(g.astep * s) * eb,
+                    static_cast<uint64_t>(s) * eb, static_cast<uint64_t>(s) * eb};
+  uint64_t sB[4] = {static_cast<uint64_t>(bs.b_ib * s) * eb, static_cast<uint64_t>(g.bstep * s) * eb,
+                    static_cast<uint64_t>(s) * eb, static_cast<uint64_t>(s) * eb};
+  for (int i = 0; i < pr.g.nd; ++i) {
+    if (pr.g.a_stride[i] > 0) {
+      ts.a_act[i] = 1;
+      dA[3 + i] = static_cast<uint64_t>(pr.g.ext[i]);
+      sA[2 + i] = static_cast<uint64_t>(pr.g.a_stride[i] * s) * eb;
+    } else if (pr.g.a_stride[i] < 0) {
+      return false;
+    }
+    if (pr.g.b_stride[i] > 0) {
+      ts.b_act[i] = 1;
+      dB[3 + i] = static_cast<uint64_t>(pr.g.ext[i]);
+      sB[2 + i] = static_cast<uint64_t>(pr.g.b_stride[i] * s) * eb;
+    } else if (pr.g.b_stride[i] < 0) {
+      return false;
+    }
+  }
+  if (bs.a_ia <= 0 || bs.b_ib <= 0 || g.astep < 0 || g.bstep < 0) return false;
+  const uint32_t boxA[5] = {static_cast<uint32_t>(SL), kGemmBlk, kTgSteps, 1, 1};
+  const uint32_t boxB[5] = {static_cast<uint32_t>(SL), BC, kTgSteps, 1, 1};
+  if (!encode_tensor_map_f64(mapA, 5, ta + first * g.astep * s, dA, sA, boxA) ||
+      !encode_tensor_map_f64(mapB, 5, tb + first * g.bstep * s, dB, sB, boxB))
+    return false;
+  bs.nbq = (bs.ext_ib + BC - 1) / BC;
+  bs.chunks = s / SL;
+  bs.units = pr.g.groups * bs.chunks * bs.nbp * bs.nbq;
+  bs.div_nbq = make_div64(static_cast<uint64_t>(bs.nbq));
+  bs.div_chunks = make_div64(static_cast<uint64_t>(bs.chunks));
+  auto k = fold_gemm_tma_kernel<BC, SL, kTgSteps, kTgStages, SC>;
+  constexpr size_t smem = tg_smem_bytes<BC, SL, kTgSteps, kTgStages>();
+  constexpr int threads = tg_warps<BC, SL, SC>() * 32;
+  set_smem_attr((const void*)k, smem);
+  const int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
+  k<<<grid, threads, smem, c.stream>>>(*reinterpret_cast<const CUtensorMap*>(mapA),
+                                       *reinterpret_cast<const CUtensorMap*>(mapB), pr, bs, ts, tout);
+  post_launch(c, "gemm fold kernel (TMA)");
+  return true;
+}
+
+
+const int g_gemm_cfg = [] {
+  const char* e = std::getenv("TT_GEMM_CFG");
+  return e ? std::atoi(e) : 0;
+}();
+
+bool launch_gemm_tma(const LaunchCtx& c, const GroupParams& p, const GroupParams& pr,
+                     const BlockSpec& bs, const double* ta, const double* tb, double* tout) {
+  switch (g_gemm_cfg) {
+    case 1: return launch_gemm_tma_sl<16, 2, 6, 4>(c, p, pr, bs, ta, tb, tout);
+    case 2: return launch_gemm_tma_sl<16, 4, 4, 4>(c, p, pr, bs, ta, tb, tout);
+    case 3: return launch_gemm_tma_sl<32, 2, 6, 4>(c, p, pr, bs, ta, tb, tout);
+    default: return launch_gemm_tma_sl<16, 4, 3, 4>(c, p, pr, bs, ta, tb, tout);
+  }
 }
 
 template <bool HAS_B, int P, int Q>
@@ -1868,13 +2215,13 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
   bs.div_nbq = make_div64(static_cast<uint64_t>(bs.nbq));
   bs.div_nbp = make_div64(static_cast<uint64_t>(bs.nbp));
   bs.div_chunks = make_div64(static_cast<uint64_t>(bs.chunks));
-  if (slots32) {
+  if (slots32 && !coltree && g_gemm_tma && launch_gemm_tma(c, p, pr, bs, ta, tb, tout)) {
+    return;
+  } else if (slots32) {
     const size_t smem = static_cast<size_t>(kGemmStages) * kGemmPair * (kGemmBlk + Q) * 32 * sizeof(double);
     auto k = coltree ? fold_gemm_kernel<16, true, 32>
                      : (Q == 8 ? fold_gemm_kernel<8, false, 32> : fold_gemm_kernel<16, false, 32>);
-    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)),
-               "smem attribute");
+    set_smem_attr((const void*)k, smem);
     const int threads = Q == 8 ? 128 : 256;
     const int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
     k<<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
@@ -1885,9 +2232,7 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
     const void* k = coltree ? (const void*)fold_gemm_kernel<16, true>
                             : (Q == 16 ? (const void*)fold_gemm_kernel<16, false>
                                        : (const void*)fold_gemm_kernel<8, false>);
-    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)),
-               "smem attribute");
+    set_smem_attr((const void*)k, smem);
     const int threads = Q == 16 ? 512 : 256;
     const int grid = grid_for(c, k, threads, smem, bs.units);
     if (coltree)
@@ -1920,9 +2265,7 @@ template <int VMAX, bool HAS_B, bool VEC>
 void run_pow2(const LaunchCtx& c, const GroupParams& p, int threads, size_t smem,
               const double* ta, const double* tb, double* tout) {
   auto k = group_pow2_kernel<VMAX, HAS_B, VEC>;
-  check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)),
-             "smem attribute");
+  set_smem_attr((const void*)k, smem);
   const int grid = grid_for(c, (const void*)k, threads, smem, p.g.groups);
   k<<<grid, threads, smem, c.stream>>>(p, ta, tb, tout);
   post_launch(c, "group pow2 kernel");
@@ -1953,9 +2296,7 @@ void run_tma(const LaunchCtx& c, const GroupParams& p, const double* ta, const d
   if (nstages < 2) invalid_argument("TMA path needs two ring stages");
   const size_t smem = tile_bytes + nstages * (stage_bytes + 16);
   auto k = group_tma_kernel<VMAX, HAS_B>;
-  check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)),
-             "smem attribute");
+  set_smem_attr((const void*)k, smem);
   const int grid = grid_for(c, (const void*)k, kTmaThreads, smem, p.g.groups);
   k<<<grid, kTmaThreads, smem, c.stream>>>(p, ta, tb, tout, nstages);
   post_launch(c, "group tma kernel");
@@ -1972,9 +2313,7 @@ void run_tma_win(const LaunchCtx& c, const GroupParams& p, int halo, const doubl
   if (nstages < 2) invalid_argument("window path needs two ring stages");
   const size_t smem = fixed + nstages * (stage_bytes + 16);
   auto k = group_tma_win_kernel<HAS_B>;
-  check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)),
-             "smem attribute");
+  set_smem_attr((const void*)k, smem);
   const int grid = grid_for(c, (const void*)k, kTmaThreads, smem, p.g.groups);
   k<<<grid, kTmaThreads, smem, c.stream>>>(p, ta, tb, tout, nstages, halo);
   post_launch(c, "group tma window kernel");
@@ -2175,9 +2514,7 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
   if (phys <= c.smem_optin) {
     p.use_smem = 1;
     smem = phys;
-    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)),
-               "smem attribute");
+    set_smem_attr((const void*)k, smem);
   }
   const int grid = grid_for(c, (const void*)k, gthreads, smem, g.groups);
   if (!p.use_smem) scratch = c.scratch(c.scratch_owner, phys * static_cast<size_t>(grid));

@@ -41,6 +41,11 @@ void launch_unpack(const LaunchCtx& c, const Shape& shape, int64_t s, const doub
                    double* dense);
 // TMA tensor-map pack / unpack (tt_tma_pack.cu); return false when the shape
 // is not eligible (replication, `~`, relaxed, rank > 5, odd last extent...).
+// Encodes a float64 tiled tensor map (CUtensorMap, 128 bytes at map128):
+// dims/box innermost first, stride_bytes for dims 1..rank-1.  False if the
+// driver entry point is missing or the geometry is not expressible.
+bool encode_tensor_map_f64(void* map128, int rank, const void* base, const uint64_t* dims,
+                           const uint64_t* stride_bytes, const uint32_t* box);
 bool launch_pack_tma(const LaunchCtx& c, const Shape& shape, int64_t s, const double* dense,
                      double* tiles);
 bool launch_unpack_tma(const LaunchCtx& c, const Shape& shape, int64_t s, const double* tiles,

@@ -301,6 +301,24 @@ bool launch_tma_copy(const LaunchCtx& c, const Shape& sh, int64_t s, const doubl
 
 }  // namespace
 
+bool encode_tensor_map_f64(void* map128, int rank, const void* base, const uint64_t* dims,
+                           const uint64_t* stride_bytes, const uint32_t* box) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc || rank < 1 || rank > 5) return false;
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t bx[5], estride[5];
+  for (int k = 0; k < rank; ++k) {
+    gdim[k] = dims[k];
+    bx[k] = box[k];
+    estride[k] = 1;
+    if (k > 0) gstride[k - 1] = stride_bytes[k - 1];
+  }
+  return enc(static_cast<CUtensorMap*>(map128), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank,
+             const_cast<void*>(base), gdim, gstride, bx, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool launch_pack_tma(const LaunchCtx& c, const Shape& shape, int64_t s, const double* dense,
                      double* tiles) {
   return launch_tma_copy<true>(c, shape, s, dense, tiles);

@@ -107,18 +107,30 @@ def _ceil_div(a: int, b: int) -> int:
     return (a + b - 1) // b
 
 
+# shapes decoded from C structs, by struct bytes (shapes are immutable values)
+_FROM_C_CACHE: dict = {}
+
+
 class TileTensorShape:
     """TileTensorShape shape.hpp:72-138 (validated by the native library)."""
 
-    __slots__ = ("_dims", "_relaxed")
+    __slots__ = ("_dims", "_relaxed", "_c", "_tiles")
 
     def __init__(self, dims: Sequence[DimSpec], relaxed: bool = False):
         self._dims = tuple(dims)
         self._relaxed = bool(relaxed)
+        self._c = None
+        self._tiles = None
         _check(lib().tt_shape_check(ctypes.byref(self.to_c())))
 
     # construction helpers
     def to_c(self) -> CShape:
+        """The C struct (cached: shapes are immutable and the C ABI takes them const)."""
+        if self._c is None:
+            self._c = self._make_c()
+        return self._c
+
+    def _make_c(self) -> CShape:
         c = CShape()
         c.rank = len(self._dims)
         c.relaxed = 1 if self._relaxed else 0
@@ -132,11 +144,20 @@ class TileTensorShape:
 
     @classmethod
     def from_c(cls, c: CShape) -> "TileTensorShape":
+        key = bytes(c)
+        obj = _FROM_C_CACHE.get(key)
+        if obj is not None:
+            return obj
         obj = cls.__new__(cls)
         obj._dims = tuple(
             DimSpec(c.dims[i].n, c.dims[i].d, c.dims[i].t, bool(c.dims[i].unknown),
                     bool(c.dims[i].interleaved)) for i in range(c.rank))
         obj._relaxed = bool(c.relaxed)
+        obj._c = None
+        obj._tiles = None
+        if len(_FROM_C_CACHE) >= 4096:
+            _FROM_C_CACHE.clear()
+        _FROM_C_CACHE[key] = obj
         return obj
 
     def rank(self) -> int:
@@ -164,10 +185,12 @@ class TileTensorShape:
         return [_ceil_div(d.used(), d.t) for d in self._dims]
 
     def tile_count(self) -> int:
-        p = 1
-        for e in self.external_extents():
-            p *= e
-        return p
+        if self._tiles is None:
+            p = 1
+            for e in self.external_extents():
+                p *= e
+            self._tiles = p
+        return self._tiles
 
     def used_slots(self) -> int:
         p = 1
@@ -306,6 +329,7 @@ class Session:
         self._slots = int(slot_count)
         self._depth = int(max_chain_index)
         self._device = int(device)
+        self._stream = None  # stream last bound to the native session
 
     def __del__(self):
         p = getattr(self, "_ptr", None)
@@ -320,7 +344,9 @@ class Session:
     def handle(self):
         torch = _torch()
         stream = torch.cuda.current_stream(self._device).cuda_stream
-        _check(lib().tt_session_set_stream(self._ptr, ctypes.c_void_p(stream)))
+        if stream != self._stream:  # re-bind only when torch's current stream changed
+            _check(lib().tt_session_set_stream(self._ptr, ctypes.c_void_p(stream)))
+            self._stream = stream
         return self._ptr
 
     def slot_count(self) -> int:
@@ -508,17 +534,26 @@ def tt_mul_sum(a: TileTensor, b: TileTensor, dim: int,
     return TileTensor(TileTensorShape.from_c(so), out, s, chain.value)
 
 
+_PRODUCT_TILES: dict = {}
+
+
 def _product(which: int, a: TileTensor, b: TileTensor, variant) -> TileTensor:
     s = _same_session(a, b)
     so = CShape()
     chain = ctypes.c_int64()
     # allocate from the worst case (the product's summed shape) after validation
-    try:
-        prod = elementwise_result_shape(a.shape(), b.shape(), OpKind.mul)
-        dim = 2 if which in (0, 2) else 1
-        n_out = sum_result_shape(prod, dim).tile_count()
-    except ShapeError:
-        n_out = 0
+    key = (which, a.shape(), b.shape())
+    n_out = _PRODUCT_TILES.get(key)
+    if n_out is None:
+        try:
+            prod = elementwise_result_shape(a.shape(), b.shape(), OpKind.mul)
+            dim = 2 if which in (0, 2) else 1
+            n_out = sum_result_shape(prod, dim).tile_count()
+        except ShapeError:
+            n_out = 0
+        if len(_PRODUCT_TILES) >= 4096:
+            _PRODUCT_TILES.clear()
+        _PRODUCT_TILES[key] = n_out
     out = s.empty_tiles(max(n_out, 1))
     _check(lib().tt_linalg_product(s.handle, which, ctypes.byref(a.shape().to_c()),
                                    _ptr(a.data()), a.chain_index(),
