@@ -30,6 +30,10 @@ struct tt_session {
   uint64_t launches = 0;
   std::mutex mu;  // serialises launches + scratch (counters are atomic)
   double* scratch = nullptr;
+  // work-queue counters of dynamically scheduled kernels: a ring of
+  // kSchedSlots (next, done) pairs, each left at zero by the launch using it
+  unsigned int* sched = nullptr;
+  unsigned int sched_next = 0;
   size_t scratch_bytes = 0;
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;
@@ -93,6 +97,8 @@ LaunchCtx ctx_of(tt_session* s) {
   c.launches = &s->launches;
   c.scratch = scratch_fn;
   c.scratch_owner = s;
+  c.sched_base = s->sched;
+  c.sched_next = &s->sched_next;
   return c;
 }
 
@@ -338,6 +344,9 @@ int tt_session_create(int64_t slot_count, int64_t max_chain_index, int device, t
       check_cuda(cudaGetDeviceProperties(&prop, device), "device properties");
       s->sm_count = prop.multiProcessorCount;
       s->smem_optin = prop.sharedMemPerBlockOptin;
+      const size_t sched_bytes = 2 * kSchedSlots * sizeof(unsigned int);
+      check_cuda(cudaMalloc(&s->sched, sched_bytes), "scheduler counters");
+      check_cuda(cudaMemset(s->sched, 0, sched_bytes), "scheduler counters");
     } catch (...) {
       delete s;
       throw;
@@ -351,6 +360,7 @@ void tt_session_destroy(tt_session* s) {
   cudaSetDevice(s->device);
   if (s->own_stream) cudaStreamSynchronize(s->own_stream);
   if (s->scratch) cudaFree(s->scratch);
+  if (s->sched) cudaFree(s->sched);
   if (s->own_stream) cudaStreamDestroy(s->own_stream);
   delete s;
 }

@@ -1565,7 +1565,7 @@ __host__ __device__ constexpr int tg_warps() {
 template <int BC, int SL, int kTgSteps, int kTgStages>
 __host__ __device__ constexpr size_t tg_smem_bytes() {
   return static_cast<size_t>(kTgStages) * kTgSteps * (kGemmBlk + BC) * SL * sizeof(double) +
-         2 * kTgStages * sizeof(uint64_t);
+         3 * kTgStages * sizeof(uint64_t);
 }
 
 struct TgUnit {
@@ -1597,7 +1597,8 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
     fold_gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
                          const __grid_constant__ CUtensorMap mapB,
                          const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
-                         const __grid_constant__ TgSpec ts, double* __restrict__ OUT) {
+                         const __grid_constant__ TgSpec ts, double* __restrict__ OUT,
+                         unsigned int* __restrict__ sched) {
   constexpr int kW = tg_warps<BC, SL, SC>();
   constexpr int kTgRows = 8 / SC;  // rows of products batched before their adds
   constexpr int kA = kTgSteps * kGemmBlk * SL;  // doubles per stage
@@ -1606,6 +1607,7 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
   extern __shared__ __align__(1024) double tsm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm + kTgStages * kStage);
   uint64_t* empty = full + kTgStages;
+  uint64_t* stage_unit = empty + kTgStages;  // unit loaded into each stage (~0: no more)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool issuer = threadIdx.x == 0;
   if (issuer) {
@@ -1621,10 +1623,15 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
   const int nst = (cnt + kTgSteps - 1) / kTgSteps;  // stages per unit
   const uint64_t units = static_cast<uint64_t>(bs.units);
 
-  // load sequence of this CTA (issuer only): unit lu, stage k of that unit
+  // load sequence of this CTA (issuer only): unit lu, stage k of that unit.
+  // The first unit is blockIdx.x; later ones come from the launch's work
+  // queue (sched[0], so SMs that run ahead take more units) or, without one,
+  // statically every gridDim.x.  When none is left the issuer publishes a
+  // ~0 unit on the next stage, which ends every warp's loop.
   uint64_t lu = blockIdx.x;
   int lk = 0, lstage = 0;
   uint32_t lphase = 0;
+  bool ended = false;
   int rc[2] = {0, 0};
   TgUnit lt{};
   auto load_unit = [&]() {
@@ -1640,8 +1647,16 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
     }
   };
   auto issue_next = [&]() {
-    if (lu >= units) return;
+    if (lu >= units) {
+      if (ended) return;
+      mbar_wait(&empty[lstage], lphase ^ 1);
+      stage_unit[lstage] = ~uint64_t{0};
+      mbar_arrive(&full[lstage]);
+      ended = true;
+      return;
+    }
     mbar_wait(&empty[lstage], lphase ^ 1);  // every warp has released this buffer
+    stage_unit[lstage] = lu;
     mbar_arrive_expect_tx(&full[lstage], kStage * sizeof(double));
     double* st = tsm + lstage * kStage;
     const int j0 = static_cast<int>(lt.chunk * SL);
@@ -1655,12 +1670,12 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
     }
     if (++lk == nst) {
       lk = 0;
-      lu += gridDim.x;
+      lu = sched ? gridDim.x + atomicAdd(&sched[0], 1u) : lu + gridDim.x;
       if (lu < units) load_unit();
     }
   };
-  if (issuer && lu < units) {
-    load_unit();
+  if (issuer) {
+    if (lu < units) load_unit();
     for (int i = 0; i < kTgStages - 1; ++i) issue_next();
   }
 
@@ -1668,7 +1683,12 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
   const int r0 = (sub / (BC / SC)) * 8, c0 = (sub % (BC / SC)) * SC;
   int stage = 0;
   uint32_t phase = 0;
-  for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
+  for (;;) {
+    if (issuer) issue_next();  // refills the buffer released one stage ago
+    __syncwarp();
+    mbar_wait(&full[stage], phase);
+    const uint64_t u = stage_unit[stage];
+    if (u == ~uint64_t{0}) break;
     const TgUnit t = tg_decode(bs, u, ts.chunk_major);
     double acc[8][SC];
 #pragma unroll
@@ -1696,9 +1716,11 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
       }
     };
     for (int k = 0; k < nst; ++k) {
-      if (issuer) issue_next();  // refills the buffer released one stage ago
-      __syncwarp();
-      mbar_wait(&full[stage], phase);
+      if (k > 0) {
+        if (issuer) issue_next();
+        __syncwarp();
+        mbar_wait(&full[stage], phase);
+      }
       const double* sA = tsm + stage * kStage + r0 * SL + slot;
       const double* sB = tsm + stage * kStage + kA + c0 * SL + slot;
       const int nsteps = cnt - k * kTgSteps;
@@ -1731,6 +1753,15 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
           if (c0 + k < nq) st_keep(orow + k * cstep, acc[i][k], keep);
       }
       orow += rstep;
+    }
+  }
+  // the last CTA to finish leaves the queue counters at zero for the next launch
+  if (issuer && sched) {
+    __threadfence();
+    if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
     }
   }
 }
@@ -2075,6 +2106,11 @@ BlockPlan block_plan(const GroupSpec& g, bool has_b) {
 // Launches fold_gemm_tma_kernel when both operands are expressible as 5-D
 // tensor maps (<= 2 remaining group dims, non-zero fold strides); false
 // otherwise (the caller falls back to the cp.async GEMM fold).
+// TT_GEMM_DYNAMIC=0: static round-robin units instead of the work queue
+const int g_gemm_dynamic = [] {
+  const char* e = std::getenv("TT_GEMM_DYNAMIC");
+  return e ? std::atoi(e) : 1;
+}();
 const int g_gemm_order = [] {
   const char* e = std::getenv("TT_GEMM_ORDER");
   return e ? std::atoi(e) : 0;
@@ -2134,8 +2170,10 @@ bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupPar
   constexpr int threads = tg_warps<BC, SL, SC>() * 32;
   set_smem_attr((const void*)k, smem);
   const int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
+  unsigned int* sched = g_gemm_dynamic ? take_sched_slot(c) : nullptr;
   k<<<grid, threads, smem, c.stream>>>(*reinterpret_cast<const CUtensorMap*>(mapA),
-                                       *reinterpret_cast<const CUtensorMap*>(mapB), pr, bs, ts, tout);
+                                       *reinterpret_cast<const CUtensorMap*>(mapB), pr, bs, ts, tout,
+                                       sched);
   post_launch(c, "gemm fold kernel (TMA)");
   return true;
 }

@@ -18,7 +18,21 @@ struct LaunchCtx {
   // Session-owned device scratch; (re)sized by the caller via `need`.
   double* (*scratch)(void* owner, size_t bytes) = nullptr;
   void* scratch_owner = nullptr;
+  // Session-owned ring of work-queue counter pairs (next unit, CTAs done).
+  unsigned int* sched_base = nullptr;
+  unsigned int* sched_next = nullptr;
 };
+
+constexpr unsigned int kSchedSlots = 256;
+// The (next, done) counter pair for one dynamically scheduled launch.  The
+// kernel's last CTA resets both to zero, so a slot is reusable by the next
+// launch on the stream; concurrent launches (different streams) get distinct
+// slots of the ring.
+inline unsigned int* take_sched_slot(const LaunchCtx& c) {
+  if (!c.sched_base) return nullptr;
+  const unsigned int i = (*c.sched_next)++ % kSchedSlots;
+  return c.sched_base + 2 * i;
+}
 
 // Group grid of a reduction: output tile ("group") g is addressed by
 // coordinates c_0..c_{nd-1} in iteration order (outermost first); its output
