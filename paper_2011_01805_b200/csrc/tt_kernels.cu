@@ -1864,6 +1864,56 @@ __global__ void __launch_bounds__(256) row_tree_kernel(const double* __restrict_
   }
 }
 
+// (C) whole tile in shared memory: a CTA of s / PER threads holds one tile
+// in registers (thread t owns slots t + i * T), and each power-of-two level
+// v'[j] = v[j] + v[(j + r) mod s] exchanges through shared memory (store,
+// barrier, load the partner, barrier).  Any rotations, one global read and
+// one global write per slot, in place.  Several CTAs per SM overlap one
+// tile's loads with another's levels.
+__device__ __forceinline__ int level_rot(int k, const int4& a, const int4& b) {
+  switch (k) {
+    case 0: return a.x;
+    case 1: return a.y;
+    case 2: return a.z;
+    case 3: return a.w;
+    case 4: return b.x;
+    case 5: return b.y;
+    case 6: return b.z;
+    default: return b.w;
+  }
+}
+
+constexpr int kTreeThreads = 256;
+template <int PER>
+__global__ void __launch_bounds__(kTreeThreads, 2) smem_tree_kernel(double* __restrict__ tiles,
+                                                                    int64_t n_tiles, int nlevels,
+                                                                    int4 lv0, int4 lv1) {
+  extern __shared__ double tsh[];
+  constexpr int T = kTreeThreads, s = T * PER;
+  const int tid = threadIdx.x;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    double* t = tiles + tile * s;
+    double v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) v[i] = t[tid + i * T];
+    for (int k = 0; k < nlevels; ++k) {
+      const int r = level_rot(k, lv0, lv1);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) tsh[tid + i * T] = v[i];
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        int j = tid + i * T + r;
+        if (j >= s) j -= s;
+        v[i] = dadd(v[i], tsh[j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) t[tid + i * T] = v[i];
+  }
+}
+
 // ---- synthetic input generator (== or_fill_uniform in oracle/tt_oracle.c) ------------
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -2374,16 +2424,32 @@ void dispatch_tma(const LaunchCtx& c, const GroupParams& p, const double* ta, co
 // Tree-only passes (phase 2), register-resident.  kind 1 = column-local (in
 // place on OUT), kind 2 = row-shift (reads the folded tiles from a separate
 // buffer, writes OUT); 0 = none applies.
+// TT_TREE_SMEM=1 selects the whole-tile shared-memory tree pass (kind 3)
+// for any eligible schedule.  Correct for any rotations, but measured slower
+// than the column / row passes on config 3 (chain 116 vs 102 us: two 64 KiB
+// CTAs per SM leave too few loads in flight), so it is opt-in.
+const int g_tree_smem = [] {
+  const char* e = std::getenv("TT_TREE_SMEM");
+  return e ? std::atoi(e) : 0;
+}();
+
 struct TreePass {
   int kind = 0;
   int hr = 0;
   int64_t stride0 = 0, t = 0;
 };
 
-TreePass plan_tree_pass(const GroupParams& p2, int64_t s) {
+TreePass plan_tree_pass(const GroupParams& p2, int64_t s, size_t smem_optin) {
   TreePass tp;
   const int L = p2.nlevels;
   if (L < 1 || L > 8) return tp;
+  // whole-tile shared-memory tree: any rotations, tile <= 64 KiB (>= 3 CTAs/SM)
+  if (g_tree_smem && (s == 16 * kTreeThreads || s == 32 * kTreeThreads) &&
+      static_cast<size_t>(s) * sizeof(double) <= smem_optin) {
+    tp.kind = 3;
+    tp.t = int64_t{1} << L;
+    return tp;
+  }
   const int64_t stride0 = p2.rots[0];
   for (int i = 1; i < L; ++i)
     if (p2.rots[i] != stride0 << i) return tp;
@@ -2410,6 +2476,22 @@ TreePass plan_tree_pass(const GroupParams& p2, int64_t s) {
 
 void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2, int64_t n_tiles,
                    int64_t s, const double* folded, double* tout) {
+  if (tp.kind == 3) {  // in place: folded == tout
+    int lv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < p2.nlevels; ++i) lv[i] = static_cast<int>(p2.rots[i]);
+    const size_t smem = static_cast<size_t>(s) * sizeof(double);
+    const void* k = s == 32 * kTreeThreads ? (const void*)smem_tree_kernel<32>
+                                           : (const void*)smem_tree_kernel<16>;
+    set_smem_attr(k, smem);
+    const int grid = grid_for(c, k, kTreeThreads, smem, n_tiles);
+    const int4 lv0 = make_int4(lv[0], lv[1], lv[2], lv[3]), lv1 = make_int4(lv[4], lv[5], lv[6], lv[7]);
+    if (s == 32 * kTreeThreads)
+      smem_tree_kernel<32><<<grid, kTreeThreads, smem, c.stream>>>(tout, n_tiles, p2.nlevels, lv0, lv1);
+    else
+      smem_tree_kernel<16><<<grid, kTreeThreads, smem, c.stream>>>(tout, n_tiles, p2.nlevels, lv0, lv1);
+    post_launch(c, "shared-memory tree pass");
+    return;
+  }
   if (tp.kind == 1) {  // in place: folded == tout
     const int64_t stride0 = tp.stride0;
     const uint64_t total = static_cast<uint64_t>(n_tiles) * stride0;
@@ -2488,7 +2570,7 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
       // phase 2 plan first: the row-shift pass needs the folded tiles in a
       // separate buffer, so phase 1 then folds into session scratch
       TreePass tpass;
-      if (force == 0 || force == 4) tpass = plan_tree_pass(p, s);
+      if (force == 0 || force == 4) tpass = plan_tree_pass(p, s, c.smem_optin);
       double* fold_dst = tout;
       if (tpass.kind == 2)
         fold_dst = c.scratch(c.scratch_owner, static_cast<size_t>(g.groups) * tile_bytes);

@@ -37,6 +37,16 @@ if "--time" in sys.argv:
     e1.record()
     torch.cuda.synchronize()
     print(f"c3b chain: {e0.elapsed_time(e1) / n * 1e3:.1f} us")
+    s1 = tt.matmul_b(T["Bt3"], T["C3"])
+    for name, fn in (("matmul_b", lambda: tt.matmul_b(T["Bt3"], T["C3"])),
+                     ("matmul_a", lambda: tt.matmul_a(T["A3"], s1))):
+        fn()
+        e0.record()
+        for _ in range(n):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"  {name}: {e0.elapsed_time(e1) / n * 1e3:.1f} us")
 if "--host" in sys.argv:
     import time
     import cProfile
