@@ -431,6 +431,9 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+FP64_PEAK_OPS = 18.34e12  # B200, 148 SMs x 64 FP64 lanes at boost (profiles/r01_fp64_peak.txt)
+
+
 def bench_matmul(tt, configs, S, stream, hbm_peak, reps):
     """Config 3 ('3b': matmul_b then matmul_a, no repacking) on 8192-slot tiles."""
     import torch
@@ -449,8 +452,16 @@ def bench_matmul(tt, configs, S, stream, hbm_peak, reps):
     # unique operand tiles + out tiles of both stages
     alg = (1536 + 768 + 512 + 512 + 1024 + 512 + 512) * tile
     prod_tiles = 24576 + 16384
+    # the fold is FP64-issue bound, not HBM bound: one DMUL + one DADD per
+    # product slot (no contraction -- bit parity), against the measured
+    # register-only DMUL+DADD rate (tools/micro/fp64_peak.cu,
+    # profiles/r01_fp64_peak.txt)
+    fp64_ops = 2 * prod_tiles * 8192
     return {"matmul_c3b": {"ms": t * 1e3, "GB/s": alg / t / 1e9, "frac": alg / t / 1e9 / hbm_peak,
                            "tile_slots_per_s": prod_tiles * 8192 / t, "alg_bytes": alg,
+                           "fp64_tops": fp64_ops / t / 1e12,
+                           "fp64_frac": fp64_ops / t / FP64_PEAK_OPS,
+                           "fp64_peak_source": "measured DMUL+DADD issue rate, 18.34e12 thread-ops/s",
                            "note": "Bt3[768/16,1024/32,*/16] x C3[768/16,*/32,256/16] -> matmul_a(A3, .)"}}
 
 

@@ -246,6 +246,58 @@ int ref_linalg(int which, const tt_shape* sa, const double* ta, const tt_shape* 
   });
 }
 
+// pipeline (linalg.hpp:213-260) on k matrices packed back to back in
+// `mats` (matrix i is rows[i] x cols[i], row-major), vector v of length n;
+// returns the output shape, tiles and the cost since the start.
+int ref_pipeline(const double* mats, const int64_t* rows, const int64_t* cols, int k,
+                 const double* v, int64_t n, int64_t t1, int64_t t2, int64_t slots,
+                 int64_t depth, tt_shape* so, double* out, tt_cost* c) {
+  return guard([&] {
+    std::vector<DenseTensor> ms;
+    const double* p = mats;
+    for (int i = 0; i < k; ++i) {
+      const int64_t cnt = rows[i] * cols[i];
+      ms.emplace_back(std::vector<std::int64_t>{rows[i], cols[i]}, std::vector<double>(p, p + cnt));
+      p += cnt;
+    }
+    Session session(slots, depth);
+    const DenseTensor dv({n}, std::vector<double>(v, v + n));
+    const auto res = pipeline(ms, dv, {t1, t2}, session);
+    from_ref(res.out.shape(), so);
+    dump_tiles(res.out, out);
+    c->additions = res.cost.additions;
+    c->multiplications = res.cost.multiplications;
+    c->mask_multiplications = res.cost.mask_multiplications;
+    c->rotations = res.cost.rotations;
+    c->bootstraps = res.cost.bootstraps;
+    c->power_of_two_rotations = res.cost.power_of_two_rotations;
+  });
+}
+
+// score_tile_factorizations (linalg.hpp:279-294): writes up to `cap`
+// (t1, rotations, total_ops) triples in the reference's order; returns count.
+int ref_score_tile_factorizations(const double* mats, const int64_t* rows, const int64_t* cols,
+                                  int k, const double* v, int64_t n, int64_t slots, int64_t depth,
+                                  int64_t* triples, int cap, int* count) {
+  return guard([&] {
+    std::vector<DenseTensor> ms;
+    const double* p = mats;
+    for (int i = 0; i < k; ++i) {
+      const int64_t cnt = rows[i] * cols[i];
+      ms.emplace_back(std::vector<std::int64_t>{rows[i], cols[i]}, std::vector<double>(p, p + cnt));
+      p += cnt;
+    }
+    const DenseTensor dv({n}, std::vector<double>(v, v + n));
+    const auto choices = score_tile_factorizations(ms, dv, slots, depth);
+    *count = static_cast<int>(choices.size());
+    for (int i = 0; i < *count && i < cap; ++i) {
+      triples[3 * i] = choices[i].t1;
+      triples[3 * i + 1] = static_cast<int64_t>(choices[i].cost.rotations);
+      triples[3 * i + 2] = static_cast<int64_t>(choices[i].cost.total_ops());
+    }
+  });
+}
+
 int ref_clean_unknowns(const tt_shape* sh, const double* tin, int64_t slots, tt_shape* so,
                        double* out, tt_cost* c) {
   return guard([&] {

@@ -418,10 +418,126 @@ static void linalg() {
   CHECK_THROWS_AS(matvec_a(tm1, tx), ShapeError);  // rank-3 operands
 }
 
+// chain of dense matrix-vector products (the pipeline's oracle)
+static DenseTensor chain_oracle(const std::vector<DenseTensor>& ms, const DenseTensor& v) {
+  DenseTensor x = v.reshape({static_cast<std::int64_t>(v.size()), 1});
+  for (const auto& m : ms) x = dense_matmul(m, x);
+  return x.reshape({static_cast<std::int64_t>(x.size())});
+}
+
+static DenseTensor identity_matrix(std::int64_t n) {
+  std::vector<double> v(static_cast<std::size_t>(n * n), 0.0);
+  for (std::int64_t i = 0; i < n; ++i) v[static_cast<std::size_t>(i * n + i)] = 1.0;
+  return DenseTensor({n, n}, std::move(v));
+}
+
+// packing methods, the alternating pipeline and the tile-extent search
+// (inc/linalg.hpp:77-294; behaviour as pinned by tests/test_linalg.cpp:181-326)
+static void pipeline_suite() {
+  std::mt19937_64 rng(9009);
+  {  // every special-case packing runs through the same two-line body
+    const DenseTensor m = random_tensor({5, 3}, rng, -1, 1);
+    const DenseTensor v = random_tensor({3}, rng, -1, 1);
+    const DenseTensor expect = chain_oracle({m}, v);
+    for (const auto& method : {PackingMethod::row_order(), PackingMethod::column_order(),
+                               PackingMethod::input_packing(), PackingMethod::general({4, 4})}) {
+      Session session(16, 8);
+      const bool inp = method.kind == PackingMethod::Kind::input_packing;
+      const TileTensor tm = pack_for_method(m, inp ? OperandRole::lhs : OperandRole::matrix, method, session);
+      const TileTensor tv = pack_for_method(v, inp ? OperandRole::rhs : OperandRole::vector, method, session);
+      CHECK(max_rel_diff(unpack_vector(tt_sum(tt_mul(tm, tv), sum_dim_for(method))), expect) < 1e-9);
+    }
+    Session session(16, 8);
+    const DenseTensor batch = random_tensor({3, 7}, rng, -1, 1);
+    const TileTensor tw = pack_for_method(m, OperandRole::matrix, PackingMethod::batch_packing(), session);
+    const TileTensor tb = pack_for_method(batch, OperandRole::vector, PackingMethod::batch_packing(), session);
+    CHECK(format_shape(tw.shape()) == "[5,3,*/16]");
+    CHECK(format_shape(tb.shape()) == "[3,7/16]");
+    session.reset_counters();
+    const TileTensor r = tt_sum(tt_mul(tw, with_leading_unit_dim(tb)), 2);
+    CHECK(session.cost_report().rotations == 0);
+    CHECK(max_rel_diff(unpack(r).reshape({5, 7}), dense_matmul(m, batch)) < 1e-9);
+  }
+  {  // input packing: smallest divisor of s that fits the contracted extent
+    Session session(16, 8);
+    const TileTensor tm = pack_for_method(random_tensor({4, 3}, rng, -1, 1), OperandRole::lhs,
+                                          PackingMethod::input_packing(), session);
+    CHECK(format_shape(tm.shape()) == "[3/4,4/4]");
+    CHECK_THROWS_AS(pack_for_method(random_tensor({2, 17}, rng, -1, 1), OperandRole::lhs,
+                                    PackingMethod::input_packing(), session),
+                    ShapeError);
+  }
+  {  // general packing fills every slot
+    Session session(1024, 2);
+    const DenseTensor m = random_tensor({768, 768}, rng, -1, 1);
+    const TileTensor g = pack_for_method(m, OperandRole::matrix, PackingMethod::general({4, 256}), session);
+    CHECK(g.tile_count() == 576);
+    CHECK(g.shape().used_slots() == g.shape().total_slots());
+    CHECK(pack_for_method(m, OperandRole::matrix, PackingMethod::row_order(), session).tile_count() == 768);
+  }
+  {  // identities, one stage, three and four stages, two stages without masks
+    Session s8(8, 8);
+    const DenseTensor v3({3}, {1, 2, 3});
+    const std::vector<DenseTensor> ids{identity_matrix(3), identity_matrix(3)};
+    CHECK(max_rel_diff(unpack_vector(pipeline(ids, v3, {2, 4}, s8).out), v3) < 1e-12);
+    const DenseTensor m = random_tensor({5, 6}, rng, -1, 1), v = random_tensor({6}, rng, -1, 1);
+    const auto one = pipeline(std::vector<DenseTensor>{m}, v, {2, 4}, s8);
+    CHECK(format_shape(one.out.shape()) == "[*/2,5/4]");
+    CHECK(one.cost.mask_multiplications == 0);
+    CHECK(max_rel_diff(unpack_vector(one.out), chain_oracle({m}, v)) < 1e-9);
+
+    Session s32(32, 8);
+    const std::vector<DenseTensor> three{random_tensor({5, 7}, rng, -1, 1), random_tensor({9, 5}, rng, -1, 1),
+                                         random_tensor({7, 9}, rng, -1, 1)};
+    const DenseTensor v7 = random_tensor({7}, rng, -1, 1);
+    const auto r3 = pipeline(three, v7, {4, 8}, s32);
+    CHECK(max_rel_diff(unpack_vector(r3.out), chain_oracle(three, v7)) < 1e-9);
+    CHECK(r3.cost.mask_multiplications > 0);
+
+    Session s16(16, 16);
+    const std::vector<DenseTensor> two{random_tensor({6, 4}, rng, -1, 1), random_tensor({3, 6}, rng, -1, 1)};
+    const DenseTensor v4 = random_tensor({4}, rng, -1, 1);
+    const auto r2 = pipeline(two, v4, {4, 4}, s16);
+    CHECK(r2.cost.mask_multiplications == 0);
+    CHECK(max_rel_diff(unpack_vector(r2.out), chain_oracle(two, v4)) < 1e-9);
+    const std::vector<DenseTensor> four{random_tensor({5, 4}, rng, -1, 1), random_tensor({7, 5}, rng, -1, 1),
+                                        random_tensor({6, 7}, rng, -1, 1), random_tensor({3, 6}, rng, -1, 1)};
+    const auto r4 = pipeline(four, v4, {4, 4}, s16);
+    CHECK(max_rel_diff(unpack_vector(r4.out), chain_oracle(four, v4)) < 1e-9);
+    CHECK(r4.cost.mask_multiplications == 2);  // one seam: [7/4,1?/4] -> two tiles masked
+  }
+  {  // validation and depth exhaustion naming the stage
+    Session s8(8, 8);
+    CHECK_THROWS_AS(pipeline(std::vector<DenseTensor>{random_tensor({3, 4}, rng, -1, 1)},
+                             random_tensor({5}, rng, -1, 1), {2, 4}, s8),
+                    ShapeError);
+    CHECK_THROWS_AS(pipeline(std::vector<DenseTensor>{random_tensor({3, 4}, rng, -1, 1)},
+                             random_tensor({4}, rng, -1, 1), {3, 4}, s8),
+                    ShapeError);
+    Session shallow(8, 2);
+    const std::vector<DenseTensor> ms{random_tensor({4, 4}, rng, -1, 1), random_tensor({4, 4}, rng, -1, 1),
+                                      random_tensor({4, 4}, rng, -1, 1)};
+    bool named = false;
+    try {
+      (void)pipeline(ms, random_tensor({4}, rng, -1, 1), {2, 4}, shallow);
+    } catch (const DepthExhaustedError& e) {
+      named = std::string(e.what()).find("stage") != std::string::npos;
+    }
+    CHECK(named);
+  }
+  {  // the search scores every divisor pair, ordered by rotations
+    const std::vector<DenseTensor> ms{random_tensor({4, 6}, rng, -1, 1), random_tensor({5, 4}, rng, -1, 1)};
+    const auto choices = score_tile_factorizations(ms, random_tensor({6}, rng, -1, 1), 16, 8);
+    CHECK(choices.size() == 5);
+    for (std::size_t i = 1; i < choices.size(); ++i)
+      CHECK(choices[i - 1].cost.rotations <= choices[i].cost.rotations);
+  }
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> suites = {
       {"shapes", shapes}, {"backend", backend}, {"rotate_sum", rotate_sum},
-      {"tile_tensor", tile_tensor}, {"linalg", linalg}};
+      {"tile_tensor", tile_tensor}, {"linalg", linalg}, {"pipeline", pipeline_suite}};
   for (const auto& [name, fn] : suites) {
     const int before = g_failed;
     try {

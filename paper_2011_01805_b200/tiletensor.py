@@ -707,4 +707,184 @@ def device_count() -> int:
     return n.value
 
 
+# ---- packing methods, the alternating pipeline, tile-extent search ---------------------
+# (linalg.hpp:77-294).  Host orchestration of the device ops above: packs,
+# fused matvec passes, clean_unknowns and replicate_dim.
+
+
+class PackingMethod:  # linalg.hpp:77-89
+    class Kind(enum.Enum):
+        row_order = 0
+        column_order = 1
+        input_packing = 2
+        batch_packing = 3
+        general = 4
+
+    def __init__(self, kind: "PackingMethod.Kind", tile: Sequence[int] = ()):
+        self.kind = kind
+        self.tile = list(tile)
+
+    @staticmethod
+    def row_order():
+        return PackingMethod(PackingMethod.Kind.row_order)
+
+    @staticmethod
+    def column_order():
+        return PackingMethod(PackingMethod.Kind.column_order)
+
+    @staticmethod
+    def input_packing():
+        return PackingMethod(PackingMethod.Kind.input_packing)
+
+    @staticmethod
+    def batch_packing():
+        return PackingMethod(PackingMethod.Kind.batch_packing)
+
+    @staticmethod
+    def general(tile: Sequence[int]):
+        return PackingMethod(PackingMethod.Kind.general, tile)
+
+
+class OperandRole(enum.Enum):  # linalg.hpp:91
+    matrix = 0
+    vector = 1
+    lhs = 2
+    rhs = 3
+
+
+def sum_dim_for(method: PackingMethod) -> int:  # linalg.hpp:94-96
+    return 1 if method.kind == PackingMethod.Kind.input_packing else 2
+
+
+def _smallest_divisor_at_least(s: int, b: int) -> int:  # linalg.hpp:100-105
+    for t in range(max(b, 1), s + 1):
+        if s % t == 0:
+            return t
+    return s
+
+
+def _shape2(n1, d1, t1, n2, d2, t2) -> TileTensorShape:
+    return TileTensorShape([DimSpec(n1, d1, t1), DimSpec(n2, d2, t2)])
+
+
+def pack_for_method(m, role: OperandRole, method: PackingMethod, session: Session) -> TileTensor:
+    """pack_for_method linalg.hpp:114-199 (m: numpy array)."""
+    K = PackingMethod.Kind
+    m = np.asarray(m, dtype=np.float64)
+    s = session.slot_count()
+    if method.kind == K.batch_packing:
+        if role in (OperandRole.matrix, OperandRole.lhs):
+            if m.ndim != 2:
+                raise ShapeError("batch packing expects a rank-2 weight matrix")
+            a, b = m.shape
+            return pack(m.reshape(a, b, 1),
+                        TileTensorShape([DimSpec(a, 1, 1), DimSpec(b, 1, 1), DimSpec(1, s, s)]),
+                        session)
+        if m.ndim != 2:
+            raise ShapeError("batch packing expects data of shape [x, n]")
+        x, n = m.shape
+        if n > s:
+            raise ShapeError("batch size exceeds the slot count")
+        return pack(m, TileTensorShape([DimSpec(x, 1, 1), DimSpec(n, 1, s)]), session)
+    t1, t2 = 1, s
+    if method.kind == K.column_order:
+        t1, t2 = s, 1
+    elif method.kind == K.input_packing:
+        b = m.shape[1] if role in (OperandRole.lhs, OperandRole.matrix) else m.shape[0]
+        if b > s:
+            raise ShapeError("input packing requires the contracted extent <= slot count")
+        t1 = _smallest_divisor_at_least(s, b)
+        t2 = s // t1
+    elif method.kind == K.general:
+        if len(method.tile) != 2:
+            raise ShapeError("general packing here expects two tile extents")
+        t1, t2 = method.tile
+        if t1 * t2 != s:
+            raise ShapeError("tile extents must multiply to the slot count")
+    transposed = (method.kind == K.input_packing or
+                  role in (OperandRole.lhs, OperandRole.rhs))
+    if role == OperandRole.matrix:
+        if m.ndim != 2:
+            raise ShapeError("matrix role expects a rank-2 tensor")
+        mm = np.ascontiguousarray(m.T) if transposed else m
+        return pack(mm, _shape2(mm.shape[0], 1, t1, mm.shape[1], 1, t2), session)
+    if role == OperandRole.lhs:
+        if m.ndim != 2:
+            raise ShapeError("lhs role expects a rank-2 tensor")
+        mt = np.ascontiguousarray(m.T)
+        return pack(mt, _shape2(mt.shape[0], 1, t1, mt.shape[1], 1, t2), session)
+    b = m.size
+    if role == OperandRole.vector and not transposed:
+        return pack(m.reshape(1, b), _shape2(1, t1, t1, b, 1, t2), session)
+    return pack(m.reshape(b, 1), _shape2(b, 1, t1, 1, t2, t2), session)
+
+
+def unpack_vector(t: TileTensor) -> np.ndarray:  # linalg.hpp:263-266
+    return unpack(t).reshape(-1)
+
+
+@dataclass
+class PipelineResult:
+    out: TileTensor
+    cost: CostReport
+
+
+def pipeline(matrices: Sequence, v, tile: Sequence[int], session: Session) -> PipelineResult:
+    """pipeline linalg.hpp:213-260: M_k(...(M_2(M_1 v))); odd stages pack the
+    matrix transposed and sum dim 1, even stages sum dim 2 and, before a next
+    stage, clean_unknowns + replicate_dim(2) when the output is not replicated."""
+    if len(matrices) == 0:
+        raise ShapeError("pipeline needs at least one matrix")
+    t1, t2 = int(tile[0]), int(tile[1])
+    if t1 * t2 != session.slot_count():
+        raise ShapeError("tile extents must multiply to the slot count")
+    v = np.asarray(v, dtype=np.float64).reshape(-1)
+    mats = [np.asarray(m, dtype=np.float64) for m in matrices]
+    width = v.size
+    for k, m in enumerate(mats):
+        if m.ndim != 2 or m.shape[1] != width:
+            raise ShapeError(f"pipeline stage {k + 1}: matrix extents do not chain")
+        width = m.shape[0]
+    before = session.cost_report()
+    data = pack(v.reshape(-1, 1), _shape2(v.size, 1, t1, 1, t2, t2), session)
+    for k, m in enumerate(mats):
+        try:
+            if k % 2 == 0:  # odd stage k + 1
+                mt = np.ascontiguousarray(m.T)
+                tm = pack(mt, _shape2(mt.shape[0], 1, t1, mt.shape[1], 1, t2), session)
+                data = matvec_b(tm, data)
+            else:
+                tm = pack(m, _shape2(m.shape[0], 1, t1, m.shape[1], 1, t2), session)
+                data = matvec_a(tm, data)
+                if k + 1 < len(mats):
+                    data = clean_unknowns(data)
+                    if data.shape().dim(1).d < t2:
+                        data = replicate_dim(data, 2)
+        except DepthExhaustedError as e:
+            raise DepthExhaustedError(f"pipeline stage {k + 1}: {e}") from None
+    return PipelineResult(data, session.cost_report().since(before))
+
+
+@dataclass
+class TileChoice:
+    t1: int
+    t2: int
+    cost: CostReport
+
+
+def score_tile_factorizations(matrices: Sequence, v, s: int, depth: int,
+                              device: int = 0) -> list:
+    """score_tile_factorizations linalg.hpp:279-294: the pipeline under every
+    t1 * t2 = s in a scratch session, ordered by rotations then total ops."""
+    out = []
+    for t1 in range(1, s + 1):
+        if s % t1:
+            continue
+        scratch = Session(s, depth, device)
+        res = pipeline(matrices, v, (t1, s // t1), scratch)
+        out.append(TileChoice(t1, s // t1, res.cost))
+    out.sort(key=lambda c: (c.cost.rotations, c.cost.total_ops()))
+    return out
+
+
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -286,6 +286,41 @@ class Ref(_Base):
         res = TileTensorShape.from_c(so)
         return res, out[:res.tile_count()].copy(), _cost(c)
 
+    @staticmethod
+    def _chain_args(matrices, v):
+        mats = [np.ascontiguousarray(m, dtype=np.float64) for m in matrices]
+        flat = np.ascontiguousarray(np.concatenate([m.reshape(-1) for m in mats]))
+        rows = (ctypes.c_int64 * len(mats))(*[m.shape[0] for m in mats])
+        cols = (ctypes.c_int64 * len(mats))(*[m.shape[1] for m in mats])
+        v = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1))
+        return mats, flat, rows, cols, v
+
+    def pipeline(self, matrices, v, tile, s, depth=8):
+        """The reference's pipeline (linalg.hpp:213-260): (shape, tiles, cost)."""
+        mats, flat, rows, cols, v = self._chain_args(matrices, v)
+        cap = 4 * (max(max(m.shape) for m in mats) + v.size) + 8
+        out = np.empty((cap, s), dtype=np.float64)
+        so = CShape()
+        c = CCost()
+        self._rc(self.lib.ref_pipeline(_dp(flat), rows, cols, len(mats), _dp(v),
+                                       ctypes.c_int64(v.size), ctypes.c_int64(tile[0]),
+                                       ctypes.c_int64(tile[1]), ctypes.c_int64(s),
+                                       ctypes.c_int64(depth), ctypes.byref(so), _dp(out),
+                                       ctypes.byref(c)))
+        res = TileTensorShape.from_c(so)
+        return res, out[:res.tile_count()].copy(), _cost(c)
+
+    def score_tile_factorizations(self, matrices, v, s, depth=8):
+        """[(t1, rotations, total_ops)] in the reference's order (linalg.hpp:279-294)."""
+        mats, flat, rows, cols, v = self._chain_args(matrices, v)
+        cap = 256
+        trip = (ctypes.c_int64 * (3 * cap))()
+        n = ctypes.c_int()
+        self._rc(self.lib.ref_score_tile_factorizations(
+            _dp(flat), rows, cols, len(mats), _dp(v), ctypes.c_int64(v.size), ctypes.c_int64(s),
+            ctypes.c_int64(depth), trip, cap, ctypes.byref(n)))
+        return [(trip[3 * i], trip[3 * i + 1], trip[3 * i + 2]) for i in range(min(n.value, cap))]
+
     def linalg(self, which, sa, ta, sb, tb, s):
         ta = np.ascontiguousarray(ta, dtype=np.float64)
         tb = np.ascontiguousarray(tb, dtype=np.float64)
