@@ -196,6 +196,22 @@ int tt_sum_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents
 int tt_replicate_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents, int rank,
                           int dim, double* out, int64_t n_tiles);     /* rotate_sum.hpp:128-152 */
 
+/* ---- neural-network layers (nn.hpp) ------------------------------------ */
+/* Batch-packed affine layer of cryptonets_infer (nn.hpp:282-326 replaces the
+ * per-scalar Session::add / Session::mul loop of infer_batch_packed): every
+ * network scalar is one tile, and output tile o is the left fold
+ *   acc = bias[o];  acc = acc + w[k] * in[src[k]]  for k in [row_ptr[o], row_ptr[o+1])
+ * with separately rounded multiply and add, exactly as
+ * session.add(acc, session.mul(constant_tile(w[k]), v[src[k]])).  Counters
+ * grow by one multiplication and one addition per tap.  row_ptr (n_out + 1
+ * entries), src, w and bias are HOST arrays (plaintext weights); in / out are
+ * device tiles.  chain_in is the input's chain index; *chain_out gets the
+ * result's (chain_in - 1 when any tap exists, else the session depth).
+ * TT_ERR_DEPTH when a tap would multiply at chain index 0. */
+int tt_batch_affine(tt_session* s, const double* in, int64_t n_in, int64_t n_out,
+                    const int64_t* row_ptr, const int64_t* src, const double* w,
+                    const double* bias, double* out, int64_t chain_in, int64_t* chain_out);
+
 /* ---- diagnostics ------------------------------------------------------- */
 /* Force the reduction kernel path (tests / A-B measurement): 0 = best
  * eligible (default), 1 = TMA-ring fused kernel (whole-tile tree),

@@ -17,10 +17,12 @@
 #include <memory>
 #include <optional>
 #include <span>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "tiletensor/linalg.hpp"
+#include "tiletensor/nn.hpp"
 #include "tiletensor/rotate_sum.hpp"
 #include "tiletensor/tile_tensor.hpp"
 #include "../include/tiletensor_b200.h"
@@ -295,6 +297,61 @@ int ref_score_tile_factorizations(const double* mats, const int64_t* rows, const
       triples[3 * i + 1] = static_cast<int64_t>(choices[i].cost.rotations);
       triples[3 * i + 2] = static_cast<int64_t>(choices[i].cost.total_ops());
     }
+  });
+}
+
+// nn.hpp: the network from a spec text + seed (parse_network), run through
+// nn_forward (which = 0) or cryptonets_infer with tile t (which = 1) on a
+// batch [features, n] (row-major); logits [out, n] into `out` (cap values).
+int ref_nn_run(int which, const char* spec, uint64_t seed, const double* batch, int64_t features,
+               int64_t n, const int64_t* tile, int64_t slots, int64_t depth, double* out,
+               int64_t cap, int64_t* out_rows, tt_cost* c) {
+  return guard([&] {
+    std::istringstream in(spec);
+    const NetworkSpec net = parse_network(in, "", seed);
+    const DenseTensor b({features, n}, std::vector<double>(batch, batch + features * n));
+    DenseTensor logits = DenseTensor::zeros({1});
+    if (which == 0) {
+      logits = nn_forward(net, b);
+    } else {
+      Session session(slots, depth);
+      auto res = cryptonets_infer(net, b, {tile[0], tile[1], tile[2]}, session);
+      logits = std::move(res.logits);
+      c->additions = res.cost.additions;
+      c->multiplications = res.cost.multiplications;
+      c->mask_multiplications = res.cost.mask_multiplications;
+      c->rotations = res.cost.rotations;
+      c->bootstraps = res.cost.bootstraps;
+      c->power_of_two_rotations = res.cost.power_of_two_rotations;
+    }
+    if (static_cast<int64_t>(logits.size()) > cap) throw std::invalid_argument("output buffer too small");
+    *out_rows = logits.extent(0);
+    std::memcpy(out, logits.values().data(), logits.size() * sizeof(double));
+  });
+}
+
+// parse_network's seeded parameters, flattened in layer order (weights then bias)
+int ref_nn_params(const char* spec, uint64_t seed, double* out, int64_t cap, int64_t* count) {
+  return guard([&] {
+    std::istringstream in(spec);
+    const NetworkSpec net = parse_network(in, "", seed);
+    int64_t k = 0;
+    auto put = [&](const DenseTensor& t) {
+      for (double v : t.values()) {
+        if (k < cap) out[k] = v;
+        ++k;
+      }
+    };
+    for (const auto& layer : net.layers) {
+      if (const auto* cv = std::get_if<ConvLayer>(&layer)) {
+        put(cv->weights);
+        put(cv->bias);
+      } else if (const auto* f = std::get_if<FcLayer>(&layer)) {
+        put(f->weights);
+        put(f->bias);
+      }
+    }
+    *count = k;
   });
 }
 

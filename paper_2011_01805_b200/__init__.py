@@ -6,5 +6,6 @@ runs in hand-written sm_100a kernels behind the C-ABI in
 """
 from .tiletensor import *  # noqa: F401,F403
 from .tiletensor import __all__ as _tt_all
+from . import nn  # noqa: F401  (inc/nn.hpp mirror)
 
 __all__ = list(_tt_all)

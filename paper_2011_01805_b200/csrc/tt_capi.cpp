@@ -714,6 +714,50 @@ int tt_tiles_binary(tt_session* s, int op, const double* a, const double* b, dou
   });
 }
 
+int tt_batch_affine(tt_session* s, const double* in, int64_t n_in, int64_t n_out,
+                    const int64_t* row_ptr, const int64_t* src, const double* w,
+                    const double* bias, double* out, int64_t chain_in, int64_t* chain_out) {
+  return guarded([&] {
+    need_session(s);
+    if (n_in < 0 || n_out < 0) invalid_argument("negative tile count");
+    if (n_out > 0 && (!row_ptr || !bias)) invalid_argument("null layer arrays");
+    if (n_out > 0 && row_ptr[0] != 0) invalid_argument("row_ptr must start at 0");
+    for (int64_t o = 0; o < n_out; ++o)
+      if (row_ptr[o + 1] < row_ptr[o]) invalid_argument("row_ptr must be non-decreasing");
+    const int64_t nnz = n_out > 0 ? row_ptr[n_out] : 0;
+    if (nnz > 0 && (!src || !w)) invalid_argument("null tap arrays");
+    for (int64_t k = 0; k < nnz; ++k)
+      if (src[k] < 0 || src[k] >= n_in) invalid_argument("tap source tile out of range");
+    if (n_in > 0 && n_out > 0 && in && out && out < in + n_in * s->slots && in < out + n_out * s->slots)
+      invalid_argument("batch affine output must not overlap its input");
+    if (nnz > 0 && chain_in < 1)
+      depth_error("multiplication at chain index 0 (bootstrap required)");
+    if (chain_out) *chain_out = nnz > 0 ? chain_in - 1 : s->depth;
+    s->muls += static_cast<uint64_t>(nnz);
+    s->adds += static_cast<uint64_t>(nnz);
+    if (n_out == 0) return;
+    std::lock_guard<std::mutex> lk(s->mu);
+    const LaunchCtx c = ctx_of(s);
+    // stage the plaintext layer description in session scratch (stream-ordered)
+    const size_t b_rp = static_cast<size_t>(n_out + 1) * sizeof(int64_t);
+    const size_t b_src = static_cast<size_t>(nnz) * sizeof(int64_t);
+    const size_t b_w = static_cast<size_t>(nnz) * sizeof(double);
+    const size_t b_bias = static_cast<size_t>(n_out) * sizeof(double);
+    auto* base = reinterpret_cast<unsigned char*>(scratch_fn(s, b_rp + b_src + b_w + b_bias));
+    auto* d_rp = reinterpret_cast<int64_t*>(base);
+    auto* d_src = reinterpret_cast<int64_t*>(base + b_rp);
+    auto* d_w = reinterpret_cast<double*>(base + b_rp + b_src);
+    auto* d_bias = reinterpret_cast<double*>(base + b_rp + b_src + b_w);
+    check_cuda(cudaMemcpyAsync(d_rp, row_ptr, b_rp, cudaMemcpyHostToDevice, c.stream), "layer upload");
+    if (nnz > 0) {
+      check_cuda(cudaMemcpyAsync(d_src, src, b_src, cudaMemcpyHostToDevice, c.stream), "layer upload");
+      check_cuda(cudaMemcpyAsync(d_w, w, b_w, cudaMemcpyHostToDevice, c.stream), "layer upload");
+    }
+    check_cuda(cudaMemcpyAsync(d_bias, bias, b_bias, cudaMemcpyHostToDevice, c.stream), "layer upload");
+    launch_batch_affine(c, in, s->slots, n_out, d_rp, d_src, d_w, d_bias, out);
+  });
+}
+
 int tt_tiles_mask_mul(tt_session* s, const double* a, const double* mask, double* out,
                       int64_t n_tiles, const int64_t* chain_a, int64_t* chain_out) {
   return guarded([&] {

@@ -1914,6 +1914,28 @@ __global__ void __launch_bounds__(kTreeThreads, 2) smem_tree_kernel(double* __re
   }
 }
 
+// ---- batch-packed affine layer (nn.hpp:282-326) ----------------------------------------
+// One thread per (output tile o, slot j); consecutive threads take
+// consecutive slots of one output, so every tap's tile read is coalesced and
+// its weight / source index is a warp-uniform broadcast load.
+__global__ void __launch_bounds__(256) batch_affine_kernel(const double* __restrict__ in, int64_t s,
+                                                           uint64_t total,
+                                                           const int64_t* __restrict__ row_ptr,
+                                                           const int64_t* __restrict__ src,
+                                                           const double* __restrict__ w,
+                                                           const double* __restrict__ bias,
+                                                           double* __restrict__ out, FastDiv64 sdiv) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t o = fdiv(i, sdiv);
+    const int64_t j = static_cast<int64_t>(i - o * sdiv.d);
+    double acc = bias[o];
+    const int64_t k1 = row_ptr[o + 1];
+    for (int64_t k = row_ptr[o]; k < k1; ++k) acc = dadd(acc, dmul(w[k], __ldg(in + src[k] * s + j)));
+    out[i] = acc;
+  }
+}
+
 // ---- synthetic input generator (== or_fill_uniform in oracle/tt_oracle.c) ------------
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -2036,6 +2058,17 @@ void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shap
   }
 #undef TT_EW
   post_launch(c, "elementwise kernel");
+}
+
+void launch_batch_affine(const LaunchCtx& c, const double* in, int64_t s, int64_t n_out,
+                         const int64_t* row_ptr, const int64_t* src, const double* w,
+                         const double* bias, double* out) {
+  const uint64_t total = static_cast<uint64_t>(s) * n_out;
+  if (total == 0) return;
+  const int grid = grid_for(c, (const void*)batch_affine_kernel, 256, 0, (total + 255) / 256);
+  batch_affine_kernel<<<grid, 256, 0, c.stream>>>(in, s, total, row_ptr, src, w, bias, out,
+                                                   make_div64(static_cast<uint64_t>(s)));
+  post_launch(c, "batch affine kernel");
 }
 
 void launch_binary_flat(const LaunchCtx& c, int op, const double* a, const double* b, double* out,

@@ -69,6 +69,11 @@ void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shap
                         const Shape& b, int64_t s, const double* ta, const double* tb,
                         double* tout);
 // out[i] = a[i] (op) b[i] over `count` slots; op 2 = a * mask (same as mul)
+// out[o] = bias[o] (+) w[k] (*) in[src[k]] over k in [row_ptr[o], row_ptr[o+1]),
+// left fold per slot; the CSR arrays are device pointers.
+void launch_batch_affine(const LaunchCtx& c, const double* in, int64_t s, int64_t n_out,
+                         const int64_t* row_ptr, const int64_t* src, const double* w,
+                         const double* bias, double* out);
 void launch_binary_flat(const LaunchCtx& c, int op, const double* a, const double* b, double* out,
                         int64_t count);
 // out[t][j] = in[t][(j + r) mod s]   (backend.hpp:157-159), r in [1, s)

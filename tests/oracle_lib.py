@@ -286,6 +286,31 @@ class Ref(_Base):
         res = TileTensorShape.from_c(so)
         return res, out[:res.tile_count()].copy(), _cost(c)
 
+    def nn_run(self, which, spec, seed, batch, tile=(1, 1, 1), slots=1, depth=8):
+        """nn_forward (which=0) / cryptonets_infer (which=1) of the reference on
+        parse_network(spec, seed): (logits [out, n], cost)."""
+        batch = np.ascontiguousarray(batch, dtype=np.float64)
+        cap = 1 << 20
+        out = np.empty(cap, dtype=np.float64)
+        rows = ctypes.c_int64()
+        c = CCost()
+        t = (ctypes.c_int64 * 3)(*tile)
+        self._rc(self.lib.ref_nn_run(int(which), spec.encode(), ctypes.c_uint64(seed), _dp(batch),
+                                     ctypes.c_int64(batch.shape[0]), ctypes.c_int64(batch.shape[1]),
+                                     t, ctypes.c_int64(slots), ctypes.c_int64(depth), _dp(out),
+                                     ctypes.c_int64(cap), ctypes.byref(rows), ctypes.byref(c)))
+        r = rows.value
+        return out[:r * batch.shape[1]].reshape(r, batch.shape[1]).copy(), _cost(c)
+
+    def nn_params(self, spec, seed):
+        """parse_network's seeded weights and biases, flattened in layer order."""
+        cap = 1 << 20
+        out = np.empty(cap, dtype=np.float64)
+        n = ctypes.c_int64()
+        self._rc(self.lib.ref_nn_params(spec.encode(), ctypes.c_uint64(seed), _dp(out),
+                                        ctypes.c_int64(cap), ctypes.byref(n)))
+        return out[:n.value].copy()
+
     @staticmethod
     def _chain_args(matrices, v):
         mats = [np.ascontiguousarray(m, dtype=np.float64) for m in matrices]
