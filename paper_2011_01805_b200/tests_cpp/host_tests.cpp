@@ -8,11 +8,13 @@
 #include <cstdio>
 #include <functional>
 #include <random>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
 
 #include "tiletensor_b200/linalg.hpp"
+#include "tiletensor_b200/nn.hpp"
 
 using namespace tiletensor;
 
@@ -534,10 +536,68 @@ static void pipeline_suite() {
   }
 }
 
+// inference kit (inc/nn.hpp; behaviour pinned by tests/test_nn.cpp:162-270)
+static void nn_suite() {
+  std::mt19937_64 rng(3131);
+  std::istringstream spec(
+      "input h=6 w=6\nconv filters=2 kh=3 kw=3 stride=2 pad=1\nact square\n"
+      "fc in=18 out=4\nact square\nfc in=4 out=3\n");
+  const NetworkSpec net = parse_network(spec, "", 44);
+  CHECK(net.layers.size() == 5 && net.input_size() == 36);
+  const std::int64_t s = 64;
+  long runs = 0;
+  for (std::int64_t t3 = 1; t3 <= s; t3 *= 2)
+    for (std::int64_t t1 = 1; t1 * t3 <= s; t1 *= 2) {
+      const DenseTensor batch = random_tensor({36, t3}, rng, -1, 1);
+      Session session(s, 8);
+      const auto res = cryptonets_infer(net, batch, {t1, s / (t1 * t3), t3}, session);
+      CHECK(max_rel_diff(res.logits, nn_forward(net, batch)) < 1e-6);
+      if (t1 == 1 && s / (t1 * t3) == 1) CHECK(res.cost.rotations == 0);
+      ++runs;
+    }
+  CHECK(runs == 28);
+  {  // paper-scale counts for tile [32, 256, 1]
+    const NetworkSpec cn = cryptonets_network(42);
+    const DenseTensor batch = random_tensor({784, 1}, rng, -1, 1);
+    Session session(8192, 8);
+    const auto res = cryptonets_infer(cn, batch, {32, 256, 1}, session);
+    CHECK(res.cost.multiplications == 32 && res.cost.rotations == 89 && res.cost.additions == 113);
+    CHECK(max_rel_diff(res.logits, nn_forward(cn, batch)) < 1e-6);
+  }
+  {  // depth exhaustion names the layer, both branches
+    Session shallow(64, 2);
+    for (const auto& tile : {std::array<std::int64_t, 3>{2, 32, 1}, std::array<std::int64_t, 3>{1, 1, 64}}) {
+      bool named = false;
+      try {
+        (void)cryptonets_infer(net, random_tensor({36, 1}, rng, -1, 1), tile, shallow);
+      } catch (const DepthExhaustedError& e) {
+        named = std::string(e.what()).find("layer") != std::string::npos;
+      }
+      CHECK(named);
+    }
+    Session session(64, 8);
+    CHECK_THROWS_AS(cryptonets_infer(net, random_tensor({36, 9}, rng, -1, 1), {2, 4, 8}, session),
+                    ShapeError);
+  }
+  {  // im2col, text tensors, bootstrap bound
+    const DenseTensor x = random_tensor({4, 4}, rng, -1, 1);
+    const DenseTensor m1 = im2col(x, 2, 2, 2, 0);
+    CHECK(m1.shape() == (std::vector<std::int64_t>{4, 4}) && m1(3, 0) == x(2, 2));
+    CHECK(im2col(DenseTensor::zeros({28, 28}), 5, 5, 2, 1).extent(0) == 169);
+    CHECK_THROWS_AS(im2col(x, 6, 6, 1, 0), ShapeError);
+    std::stringstream io;
+    write_tensor(io, x);
+    CHECK(read_tensor(io) == x);
+    const std::vector<FilterGroup> groups{{32, 3, 50, 18}, {32, 5, 50, 16}};
+    CHECK(bootstrap_lower_bound(groups, 3) == 1088 && bootstrap_lower_bound(groups, 1) == 3264);
+    CHECK_THROWS_AS(bootstrap_lower_bound(groups, 0), std::invalid_argument);
+  }
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> suites = {
       {"shapes", shapes}, {"backend", backend}, {"rotate_sum", rotate_sum},
-      {"tile_tensor", tile_tensor}, {"linalg", linalg}, {"pipeline", pipeline_suite}};
+      {"tile_tensor", tile_tensor}, {"linalg", linalg}, {"pipeline", pipeline_suite}, {"nn", nn_suite}};
   for (const auto& [name, fn] : suites) {
     const int before = g_failed;
     try {
