@@ -6,6 +6,7 @@
 // Needs a GPU; run by tests/test_cpp_host.py.  Exit code = failed checks.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <functional>
 #include <random>
 #include <sstream>
@@ -14,6 +15,7 @@
 #include <vector>
 
 #include "tiletensor_b200/linalg.hpp"
+#include "tiletensor_b200/formats.hpp"
 #include "tiletensor_b200/nn.hpp"
 
 using namespace tiletensor;
@@ -594,10 +596,35 @@ static void nn_suite() {
   }
 }
 
+// packed tile file (tools/tiletensor_main.cpp:76-128): text and bit-exact round trip
+static void formats_suite() {
+  Session session(4, 8);
+  const TileTensor t = pack(DenseTensor({3}, {1, 2, 3}), parse_shape("[3/2,*/2]"), session);
+  std::stringstream io;
+  write_tiles(io, t);
+  CHECK(io.str() == "shape: [3/2,*/2]\nslots: 4\ntile: 1 1 2 2\ntile: 3 3 0 0\n");
+  const TileTensor back = read_tiles(io, session);
+  CHECK(back.shape() == t.shape() && back.tiles()[1].slots()[1] == 3.0);
+  std::mt19937_64 rng(4242);
+  Session s16(16, 8);
+  const TileTensor r = tt_sum(pack(random_tensor({5, 7}, rng), parse_shape("[5/4,7/4]"), s16), 2);
+  std::stringstream io2;
+  write_tiles(io2, r);
+  const TileTensor r2 = read_tiles(io2, s16);
+  CHECK(r2.shape() == r.shape());
+  bool same = true;
+  for (std::size_t i = 0; i < r.tile_count(); ++i)
+    for (std::size_t h = 0; h < 16; ++h)
+      same = same && std::memcmp(&r.tiles()[i].slots()[h], &r2.tiles()[i].slots()[h], 8) == 0;
+  CHECK(same);
+  std::istringstream bad("shape: [2/2,*/2]\nslots: 8\n");
+  CHECK_THROWS_AS(read_tiles(bad, session), std::runtime_error);
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> suites = {
       {"shapes", shapes}, {"backend", backend}, {"rotate_sum", rotate_sum},
-      {"tile_tensor", tile_tensor}, {"linalg", linalg}, {"pipeline", pipeline_suite}, {"nn", nn_suite}};
+      {"tile_tensor", tile_tensor}, {"linalg", linalg}, {"pipeline", pipeline_suite}, {"nn", nn_suite}, {"formats", formats_suite}};
   for (const auto& [name, fn] : suites) {
     const int before = g_failed;
     try {
