@@ -594,6 +594,21 @@ static void nn_suite() {
     CHECK(bootstrap_lower_bound(groups, 3) == 1088 && bootstrap_lower_bound(groups, 1) == 3264);
     CHECK_THROWS_AS(bootstrap_lower_bound(groups, 0), std::invalid_argument);
   }
+  {  // plan checker (tests/test_nn.cpp:304-385 behaviour)
+    std::vector<PlanStep> steps;
+    for (int i = 0; i < 4; ++i)
+      steps.push_back(PlanStep{"mul" + std::to_string(i + 1), "mul", {"[4/4]", "[4/4]"}, "[4/4]", 3 - i, 2 - i});
+    const auto rep = validate_plan(steps, BackendConfig{4, 3});
+    CHECK(!rep.ok && rep.issues.size() == 1 && rep.issues[0].step == 4 && !rep.issues[0].info);
+    const std::vector<PlanStep> bridge{PlanStep{"conv", "mul", {"[18,*/32,150/256,255]", "[1,32/32,150/256]"},
+                                                "[18,32/32,150/256,255]", 4, 3}};
+    const auto rb = validate_plan(bridge, BackendConfig{8192, 4});
+    CHECK(rb.ok && rb.issues.size() == 1 && rb.issues[0].info);
+    std::istringstream bad("step s1 op=add in=[4/4] out=[4/4] chain=11\n");
+    CHECK_THROWS_AS(parse_plan(bad), std::runtime_error);
+    std::istringstream fine("# c\nstep s1 op=add in=[4/4] in=[4/4] out=[4/4] chain=1:1\n");
+    CHECK(parse_plan(fine).size() == 1);
+  }
 }
 
 // packed tile file (tools/tiletensor_main.cpp:76-128): text and bit-exact round trip
