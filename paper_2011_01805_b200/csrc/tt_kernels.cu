@@ -1558,13 +1558,13 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, i
 
 // SL = slots per unit: 32 (one slot per lane) or 16 (the two half-warps take
 // different 8-column halves of the block: twice the units, for wave balance)
-template <int BC, int SL, int SC>
+template <int BC, int SL, int SC, int PB = kGemmBlk>
 __host__ __device__ constexpr int tg_warps() {
-  return (kGemmBlk / 8) * (BC / SC) * SL / 32;
+  return (PB / 8) * (BC / SC) * SL / 32;
 }
-template <int BC, int SL, int kTgSteps, int kTgStages>
+template <int BC, int SL, int kTgSteps, int kTgStages, int PB = kGemmBlk>
 __host__ __device__ constexpr size_t tg_smem_bytes() {
-  return static_cast<size_t>(kTgStages) * kTgSteps * (kGemmBlk + BC) * SL * sizeof(double) +
+  return static_cast<size_t>(kTgStages) * kTgSteps * (PB + BC) * SL * sizeof(double) +
          3 * kTgStages * sizeof(uint64_t);
 }
 
@@ -1592,16 +1592,16 @@ __device__ __forceinline__ TgUnit tg_decode(const BlockSpec& bs, uint64_t u, int
   return t;
 }
 
-template <int BC, int SL, int kTgSteps, int kTgStages, int SC>
+template <int BC, int SL, int kTgSteps, int kTgStages, int SC, int PB = kGemmBlk>
 __global__ void __maxnreg__(SC == 8 ? 232 : 128)
     fold_gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
                          const __grid_constant__ CUtensorMap mapB,
                          const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
                          const __grid_constant__ TgSpec ts, double* __restrict__ OUT,
                          unsigned int* __restrict__ sched) {
-  constexpr int kW = tg_warps<BC, SL, SC>();
+  constexpr int kW = tg_warps<BC, SL, SC, PB>();
   constexpr int kTgRows = 8 / SC;  // rows of products batched before their adds
-  constexpr int kA = kTgSteps * kGemmBlk * SL;  // doubles per stage
+  constexpr int kA = kTgSteps * PB * SL;  // doubles per stage
   constexpr int kB = kTgSteps * BC * SL;
   constexpr int kStage = kA + kB;
   extern __shared__ __align__(1024) double tsm[];
@@ -1660,7 +1660,7 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
     mbar_arrive_expect_tx(&full[lstage], kStage * sizeof(double));
     double* st = tsm + lstage * kStage;
     const int j0 = static_cast<int>(lt.chunk * SL);
-    tma_load_5d(st, &mapA, j0, static_cast<int>(lt.pb * kGemmBlk), lk * kTgSteps,
+    tma_load_5d(st, &mapA, j0, static_cast<int>(lt.pb * PB), lk * kTgSteps,
                 ts.a_act[0] ? rc[0] : 0, ts.a_act[1] ? rc[1] : 0, &full[lstage]);
     tma_load_5d(st + kA, &mapB, j0, static_cast<int>(lt.qb * BC), lk * kTgSteps,
                 ts.b_act[0] ? rc[0] : 0, ts.b_act[1] ? rc[1] : 0, &full[lstage]);
@@ -1726,9 +1726,9 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
       const int nsteps = cnt - k * kTgSteps;
       if (nsteps >= kTgSteps) {
 #pragma unroll
-        for (int h = 0; h < kTgSteps; ++h) fold_step(sA + h * kGemmBlk * SL, sB + h * BC * SL);
+        for (int h = 0; h < kTgSteps; ++h) fold_step(sA + h * PB * SL, sB + h * BC * SL);
       } else {
-        for (int h = 0; h < nsteps; ++h) fold_step(sA + h * kGemmBlk * SL, sB + h * BC * SL);
+        for (int h = 0; h < nsteps; ++h) fold_step(sA + h * PB * SL, sB + h * BC * SL);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
@@ -1738,9 +1738,9 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
       }
     }
     const GroupBase gb = group_base(p, t.rest);
-    const int np = static_cast<int>(bs.ext_ia - t.pb * kGemmBlk < kGemmBlk ? bs.ext_ia - t.pb * kGemmBlk : kGemmBlk);
+    const int np = static_cast<int>(bs.ext_ia - t.pb * PB < PB ? bs.ext_ia - t.pb * PB : PB);
     const int nq = static_cast<int>(bs.ext_ib - t.qb * BC < BC ? bs.ext_ib - t.qb * BC : BC);
-    double* orow = OUT + (gb.out + (t.pb * kGemmBlk + r0) * bs.out_ia + (t.qb * BC + c0) * bs.out_ib) * s +
+    double* orow = OUT + (gb.out + (t.pb * PB + r0) * bs.out_ia + (t.qb * BC + c0) * bs.out_ib) * s +
                    t.chunk * SL + slot;
     const int64_t rstep = bs.out_ia * s, cstep = bs.out_ib * s;
     // the fold output is re-read at once by the tree pass: keep it in L2
@@ -1812,11 +1812,10 @@ __device__ __forceinline__ void row_shift(double (&v)[NR], int D) {
 
 // Reads the folded tiles from `in` (scratch) and writes `out`: warps read
 // halo rows owned by other warps, so the pass cannot run in place.
-template <int HR>
+template <int HR, int R = 16>
 __global__ void __launch_bounds__(256) row_tree_kernel(const double* __restrict__ in,
                                                        double* __restrict__ out, int64_t n_tiles,
                                                        int64_t s, int nlevels, int4 lv0, int4 lv1) {
-  constexpr int R = 16;
   constexpr int NR = R + HR;
   const int lane = threadIdx.x & 31;
   const int rows = static_cast<int>(s / 32);
@@ -2199,7 +2198,7 @@ const int g_gemm_order = [] {
   return e ? std::atoi(e) : 0;
 }();
 
-template <int SL, int kTgSteps, int kTgStages, int SC>
+template <int SL, int kTgSteps, int kTgStages, int SC, int PB = kGemmBlk>
 bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupParams& pr,
                         BlockSpec bs, const double* ta, const double* tb, double* tout) {
   const GroupSpec& g = p.g;
@@ -2238,19 +2237,21 @@ bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupPar
     }
   }
   if (bs.a_ia <= 0 || bs.b_ib <= 0 || g.astep < 0 || g.bstep < 0) return false;
-  const uint32_t boxA[5] = {static_cast<uint32_t>(SL), kGemmBlk, kTgSteps, 1, 1};
+  const uint32_t boxA[5] = {static_cast<uint32_t>(SL), PB, kTgSteps, 1, 1};
   const uint32_t boxB[5] = {static_cast<uint32_t>(SL), BC, kTgSteps, 1, 1};
   if (!encode_tensor_map_f64(mapA, 5, ta + first * g.astep * s, dA, sA, boxA) ||
       !encode_tensor_map_f64(mapB, 5, tb + first * g.bstep * s, dB, sB, boxB))
     return false;
   bs.nbq = (bs.ext_ib + BC - 1) / BC;
+  bs.nbp = (bs.ext_ia + PB - 1) / PB;
+  bs.div_nbp = make_div64(static_cast<uint64_t>(bs.nbp));
   bs.chunks = s / SL;
   bs.units = pr.g.groups * bs.chunks * bs.nbp * bs.nbq;
   bs.div_nbq = make_div64(static_cast<uint64_t>(bs.nbq));
   bs.div_chunks = make_div64(static_cast<uint64_t>(bs.chunks));
-  auto k = fold_gemm_tma_kernel<BC, SL, kTgSteps, kTgStages, SC>;
-  constexpr size_t smem = tg_smem_bytes<BC, SL, kTgSteps, kTgStages>();
-  constexpr int threads = tg_warps<BC, SL, SC>() * 32;
+  auto k = fold_gemm_tma_kernel<BC, SL, kTgSteps, kTgStages, SC, PB>;
+  constexpr size_t smem = tg_smem_bytes<BC, SL, kTgSteps, kTgStages, PB>();
+  constexpr int threads = tg_warps<BC, SL, SC, PB>() * 32;
   set_smem_attr((const void*)k, smem);
   const int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
   unsigned int* sched = g_gemm_dynamic ? take_sched_slot(c) : nullptr;
@@ -2273,6 +2274,9 @@ bool launch_gemm_tma(const LaunchCtx& c, const GroupParams& p, const GroupParams
     case 1: return launch_gemm_tma_sl<16, 2, 6, 4>(c, p, pr, bs, ta, tb, tout);
     case 2: return launch_gemm_tma_sl<16, 4, 4, 4>(c, p, pr, bs, ta, tb, tout);
     case 3: return launch_gemm_tma_sl<32, 2, 6, 4>(c, p, pr, bs, ta, tb, tout);
+    case 4: return launch_gemm_tma_sl<8, 4, 3, 4, 32>(c, p, pr, bs, ta, tb, tout);
+    case 5: return launch_gemm_tma_sl<16, 4, 3, 4, 32>(c, p, pr, bs, ta, tb, tout);
+    case 6: return launch_gemm_tma_sl<8, 4, 4, 4, 32>(c, p, pr, bs, ta, tb, tout);
     default: return launch_gemm_tma_sl<16, 4, 3, 4>(c, p, pr, bs, ta, tb, tout);
   }
 }
@@ -2466,6 +2470,12 @@ const int g_tree_smem = [] {
   return e ? std::atoi(e) : 0;
 }();
 
+// rows per warp of the wide-halo row tree (TT_ROW_ROWS = 16 / 32 / 64)
+const int g_row_rows = [] {
+  const char* e = std::getenv("TT_ROW_ROWS");
+  return e ? std::atoi(e) : 16;
+}();
+
 struct TreePass {
   int kind = 0;
   int hr = 0;
@@ -2559,6 +2569,14 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
   } else if (tp.hr <= 8) {
     const int grid = grid_for(c, (const void*)row_tree_kernel<8>, 256, 0, work);
     row_tree_kernel<8><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
+  } else if (g_row_rows == 32 && s % (32 * 32) == 0) {  // 32 rows per warp: 1.5x halo reads, not 2x
+    const int64_t work32 = (n_tiles * (s / 32 / 32) + 7) / 8;
+    const int grid = grid_for(c, (const void*)row_tree_kernel<16, 32>, 256, 0, work32);
+    row_tree_kernel<16, 32><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
+  } else if (g_row_rows == 64 && s % (32 * 64) == 0) {
+    const int64_t work64 = (n_tiles * (s / 32 / 64) + 7) / 8;
+    const int grid = grid_for(c, (const void*)row_tree_kernel<16, 64>, 256, 0, work64);
+    row_tree_kernel<16, 64><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
   } else {
     const int grid = grid_for(c, (const void*)row_tree_kernel<16>, 256, 0, work);
     row_tree_kernel<16><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);

@@ -54,6 +54,9 @@ VARIANTS = [
     {"TT_GEMM_CFG": "1"},
     {"TT_GEMM_CFG": "2"},
     {"TT_GEMM_CFG": "3"},
+    {"TT_GEMM_CFG": "4"},
+    {"TT_GEMM_CFG": "5"},
+    {"TT_GEMM_CFG": "6"},
     {"TT_TREE_SMEM": "1"},
 ]
 
