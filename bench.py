@@ -369,6 +369,7 @@ def run_ours(args):
                        "alg_bytes": pb}
         del t
         ops.update(bench_matmul(tt, configs, S, stream, hbm_peak, max(3, args.steps)))
+        ops.update(bench_small_configs(tt, configs, stream, hbm_peak, max(20, args.steps)))
 
     # end to end from pinned host memory through the public API
     e2e = None
@@ -434,6 +435,41 @@ def run_ours(args):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_small_configs(tt, configs, stream, hbm_peak, reps):
+    """Configs 1, 2 and 4 (device-resident operands): per-call latency of the
+    op chain through the public API (CUDA events, averaged over `reps`).
+    These are parity configs and latency-bound; reported beside
+    the bench line, not as it."""
+    import torch
+    out = {}
+    c1 = configs.config1()
+    S1 = tt.Session(512, 8, device=torch.cuda.current_device())
+    sA = tt.parse_shape(c1.shapes["A"])
+    A, B = tt.pack(c1.tensors["A"], sA, S1), tt.pack(c1.tensors["B"], sA, S1)
+    t = time_events(lambda: tt.tt_mul_sum(A, B, 2), reps, stream)
+    out["c1_mul_sum"] = {"us": t * 1e6, "note": "[100/16,200/32] x same, sum dim 2 (49 tiles of 512)"}
+    c2 = configs.config2()
+    S2 = tt.Session(8192, 8, device=torch.cuda.current_device())
+    M = tt.pack(c2.tensors["M"], tt.parse_shape(c2.shapes["M"]), S2)
+    V = tt.pack(c2.tensors["V"], tt.parse_shape(c2.shapes["V"]), S2)
+    t = time_events(lambda: tt.matvec_a(M, V), reps, stream)
+    alg = (512 + 32 + 16) * 8192 * 8
+    out["c2_matvec"] = {"us": t * 1e6, "GB/s": alg / t / 1e9, "frac": alg / t / 1e9 / hbm_peak,
+                        "note": "M[1024/64,4096/128] x V[*/64,4096/128], sum dim 2 (35 MiB, L2-scale)"}
+    c4 = configs.config4(True)
+    S4 = tt.Session(8192, 8, device=torch.cuda.current_device())
+    T = {k: tt.pack(c4.tensors[k], tt.parse_shape(v), S4) for k, v in c4.shapes.items()}
+
+    def c4_chain():
+        h = tt.tt_add(tt.tt_mul_sum(T["W1t"], T["X"], 1), T["b1"])
+        h = tt.tt_mul(h, h)
+        return tt.tt_add(tt.tt_mul_sum(T["W2"], h, 2), T["b2"])
+    t = time_events(c4_chain, reps, stream)
+    out["c4_fc_square_fc"] = {"us": t * 1e6, "samples_per_s": 4096 / t,
+                              "note": "784->100->square->10 on 4096 samples, batch interleaved (~) in tile dim 3"}
+    return out
 
 
 FP64_PEAK_OPS = 18.34e12  # B200, 148 SMs x 64 FP64 lanes at boost (profiles/r01_fp64_peak.txt)

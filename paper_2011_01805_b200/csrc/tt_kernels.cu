@@ -478,7 +478,31 @@ struct GroupBase {
   int64_t out, a, b;
 };
 
-__device__ __forceinline__ GroupBase group_base(const GroupParams& p, uint64_t v) {
+// Compact parameters of the fold-only kernels (phase 1, GEMM folds): the
+// group grid and the one FOLD instruction.  ~0.5 KB instead of GroupParams'
+// ~3.3 KB program -- kernel-parameter size is paid on every launch, and small
+// ops are launch bound.
+struct FoldParams {
+  GroupSpec g;
+  FastDiv64 gdiv[R];
+  int64_t s;
+  int64_t first, count;  // FOLD over operand steps [first, first + count)
+  int nlevels;           // column-tree fusion: power-of-two levels
+};
+
+FoldParams to_fold(const GroupParams& p) {
+  FoldParams f;
+  f.g = p.g;
+  for (int i = 0; i < R; ++i) f.gdiv[i] = p.gdiv[i];
+  f.s = p.s;
+  f.first = p.ops[0].x;
+  f.count = p.ops[0].y;
+  f.nlevels = p.nlevels;
+  return f;
+}
+
+template <class PP>
+__device__ __forceinline__ GroupBase group_base(const PP& p, uint64_t v) {
   GroupBase gb{0, 0, 0};
 #pragma unroll
   for (int i = R - 1; i >= 0; --i) {
@@ -496,8 +520,8 @@ __device__ __forceinline__ GroupBase group_base(const GroupParams& p, uint64_t v
 
 // FOLD for one pair of slots (j, j+1) when VEC, else one slot j:
 //   acc = P[first]; acc = acc + P[first+1]; ...   P[l] = A[l] (* B[l]).
-template <bool HAS_B, bool VEC>
-__device__ __forceinline__ void fold_slots(const GroupParams& p, const GroupBase& gb,
+template <bool HAS_B, bool VEC, class PP>
+__device__ __forceinline__ void fold_slots(const PP& p, const GroupBase& gb,
                                            const double* __restrict__ A,
                                            const double* __restrict__ B, int64_t first,
                                            int64_t count, int64_t j, double* dst) {
@@ -554,8 +578,8 @@ __device__ __forceinline__ void fold_slots(const GroupParams& p, const GroupBase
 // independent 16-byte loads before any dependent arithmetic, so a thread
 // keeps NP*16 B (x2 with unroll) of HBM reads in flight -- the fold is
 // latency bound otherwise (one long-scoreboard stall per tile step).
-template <bool HAS_B, int NP>
-__device__ __forceinline__ void fold_pairs(const GroupParams& p, const GroupBase& gb,
+template <bool HAS_B, int NP, class PP>
+__device__ __forceinline__ void fold_pairs(const PP& p, const GroupBase& gb,
                                            const double* __restrict__ A,
                                            const double* __restrict__ B, int64_t first,
                                            int64_t count, int64_t j0, int64_t jstride,
@@ -1171,13 +1195,13 @@ __global__ void __launch_bounds__(512) group_generic_kernel(const __grid_constan
 // pairs l, l+32, l+64, l+96 (fully coalesced 512-byte requests, 4 loads in
 // flight per operand).  Scalar mode: one slot per work item.
 template <bool HAS_B, bool VEC>
-__global__ void __launch_bounds__(256) fold_kernel(const __grid_constant__ GroupParams p,
+__global__ void __launch_bounds__(256) fold_kernel(const __grid_constant__ FoldParams p,
                                                     const double* __restrict__ A,
                                                     const double* __restrict__ B,
                                                     double* __restrict__ OUT,
                                                     FastDiv64 units_div) {
-  const int64_t first = p.ops[0].x;
-  const int64_t count = p.ops[0].y;
+  const int64_t first = p.first;
+  const int64_t count = p.count;
   const int64_t s = p.s;
   if (VEC) {
     const uint64_t total = static_cast<uint64_t>(p.g.groups) * units_div.d;  // warp units
@@ -1234,11 +1258,11 @@ constexpr int kBlockThreads = 256;
 
 template <bool HAS_B, int P, int Q>
 __global__ void __launch_bounds__(kBlockThreads) fold_blocked_kernel(
-    const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
+    const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
     const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ OUT) {
   const int64_t s = p.s;
-  const int64_t first = p.ops[0].x;
-  const int64_t count = p.ops[0].y;
+  const int64_t first = p.first;
+  const int64_t count = p.count;
   const int64_t sa = p.g.astep * s, sb = p.g.bstep * s;
   for (uint64_t u = blockIdx.x; u < static_cast<uint64_t>(bs.units); u += gridDim.x) {
     // u = ((rest * chunks + chunk) * nbp + pb) * nbq + qb
@@ -1331,7 +1355,7 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int BC, bool COLTREE, int SLOTS = kGemmSlots>
 __global__ void __launch_bounds__((SLOTS / 32) * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32,
                                   (SLOTS == 32 && BC == 8) ? 4 : (SLOTS == 32 || BC == 8) ? 2 : 1)
-    fold_gemm_kernel(const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
+    fold_gemm_kernel(const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
                      const double* __restrict__ A, const double* __restrict__ B,
                      double* __restrict__ OUT) {
   constexpr int kHalves = SLOTS / 32;
@@ -1342,8 +1366,8 @@ __global__ void __launch_bounds__((SLOTS / 32) * (kGemmBlk / kGemmSubR) * (BC / 
   extern __shared__ __align__(16) double gsm[];
   // ring of kGemmStages super-stages, each holding kGemmPair fold steps
   const int64_t s = p.s;
-  const int64_t first = p.ops[0].x;
-  const int64_t count = p.ops[0].y;
+  const int64_t first = p.first;
+  const int64_t count = p.count;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int slot = (warp % kHalves) * 32 + lane;  // slot within the unit
@@ -1596,7 +1620,7 @@ template <int BC, int SL, int kTgSteps, int kTgStages, int SC, int PB = kGemmBlk
 __global__ void __maxnreg__(SC == 8 ? 232 : 128)
     fold_gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
                          const __grid_constant__ CUtensorMap mapB,
-                         const __grid_constant__ GroupParams p, const __grid_constant__ BlockSpec bs,
+                         const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
                          const __grid_constant__ TgSpec ts, double* __restrict__ OUT,
                          unsigned int* __restrict__ sched) {
   constexpr int kW = tg_warps<BC, SL, SC, PB>();
@@ -1619,7 +1643,7 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
   }
   __syncthreads();
   const int64_t s = p.s;
-  const int cnt = static_cast<int>(p.ops[0].y);
+  const int cnt = static_cast<int>(p.count);
   const int nst = (cnt + kTgSteps - 1) / kTgSteps;  // stages per unit
   const uint64_t units = static_cast<uint64_t>(bs.units);
 
@@ -2134,16 +2158,20 @@ template <bool HAS_B>
 void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
                  double* tout) {
   const int64_t s = p.s;
-  const bool vec = (s % 2 == 0) && aligned16(ta) && (!HAS_B || aligned16(tb)) && aligned16(tout);
+  // 256 slots per warp when that still gives every SM >= 8 warps; otherwise
+  // one slot per thread (small folds are latency bound: more loads in flight)
+  const int64_t vec_warps = p.g.groups * ((s / 2 + 127) / 128);
+  const bool vec = (s % 2 == 0) && aligned16(ta) && (!HAS_B || aligned16(tb)) && aligned16(tout) &&
+                   vec_warps >= 8 * static_cast<int64_t>(c.sm_count);
   if (vec) {
     const uint64_t units = static_cast<uint64_t>((s / 2 + 127) / 128);
     const int64_t work = (p.g.groups * static_cast<int64_t>(units) + 7) / 8;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, true>, 256, 0, work);
-    fold_kernel<HAS_B, true><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout, make_div64(units));
+    fold_kernel<HAS_B, true><<<grid, 256, 0, c.stream>>>(to_fold(p), ta, tb, tout, make_div64(units));
   } else {
     const int64_t work = (p.g.groups * s + 255) / 256;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, false>, 256, 0, work);
-    fold_kernel<HAS_B, false><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout,
+    fold_kernel<HAS_B, false><<<grid, 256, 0, c.stream>>>(to_fold(p), ta, tb, tout,
                                                            make_div64(static_cast<uint64_t>(s)));
   }
   post_launch(c, "fold kernel");
@@ -2256,7 +2284,7 @@ bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupPar
   const int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
   unsigned int* sched = g_gemm_dynamic ? take_sched_slot(c) : nullptr;
   k<<<grid, threads, smem, c.stream>>>(*reinterpret_cast<const CUtensorMap*>(mapA),
-                                       *reinterpret_cast<const CUtensorMap*>(mapB), pr, bs, ts, tout,
+                                       *reinterpret_cast<const CUtensorMap*>(mapB), to_fold(pr), bs, ts, tout,
                                        sched);
   post_launch(c, "gemm fold kernel (TMA)");
   return true;
@@ -2286,7 +2314,7 @@ void run_blocked(const LaunchCtx& c, const GroupParams& p, const BlockSpec& bs, 
                  const double* tb, double* tout) {
   auto k = fold_blocked_kernel<HAS_B, P, Q>;
   const int grid = grid_for(c, (const void*)k, kBlockThreads, 0, bs.units);
-  k<<<grid, kBlockThreads, 0, c.stream>>>(p, bs, ta, tb, tout);
+  k<<<grid, kBlockThreads, 0, c.stream>>>(to_fold(p), bs, ta, tb, tout);
   post_launch(c, "blocked fold kernel");
 }
 
@@ -2349,7 +2377,7 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
     set_smem_attr((const void*)k, smem);
     const int threads = Q == 8 ? 128 : 256;
     const int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
-    k<<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+    k<<<grid, threads, smem, c.stream>>>(to_fold(pr), bs, ta, tb, tout);
     post_launch(c, coltree ? "gemm fold + column tree kernel (32-slot units)" : "gemm fold kernel (32-slot units)");
   } else if (gemm) {
     const size_t smem =
@@ -2361,11 +2389,11 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
     const int threads = Q == 16 ? 512 : 256;
     const int grid = grid_for(c, k, threads, smem, bs.units);
     if (coltree)
-      fold_gemm_kernel<16, true><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+      fold_gemm_kernel<16, true><<<grid, threads, smem, c.stream>>>(to_fold(pr), bs, ta, tb, tout);
     else if (Q == 16)
-      fold_gemm_kernel<16, false><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+      fold_gemm_kernel<16, false><<<grid, threads, smem, c.stream>>>(to_fold(pr), bs, ta, tb, tout);
     else
-      fold_gemm_kernel<8, false><<<grid, threads, smem, c.stream>>>(pr, bs, ta, tb, tout);
+      fold_gemm_kernel<8, false><<<grid, threads, smem, c.stream>>>(to_fold(pr), bs, ta, tb, tout);
     post_launch(c, coltree ? "gemm fold + column tree kernel" : "gemm fold kernel");
   } else if (P == 8 && Q == 8)
     run_blocked<HAS_B, 8, 8>(c, pr, bs, ta, tb, tout);
@@ -2380,7 +2408,16 @@ template <bool HAS_B>
 void launch_fold_best(const LaunchCtx& c, const GroupParams& p, const double* ta,
                       const double* tb, double* tout) {
   const BlockPlan bp = block_plan(p.g, HAS_B);
-  if (HAS_B && (bp.ia >= 0 || bp.ib >= 0) && p.ops[0].y > 1 && forced_path() != 3)
+  bool blocked = HAS_B && (bp.ia >= 0 || bp.ib >= 0) && p.ops[0].y > 1 && forced_path() != 3;
+  if (blocked && (bp.ia < 0 || bp.ib < 0)) {
+    // one broadcast dim: the blocked kernel's 256-thread units (8 groups x 256
+    // slots) must still cover every SM twice, else the plain fold has more
+    // loads in flight (config 2: 24 -> ~8 us)
+    const int64_t e = p.g.ext[bp.ia >= 0 ? bp.ia : bp.ib];
+    const int64_t units = (p.g.groups / e) * ((e + 7) / 8) * ((p.s + kBlockThreads - 1) / kBlockThreads);
+    if (units < 2 * static_cast<int64_t>(c.sm_count)) blocked = false;
+  }
+  if (blocked)
     launch_fold_blocked<HAS_B>(c, p, bp, ta, tb, tout);
   else
     launch_fold<HAS_B>(c, p, ta, tb, tout);
@@ -2615,9 +2652,12 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
     // Too few groups to occupy every SM: fold over the whole grid first
     // (phase 1, into OUT), then run the schedule on OUT in place (phase 2).
     const int64_t per_sm = std::max<int64_t>(1, static_cast<int64_t>(c.smem_optin / (tile_bytes + 1024)));
+    // ...unless the whole reduction is tiny (< 2^20 product slots): then one
+    // fused launch beats two (small ops are launch-latency bound; config 1)
+    const bool tiny = g.groups * prog.ops[0].y * s < (int64_t{1} << 20);
     if ((g.groups < static_cast<int64_t>(c.sm_count) * std::min<int64_t>(per_sm, 4) ||
          (matmul_like && force != 1 && force != 2)) &&
-        prog.ops[0].y > 1) {
+        prog.ops[0].y > 1 && !(tiny && force == 0)) {
       // phase 2 plan first: the row-shift pass needs the folded tiles in a
       // separate buffer, so phase 1 then folds into session scratch
       TreePass tpass;

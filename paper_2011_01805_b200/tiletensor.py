@@ -114,13 +114,14 @@ _FROM_C_CACHE: dict = {}
 class TileTensorShape:
     """TileTensorShape shape.hpp:72-138 (validated by the native library)."""
 
-    __slots__ = ("_dims", "_relaxed", "_c", "_tiles")
+    __slots__ = ("_dims", "_relaxed", "_c", "_tiles", "_hash")
 
     def __init__(self, dims: Sequence[DimSpec], relaxed: bool = False):
         self._dims = tuple(dims)
         self._relaxed = bool(relaxed)
         self._c = None
         self._tiles = None
+        self._hash = None
         _check(lib().tt_shape_check(ctypes.byref(self.to_c())))
 
     # construction helpers
@@ -155,6 +156,7 @@ class TileTensorShape:
         obj._relaxed = bool(c.relaxed)
         obj._c = None
         obj._tiles = None
+        obj._hash = None
         if len(_FROM_C_CACHE) >= 4096:
             _FROM_C_CACHE.clear()
         _FROM_C_CACHE[key] = obj
@@ -214,7 +216,9 @@ class TileTensorShape:
                 and self._relaxed == other._relaxed)
 
     def __hash__(self):
-        return hash((self._dims, self._relaxed))
+        if self._hash is None:
+            self._hash = hash((self._dims, self._relaxed))
+        return self._hash
 
     def __repr__(self) -> str:
         return f"TileTensorShape({format_shape(self)}{', relaxed' if self._relaxed else ''})"
@@ -310,6 +314,16 @@ _COST_FIELDS = ("additions", "multiplications", "mask_multiplications", "rotatio
 # ---- session ------------------------------------------------------------------------
 
 
+def _current_raw_stream(device: int) -> int:
+    """cudaStream_t of torch's current stream on `device` (the raw accessor
+    when this torch has it: ~10x cheaper than building a Stream object)."""
+    torch = _torch()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(device))
+    return torch.cuda.current_stream(device).cuda_stream
+
+
 def _torch():
     import torch  # plumbing: device memory + streams
     return torch
@@ -342,8 +356,7 @@ class Session:
 
     @property
     def handle(self):
-        torch = _torch()
-        stream = torch.cuda.current_stream(self._device).cuda_stream
+        stream = _current_raw_stream(self._device)
         if stream != self._stream:  # re-bind only when torch's current stream changed
             _check(lib().tt_session_set_stream(self._ptr, ctypes.c_void_p(stream)))
             self._stream = stream
@@ -414,6 +427,17 @@ class TileTensor:
         self._session = session
         self._chain = session.max_chain_index() if chain is None else int(chain)
 
+    @classmethod
+    def _wrap(cls, shape: TileTensorShape, tiles, session: Session, chain: int) -> "TileTensor":
+        """An operator result: `tiles` is a fresh contiguous [tile_count, s]
+        device array from Session.empty_tiles (no validation needed)."""
+        obj = cls.__new__(cls)
+        obj._shape = shape
+        obj._tiles = tiles
+        obj._session = session
+        obj._chain = int(chain)
+        return obj
+
     def shape(self) -> TileTensorShape:
         return self._shape
 
@@ -483,16 +507,32 @@ def unpack(t: TileTensor) -> np.ndarray:
     return unpack_device(t).cpu().numpy()
 
 
+# result tile counts by (op, operand shapes, dim): sizing an output costs a
+# shape-rule evaluation through the C-ABI, which dominates small ops' host time
+_RESULT_TILES: dict = {}
+
+
+def _result_tiles(key, compute) -> int:
+    n = _RESULT_TILES.get(key)
+    if n is None:
+        n = compute()
+        if len(_RESULT_TILES) >= 4096:
+            _RESULT_TILES.clear()
+        _RESULT_TILES[key] = n
+    return n
+
+
 def tt_elementwise(a: TileTensor, b: TileTensor, op) -> TileTensor:
     s = _same_session(a, b)
     so = CShape()
     chain = ctypes.c_int64()
-    res_shape = elementwise_result_shape(a.shape(), b.shape(), op)
-    out = s.empty_tiles(res_shape.tile_count())
+    n_out = _result_tiles(("ew", int(op), a.shape(), b.shape()),
+                          lambda: elementwise_result_shape(a.shape(), b.shape(), op).tile_count())
+    out = s.empty_tiles(n_out)
     _check(lib().tt_elementwise(s.handle, int(op), ctypes.byref(a.shape().to_c()), _ptr(a.data()),
                                 a.chain_index(), ctypes.byref(b.shape().to_c()), _ptr(b.data()),
                                 b.chain_index(), ctypes.byref(so), _ptr(out), ctypes.byref(chain)))
-    return TileTensor(TileTensorShape.from_c(so), out, s, chain.value)
+    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
 
 
 def tt_add(a: TileTensor, b: TileTensor) -> TileTensor:
@@ -510,28 +550,29 @@ def _variant(v) -> int:
 def tt_sum(t: TileTensor, dim: int, variant: Optional[SumVariant] = None) -> TileTensor:
     """tt_sum tile_tensor.hpp:286-347."""
     s = t.session()
-    res_shape = sum_result_shape(t.shape(), dim)
-    out = s.empty_tiles(res_shape.tile_count())
+    n_out = _result_tiles(("sum", t.shape(), int(dim)),
+                          lambda: sum_result_shape(t.shape(), dim).tile_count())
+    out = s.empty_tiles(n_out)
     so = CShape()
     _check(lib().tt_sum(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()), int(dim),
                         _variant(variant), ctypes.byref(so), _ptr(out)))
-    return TileTensor(TileTensorShape.from_c(so), out, s, t.chain_index())
+    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, t.chain_index())
 
 
 def tt_mul_sum(a: TileTensor, b: TileTensor, dim: int,
                variant: Optional[SumVariant] = None) -> TileTensor:
     """tt_sum(tt_mul(a, b), dim) fused: one pass, product never stored."""
     s = _same_session(a, b)
-    prod = elementwise_result_shape(a.shape(), b.shape(), OpKind.mul)
-    res_shape = sum_result_shape(prod, dim)
-    out = s.empty_tiles(res_shape.tile_count())
+    n_out = _result_tiles(("mulsum", a.shape(), b.shape(), int(dim)), lambda: sum_result_shape(
+        elementwise_result_shape(a.shape(), b.shape(), OpKind.mul), dim).tile_count())
+    out = s.empty_tiles(n_out)
     so = CShape()
     chain = ctypes.c_int64()
     _check(lib().tt_mul_sum(s.handle, ctypes.byref(a.shape().to_c()), _ptr(a.data()),
                             a.chain_index(), ctypes.byref(b.shape().to_c()), _ptr(b.data()),
                             b.chain_index(), int(dim), _variant(variant), ctypes.byref(so),
                             _ptr(out), ctypes.byref(chain)))
-    return TileTensor(TileTensorShape.from_c(so), out, s, chain.value)
+    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
 
 
 _PRODUCT_TILES: dict = {}
@@ -588,7 +629,7 @@ def clean_unknowns(t: TileTensor) -> TileTensor:  # tile_tensor.hpp:352-386
     _check(lib().tt_clean_unknowns(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()),
                                    t.chain_index(), ctypes.byref(so), _ptr(out),
                                    ctypes.byref(chain)))
-    return TileTensor(TileTensorShape.from_c(so), out, s, chain.value)
+    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
 
 
 def replicate_dim(t: TileTensor, dim: int) -> TileTensor:  # tile_tensor.hpp:391-420
@@ -597,7 +638,7 @@ def replicate_dim(t: TileTensor, dim: int) -> TileTensor:  # tile_tensor.hpp:391
     so = CShape()
     _check(lib().tt_replicate_dim(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()),
                                   int(dim), ctypes.byref(so), _ptr(out)))
-    return TileTensor(TileTensorShape.from_c(so), out, s, t.chain_index())
+    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, t.chain_index())
 
 
 # ---- tile-level primitives over [n, s] device arrays (backend.hpp / rotate_sum.hpp) ----
