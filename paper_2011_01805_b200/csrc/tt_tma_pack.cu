@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -27,8 +28,16 @@ namespace ttb {
 
 namespace {
 
-constexpr int kMaxBoxBytes = 64 * 1024;
-constexpr int kMaxRing = 8;
+// Largest sub-box per TMA transfer and ring depth.  Measured on config 5
+// (16 GiB): pack is fastest with 16 KiB boxes x 8 buffers (5.13 ms, 6.69 TB/s;
+// 64 KiB x 3: 5.52 ms), unpack with 64 KiB boxes (5.54 ms; 16 KiB x 8: 5.98).
+// TT_PACK_BOX_KB / TT_PACK_RING override both, for measurement.
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+int max_box_bytes(bool pack) { return env_int("TT_PACK_BOX_KB", pack ? 16 : 64) * 1024; }
+int max_ring() { return env_int("TT_PACK_RING", 8); }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -206,7 +215,9 @@ struct TmaPlan {
   size_t smem = 0;
 };
 
-TmaPlan plan_tma(const LaunchCtx& c, const Shape& sh, int64_t s, const double* dense) {
+TmaPlan plan_tma(const LaunchCtx& c, const Shape& sh, int64_t s, const double* dense, bool pack) {
+  const int kMaxBoxBytes = max_box_bytes(pack);
+  const int kMaxRing = max_ring();
   TmaPlan tp;
   const int rank = sh.rank();
   if (rank > 5 || sh.relaxed || sh.tile_slots() != s) return tp;
@@ -227,7 +238,9 @@ TmaPlan plan_tma(const LaunchCtx& c, const Shape& sh, int64_t s, const double* d
   int64_t subs = 1;
   const int64_t tile_bytes = s * static_cast<int64_t>(sizeof(double));
   while (tile_bytes / subs > kMaxBoxBytes && sh.dims[split].t % (subs * 2) == 0) subs *= 2;
-  if (tile_bytes / subs > kMaxBoxBytes) return tp;
+  // a tile that cannot be split down to the preferred box still takes TMA
+  // with boxes up to 64 KiB
+  if (tile_bytes / subs > std::max(kMaxBoxBytes, 64 * 1024)) return tp;
   EncodeTiledFn enc = encode_fn();
   if (!enc) return tp;
   cuuint64_t gdim[5], gstride[4];
@@ -270,7 +283,7 @@ template <bool PACK>
 bool launch_tma_copy(const LaunchCtx& c, const Shape& sh, int64_t s, const double* dense,
                      double* tiles) {
   if ((reinterpret_cast<uintptr_t>(tiles) & 15) != 0) return false;
-  TmaPlan tp = plan_tma(c, sh, s, dense);
+  TmaPlan tp = plan_tma(c, sh, s, dense, PACK);
   if (!tp.ok) return false;
   const void* k = nullptr;
   switch (tp.pp.rank) {
