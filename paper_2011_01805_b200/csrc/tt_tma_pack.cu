@@ -29,14 +29,16 @@ namespace ttb {
 namespace {
 
 // Largest sub-box per TMA transfer and ring depth.  Measured on config 5
-// (16 GiB): pack is fastest with 16 KiB boxes x 8 buffers (5.13 ms, 6.69 TB/s;
-// 64 KiB x 3: 5.52 ms), unpack with 64 KiB boxes (5.54 ms; 16 KiB x 8: 5.98).
-// TT_PACK_BOX_KB / TT_PACK_RING override both, for measurement.
+// (16 GiB): on an idle GPU pack is fastest with 16 KiB boxes x 8 buffers
+// (5.13 ms vs 5.52 ms with 64 KiB x 3), but right after ~100 ms of fused
+// products (the bench's order) the 16 KiB ring drops to 6.1 ms while 64 KiB
+// boxes hold 5.56 ms -- so 64 KiB is the default for both directions.
+// TT_PACK_BOX_KB / TT_PACK_RING override, for measurement.
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
 }
-int max_box_bytes(bool pack) { return env_int("TT_PACK_BOX_KB", pack ? 16 : 64) * 1024; }
+int max_box_bytes(bool) { return env_int("TT_PACK_BOX_KB", 64) * 1024; }
 int max_ring() { return env_int("TT_PACK_RING", 8); }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
