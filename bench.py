@@ -469,6 +469,19 @@ def bench_small_configs(tt, configs, stream, hbm_peak, reps):
     t = time_events(c4_chain, reps, stream)
     out["c4_fc_square_fc"] = {"us": t * 1e6, "samples_per_s": 4096 / t,
                               "note": "784->100->square->10 on 4096 samples, batch interleaved (~) in tile dim 3"}
+    # the same chains captured once into CUDA graphs and replayed (no host launch cost)
+    for name, fn in (("c1_mul_sum", lambda: tt.tt_mul_sum(A, B, 2)),
+                     ("c2_matvec", lambda: tt.matvec_a(M, V)), ("c4_fc_square_fc", c4_chain)):
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                fn()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        out[name]["graph_replay_us"] = time_events(g.replay, reps, stream) * 1e6
     return out
 
 

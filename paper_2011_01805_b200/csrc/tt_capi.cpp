@@ -16,6 +16,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "tt_internal.hpp"
 #include "tt_launch.hpp"
@@ -30,6 +31,7 @@ struct tt_session {
   uint64_t launches = 0;
   std::mutex mu;  // serialises launches + scratch (counters are atomic)
   double* scratch = nullptr;
+  std::vector<double*> retired;  // outgrown scratch buffers (see scratch_fn)
   // work-queue counters of dynamically scheduled kernels: a ring of
   // kSchedSlots (next, done) pairs, each left at zero by the launch using it
   unsigned int* sched = nullptr;
@@ -76,11 +78,11 @@ int guarded(Fn&& fn) {
 double* scratch_fn(void* owner, size_t bytes) {
   auto* s = static_cast<tt_session*>(owner);
   if (bytes > s->scratch_bytes) {
-    if (s->scratch) {
-      check_cuda(cudaStreamSynchronize(s->stream), "scratch sync");
-      check_cuda(cudaFree(s->scratch), "scratch free");
-      s->scratch = nullptr;
-    }
+    // a smaller buffer is retired, not freed: work already enqueued -- or
+    // captured into a CUDA graph -- may still reference it (freed at destroy)
+    if (s->scratch) s->retired.push_back(s->scratch);
+    s->scratch = nullptr;
+    bytes = std::max(bytes, s->scratch_bytes + s->scratch_bytes / 2);  // geometric growth
     check_cuda(cudaMalloc(&s->scratch, bytes), "scratch alloc");
     s->scratch_bytes = bytes;
   }
@@ -360,6 +362,7 @@ void tt_session_destroy(tt_session* s) {
   cudaSetDevice(s->device);
   if (s->own_stream) cudaStreamSynchronize(s->own_stream);
   if (s->scratch) cudaFree(s->scratch);
+  for (double* p : s->retired) cudaFree(p);
   if (s->sched) cudaFree(s->sched);
   if (s->own_stream) cudaStreamDestroy(s->own_stream);
   delete s;
