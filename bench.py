@@ -368,6 +368,12 @@ def run_ours(args):
                        "frac_of_8TBps": pb / t / 1e12 / 8.0, "tile_slots_per_s": X_TILES * S5 / t,
                        "alg_bytes": pb}
         del t
+        # unfused elementwise (tt_mul with W broadcast along dim 1, tt_add): 16 GiB in, 16 GiB out
+        for name, fn, nb in (("ew_mul_bcast", lambda: tt.tt_mul(X, W), (2 * X_TILES + W_TILES) * S5 * 8),
+                             ("ew_add", lambda: tt.tt_add(X, X), 2 * X_TILES * S5 * 8)):
+            t = time_events(fn, max(1, args.steps), stream)
+            ops[name] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak,
+                         "tile_slots_per_s": X_TILES * S5 / t, "alg_bytes": nb}
         ops.update(bench_matmul(tt, configs, S, stream, hbm_peak, max(3, args.steps)))
         ops.update(bench_small_configs(tt, configs, stream, hbm_peak, max(20, args.steps)))
 

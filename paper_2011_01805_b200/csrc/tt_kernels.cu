@@ -385,6 +385,7 @@ struct EwParams {
   FastDiv32 ediv[R];      // out external extents
   int64_t a_stride[R];    // tile-index stride of A along dim i, 0 where A broadcasts
   int64_t b_stride[R];
+  int64_t o_stride[R];    // chunk kernel: out tile-index stride; dims in visiting order
 };
 
 template <int OP, bool VEC>
@@ -433,6 +434,61 @@ __global__ void __launch_bounds__(256) elementwise_kernel(const __grid_constant_
       for (int k = 0; k < 4; ++k)
         if (h0 + k < p.s)
           po[k] = OP == TT_OP_ADD ? dadd(pa[k], pb[k]) : dmul(pa[k], pb[k]);
+    }
+  }
+}
+
+// Streaming form for even s (the common case): a work item is a 2048-slot
+// chunk of one output tile; the external-index decomposition (broadcast
+// source tiles) is done once per item, uniformly, and each thread then
+// moves 4 x 16 bytes of A, B and OUT with all eight loads in flight --
+// the per-16-byte index math of elementwise_kernel is what held the
+// broadcast product on config 5 to 62% of the copy peak.
+constexpr int kEwU = 8;                // double2 per thread per item
+constexpr int kEwChunk = 512 * kEwU;   // slots per work item (256 threads x kEwU x double2)
+template <int OP>
+__global__ void __launch_bounds__(256) elementwise_chunk_kernel(const __grid_constant__ EwParams p,
+                                                                 const double* __restrict__ a,
+                                                                 const double* __restrict__ b,
+                                                                 double* __restrict__ out,
+                                                                 FastDiv64 chunks_div) {
+  const uint64_t items = static_cast<uint64_t>(p.n_tiles) * chunks_div.d;
+  const int tid = threadIdx.x;
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const uint64_t vt = fdiv(item, chunks_div);  // tile in visiting order
+    const int64_t base = static_cast<int64_t>(item - vt * chunks_div.d) * kEwChunk;
+    uint32_t rem = static_cast<uint32_t>(vt);
+    int64_t fa = 0, fb = 0, flat = 0;
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      if (i < p.rank) {
+        const uint32_t q = fdiv(rem, p.ediv[i]);
+        const int64_t li = rem - q * p.ediv[i].d;
+        rem = q;
+        fa += li * p.a_stride[i];
+        fb += li * p.b_stride[i];
+        flat += li * p.o_stride[i];
+      }
+    }
+    const double2* pa = reinterpret_cast<const double2*>(a + fa * p.s + base);
+    const double2* pb = reinterpret_cast<const double2*>(b + fb * p.s + base);
+    double2* po = reinterpret_cast<double2*>(out + flat * p.s + base);
+    const int64_t npairs = (p.s - base) / 2 < kEwChunk / 2 ? (p.s - base) / 2 : kEwChunk / 2;
+    double2 va[kEwU], vb[kEwU];
+#pragma unroll
+    for (int u = 0; u < kEwU; ++u) {
+      const int k = u * 256 + tid;
+      if (k < npairs) {
+        va[u] = __ldg(pa + k);
+        vb[u] = __ldg(pb + k);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kEwU; ++u) {
+      const int k = u * 256 + tid;
+      if (k < npairs)
+        po[k] = OP == TT_OP_ADD ? make_double2(dadd(va[u].x, vb[u].x), dadd(va[u].y, vb[u].y))
+                                : make_double2(dmul(va[u].x, vb[u].x), dmul(va[u].y, vb[u].y));
     }
   }
 }
@@ -2044,6 +2100,12 @@ void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const doubl
   post_launch(c, "clean_unknowns kernel");
 }
 
+// TT_EW_CHUNK=0 keeps the per-16-byte elementwise kernel (measurement)
+const int g_ew_chunk = [] {
+  const char* e = std::getenv("TT_EW_CHUNK");
+  return e ? std::atoi(e) : 1;
+}();
+
 void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shape& a,
                         const Shape& b, int64_t s, const double* ta, const double* tb,
                         double* tout) {
@@ -2065,9 +2127,41 @@ void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shap
     p.b_stride[i] = eb[i] == 1 ? 0 : sb[i];
   }
   if (p.n_tiles == 0) return;
+  const bool vec = (s % 2 == 0) && aligned16(ta) && aligned16(tb) && aligned16(tout);
+  if (vec && g_ew_chunk) {
+    // visit output tiles with the dims along which an operand broadcasts
+    // innermost: consecutive work items then reuse the broadcast operand's
+    // tile from L2 (config 5 X * W: W is 128 MiB, re-read per X row otherwise)
+    EwParams q = p;
+    const auto so = row_major_strides(eo);
+    int order[R], n = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i = 0; i < p.rank; ++i) {
+        const bool bcast = eo[i] > 1 && (p.a_stride[i] == 0 || p.b_stride[i] == 0);
+        if (bcast == (pass == 1)) order[n++] = i;
+      }
+    for (int k = 0; k < p.rank; ++k) {
+      const int i = order[k];
+      q.ediv[k] = p.ediv[i];
+      q.a_stride[k] = p.a_stride[i];
+      q.b_stride[k] = p.b_stride[i];
+      q.o_stride[k] = so[i];
+    }
+    const uint64_t chunks = static_cast<uint64_t>((s + kEwChunk - 1) / kEwChunk);
+    const FastDiv64 cd = make_div64(chunks);
+    const int64_t items = p.n_tiles * static_cast<int64_t>(chunks);
+    if (op == TT_OP_ADD) {
+      const int grid = grid_for(c, (const void*)elementwise_chunk_kernel<TT_OP_ADD>, 256, 0, items);
+      elementwise_chunk_kernel<TT_OP_ADD><<<grid, 256, 0, c.stream>>>(q, ta, tb, tout, cd);
+    } else {
+      const int grid = grid_for(c, (const void*)elementwise_chunk_kernel<TT_OP_MUL>, 256, 0, items);
+      elementwise_chunk_kernel<TT_OP_MUL><<<grid, 256, 0, c.stream>>>(q, ta, tb, tout, cd);
+    }
+    post_launch(c, "elementwise chunk kernel");
+    return;
+  }
   const uint64_t quads = static_cast<uint64_t>((s + 3) / 4);
   const FastDiv64 qd = make_div64(quads);
-  const bool vec = (s % 2 == 0) && aligned16(ta) && aligned16(tb) && aligned16(tout);
   const int64_t work = (p.n_tiles * static_cast<int64_t>(quads) + 255) / 256;
 #define TT_EW(OPV, VECV)                                                                  \
   {                                                                                       \
