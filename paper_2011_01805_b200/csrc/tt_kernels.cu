@@ -376,6 +376,86 @@ __global__ void __launch_bounds__(256) clean_kernel(const __grid_constant__ Geo 
   }
 }
 
+// Chunked form (even s): a work item is a 4096-slot chunk of one tile.  The
+// tile's coordinates are decoded once per item; when every in-tile coordinate
+// of the tile maps inside the used region (all tiles but the '?' boundary
+// ones), the chunk is a vectorised multiply by 1.0 with no per-slot index
+// math, otherwise the per-slot mask test of clean_kernel.
+constexpr int kCleanChunk = 4096;
+template <int RK>
+__global__ void __launch_bounds__(256) clean_chunk_kernel(const __grid_constant__ Geo g,
+                                                           const double* __restrict__ in,
+                                                           double* __restrict__ out,
+                                                           FastDiv64 chunks_div) {
+  const uint64_t items = static_cast<uint64_t>(g.n_tiles) * chunks_div.d;
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const uint64_t flat = fdiv(item, chunks_div);
+    const int64_t base = static_cast<int64_t>(item - flat * chunks_div.d) * kCleanChunk;
+    uint32_t l[RK];
+    tile_coords<RK>(g, static_cast<uint32_t>(flat), l);
+    bool full = g.tile_slots == g.s;
+#pragma unroll
+    for (int i = 0; i < RK; ++i) {
+      const int64_t last = g.inter[i] ? (g.t[i] - 1) * g.ext[i] + l[i] : l[i] * g.t[i] + g.t[i] - 1;
+      full = full && last < g.used[i];
+    }
+    const double* src = in + flat * g.s + base;
+    double* dst = out + flat * g.s + base;
+    const int64_t n = g.s - base < kCleanChunk ? g.s - base : kCleanChunk;
+    if (full) {
+      const double2* s2 = reinterpret_cast<const double2*>(src);
+      double2* d2 = reinterpret_cast<double2*>(dst);
+      double2 v[kCleanChunk / 512];
+#pragma unroll
+      for (int u = 0; u < kCleanChunk / 512; ++u) {
+        const int64_t k = u * 256 + threadIdx.x;
+        if (2 * k < n) v[u] = __ldg(s2 + k);
+      }
+#pragma unroll
+      for (int u = 0; u < kCleanChunk / 512; ++u) {
+        const int64_t k = u * 256 + threadIdx.x;
+        if (2 * k < n) d2[k] = make_double2(dmul(v[u].x, 1.0), dmul(v[u].y, 1.0));
+      }
+    } else {
+      // boundary tile: the used slots form the box m_i < v_i in tile
+      // coordinates; with power-of-two extents m_i = (h >> sh_i) & (t_i - 1)
+      bool pow2 = true;
+      int64_t v[RK];
+      int sh[RK];
+#pragma unroll
+      for (int i = 0; i < RK; ++i) {
+        pow2 = pow2 && (g.t[i] & (g.t[i] - 1)) == 0 && (g.tstride[i] & (g.tstride[i] - 1)) == 0;
+        const int64_t left = g.inter[i] ? (g.used[i] - l[i] + g.ext[i] - 1) / g.ext[i]
+                                        : g.used[i] - static_cast<int64_t>(l[i]) * g.t[i];
+        v[i] = left < 0 ? 0 : (left > g.t[i] ? g.t[i] : left);
+        sh[i] = __ffsll(static_cast<long long>(g.tstride[i])) - 1;
+      }
+      if (pow2) {
+        const double2* s2 = reinterpret_cast<const double2*>(src);
+        double2* d2 = reinterpret_cast<double2*>(dst);
+        for (int64_t k = threadIdx.x; 2 * k < n; k += blockDim.x) {
+          const double2 x = __ldg(s2 + k);
+          double m[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t h = base + 2 * k + e;
+            bool ok = h < g.tile_slots;
+#pragma unroll
+            for (int i = 0; i < RK; ++i) ok = ok && ((h >> sh[i]) & (g.t[i] - 1)) < v[i];
+            m[e] = ok ? 1.0 : 0.0;
+          }
+          d2[k] = make_double2(dmul(x.x, m[0]), dmul(x.y, m[1]));
+        }
+      } else {
+        for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+          const double mask = slot_source<RK>(g, l, static_cast<uint32_t>(base + k)) >= 0 ? 1.0 : 0.0;
+          dst[k] = dmul(src[k], mask);  // Session::mask_mul backend.hpp:145
+        }
+      }
+    }
+  }
+}
+
 // ---- elementwise with external broadcast ------------------------------------------
 
 struct EwParams {
@@ -2087,9 +2167,26 @@ void launch_unpack(const LaunchCtx& c, const Shape& shape, int64_t s, const doub
   post_launch(c, "unpack kernel");
 }
 
+// TT_EW_CHUNK=0 keeps the per-16-byte elementwise / clean kernels (measurement)
+const int g_ew_chunk = [] {
+  const char* e = std::getenv("TT_EW_CHUNK");
+  return e ? std::atoi(e) : 1;
+}();
+
 void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const double* in,
                   double* out) {
   const Geo g = make_geo(shape, s);
+  if (s % 2 == 0 && aligned16(in) && aligned16(out) && g_ew_chunk) {
+    const uint64_t chunks = static_cast<uint64_t>((s + kCleanChunk - 1) / kCleanChunk);
+    const FastDiv64 cd = make_div64(chunks);
+    const int64_t items = g.n_tiles * static_cast<int64_t>(chunks);
+    TT_RANK_SWITCH(g.rank, RK, {
+      const int grid = grid_for(c, (const void*)clean_chunk_kernel<RK>, 256, 0, items);
+      clean_chunk_kernel<RK><<<grid, 256, 0, c.stream>>>(g, in, out, cd);
+    });
+    post_launch(c, "clean_unknowns chunk kernel");
+    return;
+  }
   const uint64_t quads = static_cast<uint64_t>((s + 3) / 4);
   const FastDiv64 qd = make_div64(quads);
   const int64_t work = (g.n_tiles * static_cast<int64_t>(quads) + 255) / 256;
@@ -2099,12 +2196,6 @@ void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const doubl
   });
   post_launch(c, "clean_unknowns kernel");
 }
-
-// TT_EW_CHUNK=0 keeps the per-16-byte elementwise kernel (measurement)
-const int g_ew_chunk = [] {
-  const char* e = std::getenv("TT_EW_CHUNK");
-  return e ? std::atoi(e) : 1;
-}();
 
 void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shape& a,
                         const Shape& b, int64_t s, const double* ta, const double* tb,

@@ -100,6 +100,9 @@ struct Builder {
         while (true) {
           if (m % 2 == 1) {
             if (y == -2) {
+              // y = x (a value copy, no primitive); when nothing follows, the
+              // result IS x: no copy, so the schedule stays one in-place chain
+              if ((m - 1) / 2 == 0) return x;
               y = new_buf();
               copy(y, x);
             } else {
@@ -128,6 +131,7 @@ struct Builder {
     while (true) {
       if (m % 2 == 1) {
         if (y == -2) {
+          if ((m - 1) / 2 == 0) return x;  // as in strided(): the result is x itself
           y = new_buf();
           copy(y, x);
         } else {
