@@ -596,6 +596,38 @@ __global__ void __launch_bounds__(256) rotate_kernel(const double* __restrict__ 
   }
 }
 
+// Chunked rotate: a work item is a 4096-slot chunk of one output tile; its
+// source is the contiguous (cyclic) range starting at base + r, so each
+// thread issues 16 coalesced loads before its 16 stores (no per-slot division).
+constexpr int kRotChunk = 4096;
+__global__ void __launch_bounds__(256) rotate_chunk_kernel(const double* __restrict__ in,
+                                                            double* __restrict__ out, int64_t s,
+                                                            int64_t r, uint64_t items,
+                                                            FastDiv64 chunks_div) {
+  constexpr int U = kRotChunk / 256;
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const uint64_t tile = fdiv(item, chunks_div);
+    const int64_t base = static_cast<int64_t>(item - tile * chunks_div.d) * kRotChunk;
+    const double* t = in + tile * s;
+    double* o = out + tile * s;
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t h = base + u * 256 + threadIdx.x;
+      if (h < s) {
+        int64_t j = h + r;
+        if (j >= s) j -= s;
+        v[u] = __ldg(t + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t h = base + u * 256 + threadIdx.x;
+      if (h < s) o[h] = v[u];
+    }
+  }
+}
+
 // ---- group programs (reductions) ---------------------------------------------------
 
 struct GroupParams {
@@ -2297,6 +2329,14 @@ void launch_rotate(const LaunchCtx& c, const double* in, double* out, int64_t s,
                    int64_t n_tiles) {
   const uint64_t total = static_cast<uint64_t>(s) * n_tiles;
   if (total == 0) return;
+  const uint64_t chunks = static_cast<uint64_t>((s + kRotChunk - 1) / kRotChunk);
+  const uint64_t items = chunks * static_cast<uint64_t>(n_tiles);
+  if (s >= 1024) {  // chunked: whole 4096-slot items (small tiles keep one slot per thread)
+    const int grid = grid_for(c, (const void*)rotate_chunk_kernel, 256, 0, static_cast<int64_t>(items));
+    rotate_chunk_kernel<<<grid, 256, 0, c.stream>>>(in, out, s, r, items, make_div64(chunks));
+    post_launch(c, "rotate chunk kernel");
+    return;
+  }
   const int grid = grid_for(c, (const void*)rotate_kernel, 256, 0, (total + 255) / 256);
   rotate_kernel<<<grid, 256, 0, c.stream>>>(in, out, s, r, total, make_div64(s));
   post_launch(c, "rotate kernel");
