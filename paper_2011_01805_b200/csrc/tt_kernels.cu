@@ -24,6 +24,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <type_traits>
 
 #include "tt_launch.hpp"
 
@@ -1964,18 +1965,22 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
 // values; a thread loads its column, runs the power-of-two levels in
 // registers (v'[m] = v[m] + v[(m + e) mod t]), stores it back.  Coalesced
 // across threads (consecutive columns), no shared memory, no barrier.
-template <int T>
-__global__ void __launch_bounds__(256) col_tree_kernel(double* __restrict__ tiles, int64_t n_tiles,
+// BACK: rotations by -e*stride (replicate_tile_dim's right-to-left schedule):
+// the column is read mirrored (m -> T-1-m), which turns them into the forward
+// levels below with the same operand order.  `in` may equal `out`.
+template <int T, bool BACK = false>
+__global__ void __launch_bounds__(256) col_tree_kernel(const double* in, double* out, int64_t n_tiles,
                                                        int64_t stride, int64_t s, FastDiv64 cdiv) {
   const uint64_t total = static_cast<uint64_t>(n_tiles) * stride;
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t tile = fdiv(w, cdiv);
     const int64_t col = static_cast<int64_t>(w - tile * cdiv.d);
-    double* base = tiles + tile * s + col;
+    const double* src = in + tile * s + col;
+    double* base = out + tile * s + col;
     double v[T];
 #pragma unroll
-    for (int m = 0; m < T; ++m) v[m] = base[m * stride];
+    for (int m = 0; m < T; ++m) v[m] = src[(BACK ? T - 1 - m : m) * stride];
 #pragma unroll
     for (int e = 1; e < T; e *= 2) {
       double nv[T];
@@ -1985,7 +1990,7 @@ __global__ void __launch_bounds__(256) col_tree_kernel(double* __restrict__ tile
       for (int m = 0; m < T; ++m) v[m] = nv[m];
     }
 #pragma unroll
-    for (int m = 0; m < T; ++m) base[m * stride] = v[m];
+    for (int m = 0; m < T; ++m) base[(BACK ? T - 1 - m : m) * stride] = v[m];
   }
 }
 
@@ -2004,7 +2009,9 @@ __device__ __forceinline__ void row_shift(double (&v)[NR], int D) {
 
 // Reads the folded tiles from `in` (scratch) and writes `out`: warps read
 // halo rows owned by other warps, so the pass cannot run in place.
-template <int HR, int R = 16>
+// BACK: the tile is read and written mirrored (slot p -> s-1-p), which turns
+// rotations by -d (replicate schedules) into the forward offsets d handled here.
+template <int HR, int R = 16, bool BACK = false>
 __global__ void __launch_bounds__(256) row_tree_kernel(const double* __restrict__ in,
                                                        double* __restrict__ out, int64_t n_tiles,
                                                        int64_t s, int nlevels, int4 lv0, int4 lv1) {
@@ -2025,7 +2032,8 @@ __global__ void __launch_bounds__(256) row_tree_kernel(const double* __restrict_
     for (int i = 0; i < NR; ++i) {
       int row = rb + i;
       if (row >= rows) row -= rows;  // cyclic halo
-      v[i] = __ldg(t + row * 32 + lane);
+      const int64_t p = row * 32 + lane;
+      v[i] = __ldg(t + (BACK ? s - 1 - p : p));
     }
     for (int k = 0; k < nlevels; ++k) {
       const int d = lvl[k];
@@ -2051,7 +2059,10 @@ __global__ void __launch_bounds__(256) row_tree_kernel(const double* __restrict_
       }
     }
 #pragma unroll
-    for (int i = 0; i < R; ++i) o[(rb + i) * 32 + lane] = v[i];
+    for (int i = 0; i < R; ++i) {
+      const int64_t p = (rb + i) * 32 + lane;
+      o[BACK ? s - 1 - p : p] = v[i];
+    }
   }
 }
 
@@ -2742,6 +2753,7 @@ struct TreePass {
   int kind = 0;
   int hr = 0;
   int64_t stride0 = 0, t = 0;
+  bool back = false;  // rotations by -e*stride0 (mirrored kernels)
 };
 
 TreePass plan_tree_pass(const GroupParams& p2, int64_t s, size_t smem_optin) {
@@ -2755,9 +2767,17 @@ TreePass plan_tree_pass(const GroupParams& p2, int64_t s, size_t smem_optin) {
     tp.t = int64_t{1} << L;
     return tp;
   }
-  const int64_t stride0 = p2.rots[0];
-  for (int i = 1; i < L; ++i)
-    if (p2.rots[i] != stride0 << i) return tp;
+  // forward levels r_i = stride0 * 2^i, or backward ones r_i = s - stride0 * 2^i
+  int64_t d[8];
+  bool fwd = true, bwd = true;
+  for (int i = 0; i < L; ++i) {
+    fwd = fwd && p2.rots[i] == p2.rots[0] << i;
+    bwd = bwd && p2.rots[i] > 0 && s - p2.rots[i] == (s - p2.rots[0]) << i;
+  }
+  if (!fwd && !bwd) return tp;
+  tp.back = !fwd;
+  for (int i = 0; i < L; ++i) d[i] = tp.back ? s - p2.rots[i] : p2.rots[i];
+  const int64_t stride0 = d[0];
   const int64_t t = int64_t{1} << L;
   tp.stride0 = stride0;
   tp.t = t;
@@ -2768,9 +2788,9 @@ TreePass plan_tree_pass(const GroupParams& p2, int64_t s, size_t smem_optin) {
   if (s % (32 * 16) != 0) return tp;
   int64_t reach = 0;
   for (int i = 0; i < L; ++i) {
-    const int64_t d = p2.rots[i];
-    if (!(d < 32 || (d % 32 == 0 && d / 32 <= 16 && ((d / 32) & (d / 32 - 1)) == 0))) return tp;
-    reach += d;
+    if (!(d[i] < 32 || (d[i] % 32 == 0 && d[i] / 32 <= 16 && ((d[i] / 32) & (d[i] / 32 - 1)) == 0)))
+      return tp;
+    reach += d[i];
   }
   const int hr = static_cast<int>((reach + 31) / 32);
   if (hr > 16) return tp;
@@ -2797,52 +2817,65 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
     post_launch(c, "shared-memory tree pass");
     return;
   }
-  if (tp.kind == 1) {  // in place: folded == tout
+  if (tp.kind == 1) {  // column-local; folded may equal tout
     const int64_t stride0 = tp.stride0;
     const uint64_t total = static_cast<uint64_t>(n_tiles) * stride0;
     const FastDiv64 cd = make_div64(static_cast<uint64_t>(stride0));
     const int64_t work = static_cast<int64_t>((total + 255) / 256);
-#define TT_COL(TV)                                                                        \
-  {                                                                                      \
-    const int grid = grid_for(c, (const void*)col_tree_kernel<TV>, 256, 0, work);        \
-    col_tree_kernel<TV><<<grid, 256, 0, c.stream>>>(tout, n_tiles, stride0, s, cd);      \
+#define TT_COL(TV, BK)                                                                       \
+  {                                                                                         \
+    const int grid = grid_for(c, (const void*)col_tree_kernel<TV, BK>, 256, 0, work);       \
+    col_tree_kernel<TV, BK><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, stride0, s, cd); \
   }
-    switch (tp.t) {
-      case 2: TT_COL(2) break;
-      case 4: TT_COL(4) break;
-      case 8: TT_COL(8) break;
-      case 16: TT_COL(16) break;
-      default: TT_COL(32) break;
+#define TT_COL_T(BK)              \
+  switch (tp.t) {                 \
+    case 2: TT_COL(2, BK) break;   \
+    case 4: TT_COL(4, BK) break;   \
+    case 8: TT_COL(8, BK) break;   \
+    case 16: TT_COL(16, BK) break; \
+    default: TT_COL(32, BK) break; \
+  }
+    if (tp.back) {
+      TT_COL_T(true)
+    } else {
+      TT_COL_T(false)
     }
+#undef TT_COL_T
 #undef TT_COL
     post_launch(c, "column tree pass");
     return;
   }
   const int L = p2.nlevels;
   int lv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int i = 0; i < L; ++i) lv[i] = static_cast<int>(p2.rots[i]);
+  for (int i = 0; i < L; ++i) lv[i] = static_cast<int>(tp.back ? s - p2.rots[i] : p2.rots[i]);
   const int4 lv0 = make_int4(lv[0], lv[1], lv[2], lv[3]);
   const int4 lv1 = make_int4(lv[4], lv[5], lv[6], lv[7]);
-  const int64_t warps = n_tiles * (s / 32 / 16);
-  const int64_t work = (warps + 7) / 8;
-  if (tp.hr <= 1) {
-    const int grid = grid_for(c, (const void*)row_tree_kernel<1>, 256, 0, work);
-    row_tree_kernel<1><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
-  } else if (tp.hr <= 8) {
-    const int grid = grid_for(c, (const void*)row_tree_kernel<8>, 256, 0, work);
-    row_tree_kernel<8><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
-  } else if (g_row_rows == 32 && s % (32 * 32) == 0) {  // 32 rows per warp: 1.5x halo reads, not 2x
-    const int64_t work32 = (n_tiles * (s / 32 / 32) + 7) / 8;
-    const int grid = grid_for(c, (const void*)row_tree_kernel<16, 32>, 256, 0, work32);
-    row_tree_kernel<16, 32><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
-  } else if (g_row_rows == 64 && s % (32 * 64) == 0) {
-    const int64_t work64 = (n_tiles * (s / 32 / 64) + 7) / 8;
-    const int grid = grid_for(c, (const void*)row_tree_kernel<16, 64>, 256, 0, work64);
-    row_tree_kernel<16, 64><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
-  } else {
-    const int grid = grid_for(c, (const void*)row_tree_kernel<16>, 256, 0, work);
-    row_tree_kernel<16><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
-  }
+  auto row = [&](auto hr_c, auto r_c) {
+    constexpr int HR = decltype(hr_c)::value, RR = decltype(r_c)::value;
+    const int64_t work = (n_tiles * (s / 32 / RR) + 7) / 8;
+    if (tp.back) {
+      const int grid = grid_for(c, (const void*)row_tree_kernel<HR, RR, true>, 256, 0, work);
+      row_tree_kernel<HR, RR, true><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
+    } else {
+      const int grid = grid_for(c, (const void*)row_tree_kernel<HR, RR, false>, 256, 0, work);
+      row_tree_kernel<HR, RR, false><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
+    }
+  };
+  using I1 = std::integral_constant<int, 1>;
+  using I8 = std::integral_constant<int, 8>;
+  using I16 = std::integral_constant<int, 16>;
+  using I32 = std::integral_constant<int, 32>;
+  using I64 = std::integral_constant<int, 64>;
+  if (tp.hr <= 1)
+    row(I1{}, I16{});
+  else if (tp.hr <= 8)
+    row(I8{}, I16{});
+  else if (g_row_rows == 32 && s % (32 * 32) == 0)  // 32 rows per warp: 1.5x halo reads, not 2x
+    row(I16{}, I32{});
+  else if (g_row_rows == 64 && s % (32 * 64) == 0)
+    row(I16{}, I64{});
+  else
+    row(I16{}, I16{});
   post_launch(c, "row tree pass");
 }
 
@@ -2874,6 +2907,23 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
                         (!HAS_B || aligned16(tb)) && aligned16(tout) &&
                         tile_bytes + 2 * (2 * kTmaChunk * sizeof(double) + 16) <= c.smem_optin &&
                         force != 2;
+    // No fold (one input tile per group, e.g. replicate_dim) with a register
+    // tree pass available: read the input tiles directly, no copy and no
+    // whole-tile shared-memory tree (replicate schedules are backward
+    // rotations: the mirrored row / column kernels)
+    if (!HAS_B && prog.ops[0].y == 1 && prog.ops[0].x == 0 && force == 0) {
+      bool identity = true;
+      int64_t rm = 1;
+      for (int i = g.nd - 1; i >= 0; --i) {
+        identity = identity && g.out_stride[i] == rm && g.a_stride[i] == rm;
+        rm *= g.ext[i];
+      }
+      const TreePass tdirect = identity ? plan_tree_pass(p, s, c.smem_optin) : TreePass{};
+      if ((tdirect.kind == 1 || tdirect.kind == 2) && (tdirect.kind == 1 || ta != tout)) {
+        run_tree_pass(c, tdirect, p, g.groups, s, ta, tout);
+        return;
+      }
+    }
     // Too few groups to occupy every SM: fold over the whole grid first
     // (phase 1, into OUT), then run the schedule on OUT in place (phase 2).
     const int64_t per_sm = std::max<int64_t>(1, static_cast<int64_t>(c.smem_optin / (tile_bytes + 1024)));

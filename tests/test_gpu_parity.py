@@ -199,8 +199,14 @@ def test_clean_and_replicate(gpu, oracle):
         assert_bitwise(got.tiles(), wt, f"clean {text}")
         assert same_cost(S.cost_report(), wc)
         assert got.chain_index() == S.max_chain_index() - 1
+    # the last group reaches the mirrored register tree passes (replicate
+    # schedules rotate by -e*stride): shuffles (stride < 32), row shifts, and
+    # the column-local kind (t * stride == s)
     for text, s, dim in [("[5/2,1/4]", 8, 2), ("[7/4,1/8]", 32, 2), ("[1/8,3/4]", 32, 1),
-                         ("[3/2,1/6,2/2]", 24, 2), ("[4,1/16,5/32]", 512, 2)]:
+                         ("[3/2,1/6,2/2]", 24, 2), ("[4,1/16,5/32]", 512, 2),
+                         ("[4,3/16,1/32]", 512, 3), ("[2,1/32,3/16]", 512, 2),
+                         ("[5,1/16,2/32,3/32]", 16384, 2), ("[3,2/16,1/32,2/32]", 16384, 3),
+                         ("[3,2/16,2/32,1/32]", 16384, 4)]:
         shape = parse_shape(text)
         S = session(s)
         tiles = nrng.uniform(-5, 5, size=(shape.tile_count(), s))
