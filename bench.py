@@ -374,6 +374,23 @@ def run_ours(args):
             t = time_events(fn, max(1, args.steps), stream)
             ops[name] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak,
                          "tile_slots_per_s": X_TILES * S5 / t, "alg_bytes": nb}
+        # the other tile passes on config-5-sized data (rows a8, a10, a12)
+        reps = max(1, min(3, args.steps))
+        for k in (1, 2, 3):
+            t = time_events(lambda: tt.tt_sum(X, k), reps, stream)
+            nb = (X_TILES + OUT_TILES[k]) * S5 * 8
+            ops[f"sum_dim{k}"] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak}
+        t = time_events(lambda: tt.tiles_rotate(S, X.data(), 5), reps, stream)
+        ops["rotate"] = {"ms": t * 1e3, "GB/s": 2 * X_TILES * S5 * 8 / t / 1e9,
+                         "frac": 2 * X_TILES * S5 * 8 / t / 1e9 / hbm_peak}
+        R3 = tt.tt_sum(X, 3)  # [2048/16,2048/32,1?/32]: 8192 boundary tiles
+        nb = 2 * OUT_TILES[3] * S5 * 8
+        t = time_events(lambda: tt.clean_unknowns(R3), 10, stream)
+        ops["clean_unknowns"] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak}
+        C3 = tt.clean_unknowns(R3)
+        t = time_events(lambda: tt.replicate_dim(C3, 3), 10, stream)
+        ops["replicate_dim"] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak}
+        del R3, C3
         ops.update(bench_matmul(tt, configs, S, stream, hbm_peak, max(3, args.steps)))
         ops.update(bench_small_configs(tt, configs, stream, hbm_peak, max(20, args.steps)))
 
