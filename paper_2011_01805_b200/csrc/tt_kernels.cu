@@ -432,20 +432,35 @@ __global__ void __launch_bounds__(256) clean_chunk_kernel(const __grid_constant_
         sh[i] = __ffsll(static_cast<long long>(g.tstride[i])) - 1;
       }
       if (pow2) {
+        // only the dims this tile cuts short need a test (uniform per item)
+        bool cut[RK];
+#pragma unroll
+        for (int i = 0; i < RK; ++i) cut[i] = v[i] < g.t[i];
         const double2* s2 = reinterpret_cast<const double2*>(src);
         double2* d2 = reinterpret_cast<double2*>(dst);
-        for (int64_t k = threadIdx.x; 2 * k < n; k += blockDim.x) {
-          const double2 x = __ldg(s2 + k);
-          double m[2];
+        constexpr int U = kCleanChunk / 512;
+        double2 x[U];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int64_t h = base + 2 * k + e;
-            bool ok = h < g.tile_slots;
+        for (int u = 0; u < U; ++u) {
+          const int64_t k = u * 256 + threadIdx.x;
+          if (2 * k < n) x[u] = __ldg(s2 + k);
+        }
 #pragma unroll
-            for (int i = 0; i < RK; ++i) ok = ok && ((h >> sh[i]) & (g.t[i] - 1)) < v[i];
-            m[e] = ok ? 1.0 : 0.0;
+        for (int u = 0; u < U; ++u) {
+          const int64_t k = u * 256 + threadIdx.x;
+          if (2 * k < n) {
+            double m[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int64_t h = base + 2 * k + e;
+              bool ok = h < g.tile_slots;
+#pragma unroll
+              for (int i = 0; i < RK; ++i)
+                if (cut[i]) ok = ok && ((h >> sh[i]) & (g.t[i] - 1)) < v[i];
+              m[e] = ok ? 1.0 : 0.0;
+            }
+            d2[k] = make_double2(dmul(x[u].x, m[0]), dmul(x[u].y, m[1]));
           }
-          d2[k] = make_double2(dmul(x.x, m[0]), dmul(x.y, m[1]));
         }
       } else {
         for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
