@@ -1,0 +1,28 @@
+"""Times cryptonets_infer (paper_2011_01805_b200/nn.py) on the CryptoNets network:
+batch packed (tile [1,1,s], every scalar a tile of s samples) and tiled
+([32,256,1]-style), CUDA events around the whole call."""
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2011_01805_b200 as tt  # noqa: E402
+from paper_2011_01805_b200 import nn  # noqa: E402
+
+net = nn.cryptonets_network(42)
+for s, tile, n in ((8192, (1, 1, 8192), 8192), (8192, (32, 256, 1), 1), (8192, (8, 16, 64), 64)):
+    S = tt.Session(s, 8)
+    batch = np.random.default_rng(1).uniform(0, 1, size=(784, n))
+    nn.cryptonets_infer(net, batch, tile, S)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        r = nn.cryptonets_infer(net, batch, tile, S)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    print(f"tile {tile} batch {n}: {dt * 1e3:.2f} ms per call ({n / dt:.0f} samples/s), "
+          f"rot={r.cost.rotations} mul={r.cost.multiplications}")
