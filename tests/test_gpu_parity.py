@@ -386,3 +386,29 @@ def test_tile_matmul_gemm_paths(gpu, oracle, path):
             assert same_cost(S.cost_report(), wc)
     finally:
         tt.set_kernel_path("auto")
+
+
+def test_huge_tiles(gpu, oracle):
+    """Tiles too large for shared memory (s = 2^20 and 2^21 slots, 8-16 MiB
+    per tile): every op still runs (split fold + global-scratch schedule,
+    gather pack) and matches the oracle bit for bit -- the reference allows
+    any slot count below 2^31."""
+    nrng = np.random.default_rng(2024)
+    for text_a, text_b, s in [("[3/1024,5/1024]", "[*/1024,5/1024]", 1 << 20),
+                              ("[2/2048,2/1024]", "[2/2048,*/1024]", 1 << 21)]:
+        S = session(s)
+        sa, sb = parse_shape(text_a), parse_shape(text_b)
+        ta = nrng.uniform(-1, 1, size=(sa.tile_count(), s))
+        tb = nrng.uniform(-1, 1, size=(sb.tile_count(), s))
+        A, B = TileTensor(sa, ta, S), TileTensor(sb, tb, S)
+        for dim in (1, 2):
+            ws, wt, wc = oracle.mul_sum(sa, ta, sb, tb, s, dim)
+            S.reset_counters()
+            got = tt.tt_mul_sum(A, B, dim)
+            assert got.shape() == ws
+            assert_bitwise(got.tiles(), wt, f"huge {text_a} dim {dim}")
+            assert same_cost(S.cost_report(), wc)
+        dense = nrng.uniform(-1, 1, size=sa.tensor_extents())
+        packed = tt.pack(dense, sa, S)
+        assert_bitwise(packed.tiles(), oracle.pack(dense, sa, s), f"huge pack {text_a}")
+        assert_bitwise(tt.unpack(packed), dense, f"huge unpack {text_a}")
