@@ -644,6 +644,44 @@ __global__ void __launch_bounds__(256) rotate_chunk_kernel(const double* __restr
   }
 }
 
+// Aligned variant (s % 32 == 0): a warp owns 32 x U consecutive outputs and
+// loads the U + 1 32-slot-aligned source segments they span (cyclic), then
+// shifts by r mod 32 with shuffles -- every DRAM sector is fetched once
+// (the misaligned form's warp accesses straddle 9 sectors per 8).
+template <int U>
+__global__ void __launch_bounds__(256) rotate_aligned_kernel(const double* __restrict__ in,
+                                                              double* __restrict__ out, int64_t s,
+                                                              int64_t r, uint64_t units,
+                                                              FastDiv64 units_div) {
+  const int lane = threadIdx.x & 31;
+  const int rho = static_cast<int>(r & 31);
+  const int64_t r0 = r - rho;  // aligned part of the rotation
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+       w < units * 1; w += warps) {
+    const uint64_t tile = fdiv(w, units_div);
+    const int64_t h0 = static_cast<int64_t>(w - tile * units_div.d) * (32 * U);
+    const double* t = in + tile * s;
+    double v[U + 1];
+#pragma unroll
+    for (int u = 0; u <= U; ++u) {
+      int64_t seg = h0 + r0 + 32 * u;
+      seg = seg >= s ? seg - s : seg;
+      seg = seg >= s ? seg - s : seg;
+      v[u] = __ldg(t + seg + lane);
+    }
+    const int src = (lane + rho) & 31;
+    const bool lo = lane + rho < 32;
+    double* o = out + tile * s + h0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double a = __shfl_sync(0xffffffffu, v[u], src);
+      const double b = __shfl_sync(0xffffffffu, v[u + 1], src);
+      o[32 * u + lane] = lo ? a : b;
+    }
+  }
+}
+
 // ---- group programs (reductions) ---------------------------------------------------
 
 struct GroupParams {
@@ -2355,6 +2393,15 @@ void launch_rotate(const LaunchCtx& c, const double* in, double* out, int64_t s,
                    int64_t n_tiles) {
   const uint64_t total = static_cast<uint64_t>(s) * n_tiles;
   if (total == 0) return;
+  if (s % 512 == 0) {  // a warp unit of 32 x 16 outputs
+    const uint64_t per_tile = static_cast<uint64_t>(s / 512);
+    const uint64_t units = per_tile * static_cast<uint64_t>(n_tiles);
+    const int64_t work = static_cast<int64_t>((units + 7) / 8);
+    const int grid = grid_for(c, (const void*)rotate_aligned_kernel<16>, 256, 0, work);
+    rotate_aligned_kernel<16><<<grid, 256, 0, c.stream>>>(in, out, s, r, units, make_div64(per_tile));
+    post_launch(c, "rotate aligned kernel");
+    return;
+  }
   const uint64_t chunks = static_cast<uint64_t>((s + kRotChunk - 1) / kRotChunk);
   const uint64_t items = chunks * static_cast<uint64_t>(n_tiles);
   if (s >= 1024) {  // chunked: whole 4096-slot items (small tiles keep one slot per thread)

@@ -412,3 +412,18 @@ def test_huge_tiles(gpu, oracle):
         packed = tt.pack(dense, sa, S)
         assert_bitwise(packed.tiles(), oracle.pack(dense, sa, s), f"huge pack {text_a}")
         assert_bitwise(tt.unpack(packed), dense, f"huge unpack {text_a}")
+
+
+def test_rotate_all_kernel_forms(gpu):
+    """Session::rotate (backend.hpp:150-163): out[j] = in[(j + r) mod s] through
+    the aligned shuffle form (s % 512 == 0), the chunked form and the
+    per-slot form, for offsets across segment and tile boundaries."""
+    nrng = np.random.default_rng(31337)
+    for s in (16, 96, 1024 + 64, 512, 1024, 16384):
+        S = session(s)
+        tiles = nrng.uniform(-1, 1, size=(7, s))
+        for off in (1, 5, 31, 32, 33, 511, 512, s - 1, s + 7, -3, -s - 1):
+            r = ((off % s) + s) % s
+            got = tt.tiles_rotate(S, tiles, off)
+            want = np.roll(tiles, -r, axis=1)
+            assert_bitwise(got.detach().cpu().numpy(), want, f"rotate s={s} off={off}")
