@@ -1787,6 +1787,8 @@ __global__ void __launch_bounds__((SLOTS / 32) * (kGemmBlk / kGemmSubR) * (BC / 
 // loads in flight ahead), SC = columns of a thread's 8 x SC sub-block of groups
 
 struct TgSpec {
+  int small;                 // units < 2^31: decode with the 32-bit divisors below
+  FastDiv32 dq, dp, dc;      // nbq, nbp, chunks
   int nrest;
   int chunk_major;  // unit order: chunk fastest (consecutive CTAs read adjacent slots)
   int a_act[2], b_act[2];  // remaining group dim i is a tensor-map dim of A / B
@@ -1838,6 +1840,19 @@ __device__ __forceinline__ TgUnit tg_decode(const BlockSpec& bs, uint64_t u, int
   return t;
 }
 
+// 32-bit unit decode (qb fastest, then pb, chunk, rest), for units < 2^31
+__device__ __forceinline__ TgUnit tg_decode32(const TgSpec& ts, uint32_t u) {
+  TgUnit t;
+  const uint32_t t1 = fdiv(u, ts.dq);
+  t.qb = u - t1 * ts.dq.d;
+  const uint32_t t2 = fdiv(t1, ts.dp);
+  t.pb = t1 - t2 * ts.dp.d;
+  const uint32_t rest = fdiv(t2, ts.dc);
+  t.chunk = t2 - rest * ts.dc.d;
+  t.rest = rest;
+  return t;
+}
+
 template <int BC, int SL, int kTgSteps, int kTgStages, int SC, int PB = kGemmBlk>
 __global__ void __maxnreg__(SC == 8 ? 232 : 128)
     fold_gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA,
@@ -1881,7 +1896,8 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
   int rc[2] = {0, 0};
   TgUnit lt{};
   auto load_unit = [&]() {
-    lt = tg_decode(bs, lu, ts.chunk_major);
+    lt = (ts.small && !ts.chunk_major) ? tg_decode32(ts, static_cast<uint32_t>(lu))
+                                       : tg_decode(bs, lu, ts.chunk_major);
     uint64_t v = lt.rest;
 #pragma unroll
     for (int i = 1; i >= 0; --i) {
@@ -1927,6 +1943,13 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
 
   const int sub = warp * (32 / SL) + lane / SL, slot = lane % SL;
   const int r0 = (sub / (BC / SC)) * 8, c0 = (sub % (BC / SC)) * SC;
+  // launch-constant output strides, hoisted out of the unit loop; the fold
+  // output is re-read at once by the tree pass: keep it in L2
+  const int64_t rstep = bs.out_ia * s;
+  int64_t coff[SC];
+#pragma unroll
+  for (int k = 0; k < SC; ++k) coff[k] = k * bs.out_ib * s;
+  const uint64_t keep = policy_evict_last();
   int stage = 0;
   uint32_t phase = 0;
   for (;;) {
@@ -1935,7 +1958,8 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
     mbar_wait(&full[stage], phase);
     const uint64_t u = stage_unit[stage];
     if (u == ~uint64_t{0}) break;
-    const TgUnit t = tg_decode(bs, u, ts.chunk_major);
+    const TgUnit t = (ts.small && !ts.chunk_major) ? tg_decode32(ts, static_cast<uint32_t>(u))
+                                                   : tg_decode(bs, u, ts.chunk_major);
     double acc[8][SC];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -1983,22 +2007,28 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
         phase ^= 1;
       }
     }
-    const GroupBase gb = group_base(p, t.rest);
+    const int64_t gout = ts.nrest ? group_base(p, t.rest).out : 0;
     const int np = static_cast<int>(bs.ext_ia - t.pb * PB < PB ? bs.ext_ia - t.pb * PB : PB);
     const int nq = static_cast<int>(bs.ext_ib - t.qb * BC < BC ? bs.ext_ib - t.qb * BC : BC);
-    double* orow = OUT + (gb.out + (t.pb * PB + r0) * bs.out_ia + (t.qb * BC + c0) * bs.out_ib) * s +
+    double* orow = OUT + (gout + (t.pb * PB + r0) * bs.out_ia + (t.qb * BC + c0) * bs.out_ib) * s +
                    t.chunk * SL + slot;
-    const int64_t rstep = bs.out_ia * s, cstep = bs.out_ib * s;
-    // the fold output is re-read at once by the tree pass: keep it in L2
-    const uint64_t keep = policy_evict_last();
+    if (np == PB && nq == BC) {  // interior block: no bounds tests
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (r0 + i < np) {
+      for (int i = 0; i < 8; ++i) {
 #pragma unroll
-        for (int k = 0; k < SC; ++k)
-          if (c0 + k < nq) st_keep(orow + k * cstep, acc[i][k], keep);
+        for (int k = 0; k < SC; ++k) st_keep(orow + coff[k], acc[i][k], keep);
+        orow += rstep;
       }
-      orow += rstep;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (r0 + i < np) {
+#pragma unroll
+          for (int k = 0; k < SC; ++k)
+            if (c0 + k < nq) st_keep(orow + coff[k], acc[i][k], keep);
+        }
+        orow += rstep;
+      }
     }
   }
   // the last CTA to finish leaves the queue counters at zero for the next launch
@@ -2575,6 +2605,10 @@ bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupPar
   bs.units = pr.g.groups * bs.chunks * bs.nbp * bs.nbq;
   bs.div_nbq = make_div64(static_cast<uint64_t>(bs.nbq));
   bs.div_chunks = make_div64(static_cast<uint64_t>(bs.chunks));
+  ts.small = bs.units < (int64_t{1} << 31) ? 1 : 0;
+  ts.dq = make_div32(static_cast<uint32_t>(bs.nbq));
+  ts.dp = make_div32(static_cast<uint32_t>(bs.nbp));
+  ts.dc = make_div32(static_cast<uint32_t>(bs.chunks));
   auto k = fold_gemm_tma_kernel<BC, SL, kTgSteps, kTgStages, SC, PB>;
   constexpr size_t smem = tg_smem_bytes<BC, SL, kTgSteps, kTgStages, PB>();
   constexpr int threads = tg_warps<BC, SL, SC, PB>() * 32;
