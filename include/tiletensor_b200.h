@@ -196,6 +196,26 @@ int tt_sum_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents
 int tt_replicate_tile_dim(tt_session* s, const double* in, const int64_t* tile_extents, int rank,
                           int dim, double* out, int64_t n_tiles);     /* rotate_sum.hpp:128-152 */
 
+/* ---- cross-GPU left-fold chains (sharding.py) --------------------------- */
+/* Partial left fold of tt_sum(tt_mul(a, b), dim) -- or tt_sum(a, dim) when b
+ * is null -- over output tiles [out_begin, out_end) of the result grid (row-
+ * major): acc = init (when given), then acc = acc + product for every
+ * external index of `dim` in order; without init the fold starts from the
+ * first product, exactly as the reference's tt_sum (tile_tensor.hpp:311-318).
+ * A rank holding a slab of `dim` continues the accumulator of the rank before
+ * it, so a chain of ranks reproduces the single-GPU association bit for bit.
+ * No in-tile schedule: finish with tt_sum over `dim` on the accumulated tiles
+ * viewed with the shape tt_fold_shape gives (dim's extent one tile).
+ * Counters: the range's products and fold additions; *out_chain as tt_mul.
+ * Rejects a '?' boundary split, `~` or degenerate summed dims (use tt_mul_sum). */
+int tt_mul_fold(tt_session* s, const tt_shape* a, const double* ta, int64_t chain_a,
+                const tt_shape* b, const double* tb, int64_t chain_b, int dim,
+                int64_t out_begin, int64_t out_end, const double* init, double* acc,
+                int64_t* out_chain);
+/* Shape of the accumulated tiles of tt_mul_fold: the product shape (a alone
+ * when b is null) with `dim` reduced to one external tile (n = t). */
+int tt_fold_shape(const tt_shape* a, const tt_shape* b, int dim, tt_shape* out);
+
 /* ---- neural-network layers (nn.hpp) ------------------------------------ */
 /* Batch-packed affine layer of cryptonets_infer (nn.hpp:282-326 replaces the
  * per-scalar Session::add / Session::mul loop of infer_batch_packed): every

@@ -717,6 +717,76 @@ int tt_tiles_binary(tt_session* s, int op, const double* a, const double* b, dou
   });
 }
 
+namespace {
+// product (or a alone) and the checks shared by tt_mul_fold / tt_fold_shape
+Shape fold_product(const tt_shape* a, const tt_shape* b, int dim, int& di) {
+  const Shape sa = from_c(a);
+  const Shape prod = b ? elementwise_result_shape(sa, from_c(b), TT_OP_MUL) : sa;
+  if (dim < 1 || dim > prod.rank()) shape_error("sum dimension out of range");
+  di = dim - 1;
+  const Dim& ds = prod.dims[di];
+  if (ds.n == 1 && ds.d > 1) invalid_argument("fold chains need a non-degenerate summed dim");
+  if (ds.interleaved) invalid_argument("fold chains do not take an interleaved (~) summed dim");
+  if (ds.unknown && ds.used() % ds.t != 0)
+    invalid_argument("fold chains do not take a '?' boundary split (clean_unknowns first)");
+  return prod;
+}
+}  // namespace
+
+int tt_fold_shape(const tt_shape* a, const tt_shape* b, int dim, tt_shape* out) {
+  return guarded([&] {
+    int di = 0;
+    Shape prod = fold_product(a, b, dim, di);
+    prod.dims[di].n = prod.dims[di].t;
+    prod.dims[di].d = 1;
+    to_c(prod, out);
+  });
+}
+
+int tt_mul_fold(tt_session* s, const tt_shape* a, const double* ta, int64_t chain_a,
+                const tt_shape* b, const double* tb, int64_t chain_b, int dim,
+                int64_t out_begin, int64_t out_end, const double* init, double* acc,
+                int64_t* out_chain) {
+  return guarded([&] {
+    need_session(s);
+    if ((b == nullptr) != (tb == nullptr)) invalid_argument("operand b and its tiles go together");
+    int di = 0;
+    const Shape prod = fold_product(a, b, dim, di);
+    const Shape sa = from_c(a);
+    require_slots(s, sa, "tt_mul_fold");
+    if (b) require_slots(s, from_c(b), "tt_mul_fold");
+    check_tiles_addressable(prod);
+    const auto ext = prod.external();
+    std::vector<int64_t> gext = ext;
+    gext[di] = 1;
+    int64_t n_out = 1;
+    for (auto e : gext) n_out *= e;
+    if (out_begin < 0 || out_end > n_out || out_begin > out_end)
+      invalid_argument("output tile range out of bounds");
+    const int64_t chain = b ? mul_chain(chain_a, chain_b) : chain_a;
+    if (out_chain) *out_chain = chain;
+    const int64_t tiles = out_end - out_begin, count = ext[di];
+    if (b) s->muls += static_cast<uint64_t>(tiles * count);
+    s->adds += static_cast<uint64_t>(tiles * (count - (init ? 0 : 1)));
+    std::vector<int64_t> ast, bst;
+    operand_strides(sa, ast);
+    if (b) operand_strides(from_c(b), bst);
+    FoldRange fr;
+    fr.rank = prod.rank();
+    for (int i = 0; i < fr.rank; ++i) {
+      fr.gext[i] = gext[i];
+      fr.a_stride[i] = i == di ? 0 : ast[i];
+      fr.b_stride[i] = b && i != di ? bst[i] : 0;
+    }
+    fr.astep = ast[di];
+    fr.bstep = b ? bst[di] : 0;
+    fr.first = 0;
+    fr.count = count;
+    std::lock_guard<std::mutex> lk(s->mu);
+    launch_fold_range(ctx_of(s), fr, s->slots, out_begin, out_end, ta, tb, init, acc);
+  });
+}
+
 int tt_batch_affine(tt_session* s, const double* in, int64_t n_in, int64_t n_out,
                     const int64_t* row_ptr, const int64_t* src, const double* w,
                     const double* bias, double* out, int64_t chain_in, int64_t* chain_out) {

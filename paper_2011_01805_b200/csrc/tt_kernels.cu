@@ -2221,6 +2221,69 @@ __global__ void __launch_bounds__(256) batch_affine_kernel(const double* __restr
   }
 }
 
+// ---- fold over a range of output tiles (cross-rank chains, sharding.py) -------------
+struct FoldRangeParams {
+  int rank;
+  FastDiv32 gdiv[R];
+  int64_t a_stride[R], b_stride[R];
+  int64_t astep, bstep, first, count, s, o0, npairs_tile;
+};
+
+template <bool HAS_B, bool INIT>
+__global__ void __launch_bounds__(256) fold_range_kernel(const __grid_constant__ FoldRangeParams p,
+                                                          const double* __restrict__ A,
+                                                          const double* __restrict__ B,
+                                                          const double* __restrict__ init,
+                                                          double* __restrict__ acc_out, uint64_t total,
+                                                          FastDiv64 pairs_div) {
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = fdiv(w, pairs_div);  // output tile within the range
+    const int64_t j = static_cast<int64_t>(w - k * pairs_div.d) * 2;
+    uint32_t rem = static_cast<uint32_t>(p.o0 + static_cast<int64_t>(k));
+    int64_t fa = 0, fb = 0;
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      if (i < p.rank) {
+        const uint32_t q = fdiv(rem, p.gdiv[i]);
+        const int64_t li = rem - q * p.gdiv[i].d;
+        rem = q;
+        fa += li * p.a_stride[i];
+        fb += li * p.b_stride[i];
+      }
+    }
+    const double* pa = A + (fa + p.first * p.astep) * p.s + j;
+    const double* pb = HAS_B ? B + (fb + p.first * p.bstep) * p.s + j : nullptr;
+    const int64_t sa = p.astep * p.s, sb = p.bstep * p.s;
+    double2 acc;
+    int64_t c0 = 0;
+    if (INIT) {
+      acc = *reinterpret_cast<const double2*>(init + k * p.s + j);
+    } else {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(pa));
+      if (HAS_B) {
+        const double2 y = __ldg(reinterpret_cast<const double2*>(pb));
+        acc = make_double2(dmul(x.x, y.x), dmul(x.y, y.y));
+      } else {
+        acc = x;
+      }
+      c0 = 1;
+    }
+    for (int64_t c = c0; c < p.count; ++c) {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(pa + c * sa));
+      if (HAS_B) {
+        const double2 y = __ldg(reinterpret_cast<const double2*>(pb + c * sb));
+        acc.x = dadd(acc.x, dmul(x.x, y.x));
+        acc.y = dadd(acc.y, dmul(x.y, y.y));
+      } else {
+        acc.x = dadd(acc.x, x.x);
+        acc.y = dadd(acc.y, x.y);
+      }
+    }
+    *reinterpret_cast<double2*>(acc_out + k * p.s + j) = acc;
+  }
+}
+
 // ---- synthetic input generator (== or_fill_uniform in oracle/tt_oracle.c) ------------
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -2392,6 +2455,44 @@ void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shap
   }
 #undef TT_EW
   post_launch(c, "elementwise kernel");
+}
+
+void launch_fold_range(const LaunchCtx& c, const FoldRange& fr, int64_t s, int64_t o0, int64_t o1,
+                       const double* ta, const double* tb, const double* init, double* acc) {
+  if (o1 <= o0) return;
+  if (s % 2 != 0 || !aligned16(ta) || (tb && !aligned16(tb)) || !aligned16(acc) ||
+      (init && !aligned16(init)))
+    invalid_argument("chain folds need an even slot count and 16-byte aligned tiles");
+  FoldRangeParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.rank = fr.rank;
+  for (int i = 0; i < fr.rank; ++i) {
+    p.gdiv[i] = make_div32(static_cast<uint32_t>(fr.gext[i]));
+    p.a_stride[i] = fr.a_stride[i];
+    p.b_stride[i] = fr.b_stride[i];
+  }
+  p.astep = fr.astep;
+  p.bstep = fr.bstep;
+  p.first = fr.first;
+  p.count = fr.count;
+  p.s = s;
+  p.o0 = o0;
+  const uint64_t pairs = static_cast<uint64_t>(s / 2);
+  const uint64_t total = pairs * static_cast<uint64_t>(o1 - o0);
+  const FastDiv64 pd = make_div64(pairs);
+  const int64_t work = static_cast<int64_t>((total + 255) / 256);
+#define TT_FR(HB, IN)                                                                        \
+  {                                                                                         \
+    const int grid = grid_for(c, (const void*)fold_range_kernel<HB, IN>, 256, 0, work);      \
+    fold_range_kernel<HB, IN><<<grid, 256, 0, c.stream>>>(p, ta, tb, init, acc, total, pd);  \
+  }
+  if (tb) {
+    if (init) TT_FR(true, true) else TT_FR(true, false)
+  } else {
+    if (init) TT_FR(false, true) else TT_FR(false, false)
+  }
+#undef TT_FR
+  post_launch(c, "fold range kernel");
 }
 
 void launch_batch_affine(const LaunchCtx& c, const double* in, int64_t s, int64_t n_out,

@@ -74,6 +74,21 @@ void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shap
 void launch_batch_affine(const LaunchCtx& c, const double* in, int64_t s, int64_t n_out,
                          const int64_t* row_ptr, const int64_t* src, const double* w,
                          const double* bias, double* out);
+// Fold of a product over its summed dim for the output tiles [o0, o1) of the
+// result grid `gext` (row-major, summed dim extent 1): acc = init (when
+// given) then acc = acc + A[l]*B[l] (B optional) for l in [first, first+count)
+// in order; without init the fold starts from the first product.  Output and
+// init hold (o1 - o0) tiles.  Strides are operand tile-index strides per dim;
+// astep/bstep the operand strides along the summed dim.
+struct FoldRange {
+  int rank = 0;
+  int64_t gext[TT_MAX_RANK] = {};
+  int64_t a_stride[TT_MAX_RANK] = {};
+  int64_t b_stride[TT_MAX_RANK] = {};
+  int64_t astep = 0, bstep = 0, first = 0, count = 0;
+};
+void launch_fold_range(const LaunchCtx& c, const FoldRange& fr, int64_t s, int64_t o0, int64_t o1,
+                       const double* ta, const double* tb, const double* init, double* acc);
 void launch_binary_flat(const LaunchCtx& c, int op, const double* a, const double* b, double* out,
                         int64_t count);
 // out[t][j] = in[t][(j + r) mod s]   (backend.hpp:157-159), r in [1, s)

@@ -9,12 +9,22 @@ the same external index (or the broadcast index l mod e,
 tile_tensor.hpp:260-265), those ops run locally with NO communication and
 the results stay sharded, bit-identical to the single-GPU result.
 
-Only a sum over `shard_dim` itself spans ranks: each rank runs the fused
-fold + rotate-and-sum on its slab and the partial results are summed with one
-NCCL all-reduce over NVLink (torch.distributed, backend "nccl").  The
-cross-rank addition re-associates the reference's left fold, so that result
-matches the single-device one within 1e-12 relative (north star), not
-bitwise.
+Only a sum over `shard_dim` itself spans ranks.  Two ways:
+
+* `sharded_mul_sum`: each rank runs the fused fold + rotate-and-sum on its
+  slab and the partial results are summed with one NCCL all-reduce over
+  NVLink (torch.distributed, backend "nccl").  The cross-rank addition
+  re-associates the reference's left fold: within 1e-12 relative (north
+  star), not bitwise.
+* `chain_mul_sum`: the ranks form a chain along `shard_dim`.  Rank r
+  continues the left-fold accumulators of rank r-1 over its own slab
+  (`tt_mul_fold` with an initial accumulator) and passes them on; the last
+  rank runs the in-tile rotate-and-sum once.  This is the reference's own
+  association, so the result is bit-identical to one GPU.  The output tiles
+  are split into chunks that flow down the chain back to back (NCCL
+  send / recv are stream-ordered), so the ranks overlap: the chain costs
+  (chunks + ranks - 1) / chunks of one slab's fold plus the point-to-point
+  transfers of the accumulators.
 
 The compute backend is injectable (`ops`): on GPUs it is this package's
 CUDA path; the CPU gloo tests drive the same planning and collective logic
@@ -105,6 +115,59 @@ def sharded_mul_sum(x_local, w_local, dim: int, x_plan: ShardPlan,
     return r, True
 
 
+def chain_mul_sum(x_local, w_local, dim: int, x_plan: ShardPlan, fold: Callable, finish: Callable,
+                  n_out: int, new_acc: Callable[[int], Any], chunks: int = 16, group=None):
+    """Exact tt_sum(tt_mul(X, W), dim) for dim == shard_dim (see module doc).
+
+    fold(x, w, dim, (lo, hi), init) -> accumulator tiles of output tiles
+    [lo, hi) (init None on the first rank); finish(acc) -> the result from
+    the accumulated tiles of all n_out outputs; new_acc(k) -> a buffer of k
+    accumulator tiles to receive into.  On GPUs these are tt.mul_fold,
+    tt_sum over fold_shape and Session.empty_tiles (`gpu_chain_ops`).
+    Returns the result on the last rank, None on the others."""
+    dist = _dist()
+    world = dist.get_world_size(group) if dist is not None else 1
+    rank = dist.get_rank(group) if dist is not None else 0
+    if dim != x_plan.shard_dim or world == 1:
+        acc = fold(x_local, w_local, dim, (0, n_out), None)
+        return finish(acc)
+    chunks = max(1, min(chunks, n_out))
+    bounds = [(n_out * c // chunks, n_out * (c + 1) // chunks) for c in range(chunks)]
+    parts = []
+    for lo, hi in bounds:
+        if hi <= lo:
+            continue
+        init = None
+        if rank > 0:
+            init = new_acc(hi - lo)
+            dist.recv(init, src=rank - 1, group=group)
+        acc = fold(x_local, w_local, dim, (lo, hi), init)
+        if rank < world - 1:
+            dist.send(acc, dst=rank + 1, group=group)
+        else:
+            parts.append(acc)
+    result = finish(parts) if rank == world - 1 else None
+    return result
+
+
+def gpu_chain_ops(tt, x_local, w_local, dim: int):
+    """The (fold, finish, n_out, new_acc) of chain_mul_sum on this package's
+    CUDA path: tt.mul_fold over a tile range, and tt_sum of the concatenated
+    accumulators viewed with fold_shape (one external tile along dim)."""
+    import torch
+    s = x_local.session()
+    fshape = tt.fold_shape(x_local.shape(), w_local.shape() if w_local is not None else None, dim)
+
+    def fold(x, w, d, rng, init):
+        return tt.mul_fold(x, w, d, out_range=rng, init=init)[0]
+
+    def finish(parts):
+        acc = parts if isinstance(parts, torch.Tensor) else torch.cat(parts, dim=0)
+        return tt.tt_sum(tt.TileTensor(fshape, acc, s), dim)
+
+    return fold, finish, fshape.tile_count(), s.empty_tiles
+
+
 def local_result_tile_range(x_plan: ShardPlan, result_shape: TileTensorShape):
     """Tile rows [lo, hi) of the GLOBAL result that this rank's sharded result
     holds (row-major external order, shard_dim outermost-relative slab)."""
@@ -122,4 +185,4 @@ def local_result_tile_range(x_plan: ShardPlan, result_shape: TileTensorShape):
 
 
 __all__ = ["ShardPlan", "plan", "operand_plan", "allreduce_partial", "broadcast_operand",
-           "sharded_mul_sum", "local_result_tile_range"]
+           "sharded_mul_sum", "chain_mul_sum", "gpu_chain_ops", "local_result_tile_range"]

@@ -509,6 +509,37 @@ def unpack(t: TileTensor) -> np.ndarray:
 
 # result tile counts by (op, operand shapes, dim): sizing an output costs a
 # shape-rule evaluation through the C-ABI, which dominates small ops' host time
+def fold_shape(a: TileTensorShape, b: Optional[TileTensorShape], dim: int) -> TileTensorShape:
+    """Shape of tt_mul_fold's accumulated tiles: the product (a alone when b
+    is None) with `dim` reduced to one external tile."""
+    out = CShape()
+    _check(lib().tt_fold_shape(ctypes.byref(a.to_c()), ctypes.byref(b.to_c()) if b else None,
+                               int(dim), ctypes.byref(out)))
+    return TileTensorShape.from_c(out)
+
+
+def mul_fold(a: TileTensor, b: Optional[TileTensor], dim: int, out_range=None, init=None):
+    """Partial left fold of tt_sum(tt_mul(a, b), dim) over output tiles
+    out_range = (begin, end) (default: all), continuing from `init` (device
+    tiles [end - begin, s]) when given -- the building block of exact
+    cross-GPU chains (sharding.chain_mul_sum).  Returns (tiles, chain)."""
+    s = a.session() if b is None else _same_session(a, b)
+    fs = fold_shape(a.shape(), b.shape() if b is not None else None, dim)
+    n_out = fs.tile_count()
+    begin, end = (0, n_out) if out_range is None else (int(out_range[0]), int(out_range[1]))
+    acc = s.empty_tiles(max(end - begin, 0))
+    chain = ctypes.c_int64()
+    if init is not None and tuple(init.shape) != (end - begin, s.slot_count()):
+        raise ValueError("init must hold one tile per output tile of the range")
+    _check(lib().tt_mul_fold(s.handle, ctypes.byref(a.shape().to_c()), _ptr(a.data()),
+                             a.chain_index(),
+                             ctypes.byref(b.shape().to_c()) if b is not None else None,
+                             _ptr(b.data()) if b is not None else ctypes.c_void_p(0),
+                             b.chain_index() if b is not None else 0, int(dim), begin, end,
+                             _ptr(init), _ptr(acc), ctypes.byref(chain)))
+    return acc, chain.value
+
+
 _RESULT_TILES: dict = {}
 
 

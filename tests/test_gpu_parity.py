@@ -9,6 +9,7 @@ import random
 
 import numpy as np
 import pytest
+import torch
 
 import paper_2011_01805_b200 as tt
 from paper_2011_01805_b200 import DimSpec, TileTensor, TileTensorShape, parse_shape, format_shape
@@ -427,3 +428,49 @@ def test_rotate_all_kernel_forms(gpu):
             got = tt.tiles_rotate(S, tiles, off)
             want = np.roll(tiles, -r, axis=1)
             assert_bitwise(got.detach().cpu().numpy(), want, f"rotate s={s} off={off}")
+
+
+def test_fold_chain_matches_single_pass(gpu, oracle):
+    """tt_mul_fold continuing an accumulator (the exact cross-GPU chain of
+    sharding.chain_mul_sum, run here as slabs on one GPU): slab 0 folded from
+    its first product, slab 1 from slab 0's accumulators in chunks, then the
+    in-tile schedule once -- bit-identical to tt_mul_sum on the whole tensor,
+    with the same counters in total."""
+    nrng = np.random.default_rng(4242)
+    for gx, gw, s in [("[64/4,8/2,6/2]", "[*/4,8/2,6/2]", 16),
+                      ("[256/16,64/32,32/32]", "[*/16,64/32,32/32]", 16384),
+                      ("[96/16,32/32,16/16]", "[96/16,32/32,16/16]", 8192)]:
+        S = session(s)
+        sx, sw = parse_shape(gx), parse_shape(gw)
+        xd = nrng.uniform(-1, 1, size=sx.tensor_extents())
+        wd = nrng.uniform(-1, 1, size=sw.tensor_extents())
+        X, W = tt.pack(xd, sx, S), tt.pack(wd, sw, S)
+        S.reset_counters()
+        want = tt.tt_mul_sum(X, W, 1)
+        c_want = S.cost_report()
+        w_shared = sw.dim(0).n == 1
+        S.reset_counters()
+        parts, init = [], None
+        for p in (tt_shard(sx, 2, 0), tt_shard(sx, 2, 1)):
+            Xs = tt.pack(xd[p[1]], p[0], S)
+            Ws = W if w_shared else tt.pack(wd[p[1]], p[0], S)
+            fs = tt.fold_shape(p[0], Ws.shape(), 1)
+            n_out = fs.tile_count()
+            cuts = [0, n_out // 3, n_out]
+            chunks = [tt.mul_fold(Xs, Ws, 1, (lo, hi), None if init is None else init[lo:hi])[0]
+                      for lo, hi in zip(cuts, cuts[1:])]
+            init = torch.cat(chunks)
+        got = tt.tt_sum(tt.TileTensor(fs, init, S), 1)
+        assert got.shape() == want.shape()
+        assert_bitwise(got.tiles(), want.tiles(), f"fold chain {gx}")
+        c = S.cost_report()
+        assert (c.additions, c.multiplications, c.rotations) == \
+            (c_want.additions, c_want.multiplications, c_want.rotations)
+    with pytest.raises(tt.ShapeError):
+        tt.mul_fold(X, W, 9)
+
+
+def tt_shard(shape, world, rank):
+    from paper_2011_01805_b200 import sharding
+    p = sharding.plan(shape, 1, world, rank)
+    return p.local_shape, p.dense_slices()

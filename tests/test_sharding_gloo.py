@@ -104,3 +104,69 @@ def test_plan_covers_every_tile():
         assert rows[0].start == 0 and rows[-1].stop == shape.dim(0).n
         for a, b in zip(rows, rows[1:]):
             assert a.stop == b.start
+
+
+def _chain_worker(rank, world, port, out_dir):
+    """chain_mul_sum over gloo: the fold is a numpy left fold (acc = P0, then
+    acc + P_l in order; each np op is one correctly rounded IEEE operation,
+    like the GPU kernel's __dadd_rn / __dmul_rn), the finish is the oracle's
+    tt_sum on the accumulated tiles viewed with fold_shape."""
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle_lib import Oracle
+    from paper_2011_01805_b200 import configs, fold_shape, parse_shape, sharding
+    oracle = Oracle()
+    sx, sw = parse_shape(GLOBAL_X), parse_shape(GLOBAL_W)
+    plan = sharding.plan(sx, 1, world, rank)
+    xd = configs.uniform(64 * 8 * 6, 21, -1, 1).reshape(64, 8, 6)[plan.dense_slices()]
+    wd = configs.uniform(8 * 6, 22, -1, 1).reshape(1, 8, 6)
+    tx = oracle.pack(xd, plan.local_shape, S)
+    tw = oracle.pack(wd, sw, S)
+    n_o = 4 * 3
+    fshape = fold_shape(sx, sw, 1)
+
+    def fold(x, w, dim, rng, init):
+        lo, hi = rng
+        xs = x.reshape(-1, n_o, S)[:, lo:hi]
+        ws = w.reshape(n_o, S)[lo:hi]
+        if init is None:
+            acc, start = xs[0] * ws, 1
+        else:
+            acc, start = init.numpy().copy(), 0
+        for l in range(start, xs.shape[0]):
+            acc = acc + xs[l] * ws
+        return torch.from_numpy(np.ascontiguousarray(acc))
+
+    def finish(parts):
+        acc = np.concatenate([p.numpy() for p in parts])
+        so, out, _ = oracle.sum(fshape, acc, S, 1)
+        return out
+
+    res = sharding.chain_mul_sum(tx, tw, 1, plan, fold, finish, n_o,
+                                 lambda k: torch.empty((k, S), dtype=torch.float64), chunks=5)
+    if rank == world - 1:
+        np.save(Path(out_dir) / "chain.npy", res)
+    else:
+        assert res is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_chain_is_bitwise_exact(tmp_path, oracle, world):
+    """The exact cross-rank sum: ranks continue each other's left-fold
+    accumulators in chunks, so the sum over the sharded dim equals the
+    single-process oracle bit for bit (the all-reduce path only to 1e-12)."""
+    mp.start_processes(_chain_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    from paper_2011_01805_b200 import configs, parse_shape
+    sx, sw = parse_shape(GLOBAL_X), parse_shape(GLOBAL_W)
+    xd = configs.uniform(64 * 8 * 6, 21, -1, 1).reshape(64, 8, 6)
+    wd = configs.uniform(8 * 6, 22, -1, 1).reshape(1, 8, 6)
+    tx, tw = oracle.pack(xd, sx, S), oracle.pack(wd, sw, S)
+    so, want, _ = oracle.mul_sum(sx, tx, sw, tw, S, 1)
+    got = np.load(tmp_path / "chain.npy")
+    assert got.shape == want.shape
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
