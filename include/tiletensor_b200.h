@@ -122,7 +122,10 @@ int64_t tt_session_max_chain_index(const tt_session* s);
 int tt_session_device(const tt_session* s);
 /* Run subsequent ops on an external stream (e.g. torch's current stream; NULL
  * is the legacy default stream).  tt_session_use_own_stream restores the
- * session's private stream. */
+ * session's private stream.  A session's ops share its device scratch (the
+ * split-fold target, batch-packed layer tables): ops of ONE session issued on
+ * different streams must be ordered by the caller (events); separate
+ * sessions are independent. */
 int tt_session_set_stream(tt_session* s, void* cuda_stream);
 int tt_session_use_own_stream(tt_session* s);
 void* tt_session_stream(const tt_session* s);
