@@ -525,6 +525,17 @@ def bench_matmul(tt, configs, S, stream, hbm_peak, reps):
     chain()
     torch.cuda.synchronize()
     t = time_events(chain, reps, stream)
+    # the same chain captured once into a CUDA graph (no host launch cost between kernels)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            chain()
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        chain()
+    t_graph = time_events(g.replay, reps, stream)
     tile = 8192 * 8
     # unique operand tiles + out tiles of both stages
     alg = (1536 + 768 + 512 + 512 + 1024 + 512 + 512) * tile
@@ -536,6 +547,7 @@ def bench_matmul(tt, configs, S, stream, hbm_peak, reps):
     fp64_ops = 2 * prod_tiles * 8192
     return {"matmul_c3b": {"ms": t * 1e3, "GB/s": alg / t / 1e9, "frac": alg / t / 1e9 / hbm_peak,
                            "tile_slots_per_s": prod_tiles * 8192 / t, "alg_bytes": alg,
+                           "graph_replay_ms": t_graph * 1e3,
                            "fp64_tops": fp64_ops / t / 1e12,
                            "fp64_frac": fp64_ops / t / FP64_PEAK_OPS,
                            "fp64_peak_source": "measured DMUL+DADD issue rate, 18.34e12 thread-ops/s",
