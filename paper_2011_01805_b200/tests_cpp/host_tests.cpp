@@ -108,24 +108,6 @@ static void fuzz_unknown_regions(TileTensor& t, std::uint64_t seed) {
   }
 }
 
-static DenseTensor dense_elementwise(const DenseTensor& a, const DenseTensor& b, OpKind op) {
-  std::vector<std::int64_t> os(a.rank());
-  for (std::size_t i = 0; i < a.rank(); ++i) os[i] = std::max(a.extent(i), b.extent(i));
-  DenseTensor out = DenseTensor::zeros(os);
-  std::vector<std::int64_t> idx(os.size(), 0), ia(os.size()), ib(os.size());
-  for (std::size_t f = 0; f < out.size(); ++f) {
-    for (std::size_t i = 0; i < os.size(); ++i) {
-      ia[i] = idx[i] % a.extent(i);
-      ib[i] = idx[i] % b.extent(i);
-    }
-    out.values()[f] = op == OpKind::add ? a.at(ia) + b.at(ib) : a.at(ia) * b.at(ib);
-    for (std::size_t i = os.size(); i-- > 0;) {
-      if (++idx[i] < os[i]) break;
-      idx[i] = 0;
-    }
-  }
-  return out;
-}
 
 // ---- test_shape.cpp ---------------------------------------------------------
 static void shapes() {
@@ -420,6 +402,13 @@ static void linalg() {
   const TileTensor s2 = matmul_a(tm2, s1);
   CHECK(max_rel_diff(unpack(s2).reshape({2, 3}), dense_matmul(m2, dense_matmul(m1, x))) < 1e-9);
   CHECK_THROWS_AS(matvec_a(tm1, tx), ShapeError);  // rank-3 operands
+  // dense oracle routes (dense.hpp:107-177)
+  const DenseTensor p = random_tensor({4, 5}, rng), q = random_tensor({5, 3}, rng);
+  CHECK(max_rel_diff(dense_matmul_via_broadcast(p, q), dense_matmul(p, q)) < 1e-12);
+  const DenseTensor row = random_tensor({1, 5}, rng);
+  const DenseTensor sum = dense_elementwise(p, row, OpKind::add);
+  CHECK(sum.shape() == p.shape() && sum(2, 3) == p(2, 3) + row(0, 3));
+  CHECK_THROWS_AS(dense_elementwise(p, q, OpKind::mul), ShapeError);
 }
 
 // chain of dense matrix-vector products (the pipeline's oracle)
