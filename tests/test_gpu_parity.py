@@ -474,3 +474,94 @@ def tt_shard(shape, world, rank):
     from paper_2011_01805_b200 import sharding
     p = sharding.plan(shape, 1, world, rank)
     return p.local_shape, p.dense_slices()
+
+
+def _big_shape(rng, s, rank):
+    """A random pack shape over a large slot count with few tiles."""
+    from paper_2011_01805_b200 import DimSpec, TileTensorShape
+    t = [1] * rank
+    rem = s
+    for i in range(rank - 1):
+        t[i] = rng.choice([x for x in (1, 2, 4, 8, 16, 32, 64, 128) if x <= rem])
+        rem //= t[i]
+    t[rank - 1] = rem
+    dims = []
+    for i in range(rank):
+        pick = rng.randint(0, 4)
+        if pick == 0:
+            dims.append(DimSpec(1, t[i], t[i]))
+        elif pick == 1 and t[i] > 1:
+            dims.append(DimSpec(1, rng.randint(1, t[i]), t[i]))
+        else:
+            dims.append(DimSpec(rng.randint(1, 3 * t[i]), 1, t[i]))
+    return TileTensorShape(dims)
+
+
+def test_random_large_slot_counts(gpu, oracle):
+    """Random shapes over 512..16384-slot tiles (the chunked elementwise /
+    clean / rotate kernels, TMA pack, window and register tree passes, split
+    folds): pack, elementwise, every sum variant, fused product sums,
+    clean_unknowns and replicate_dim -- all bitwise vs the oracle."""
+    rng = random.Random(8128)
+    nrng = np.random.default_rng(8128)
+    cases = 0
+    seen = {"ew": 0, "sum": 0, "clean": 0, "replicate": 0, "mul_sum": 0}
+    while cases < 40:
+        s = rng.choice([512, 1024, 2048, 4096, 8192, 16384])
+        S = session(s)
+        sa = _big_shape(rng, s, rng.randint(2, 3))
+        if sa.tile_count() > 64:
+            continue
+        dense = nrng.uniform(-2, 2, size=sa.tensor_extents())
+        A = tt.pack(dense, sa, S)
+        assert_bitwise(A.tiles(), oracle.pack(dense, sa, s), f"pack {format_shape(sa)}")
+        sb = partner_shape(rng, sa)
+        tb = nrng.uniform(-2, 2, size=(sb.tile_count(), s))
+        B = TileTensor(sb, tb, S)
+        ta = A.tiles()
+        try:
+            oracle.elementwise_result_shape(sa, sb, 1)
+            ok = True
+        except Exception:
+            ok = False
+        if ok:
+            for op in (tt.OpKind.add, tt.OpKind.mul):
+                ws, wt, _ = oracle.elementwise(int(op), sa, ta, sb, tb, s)
+                got = tt.tt_elementwise(A, B, op)
+                assert_bitwise(got.tiles(), wt, f"ew {format_shape(sa)} {format_shape(sb)}")
+                seen["ew"] += 1
+        for dim in range(1, sa.rank() + 1):
+            for variant in (None, tt.SumVariant.left_to_right):
+                v = -1 if variant is None else int(variant)
+                try:
+                    ws, wt, wc = oracle.sum(sa, ta, s, dim, v)
+                except Exception:
+                    continue
+                S.reset_counters()
+                got = tt.tt_sum(A, dim, variant)
+                assert got.shape() == ws
+                assert_bitwise(got.tiles(), wt, f"sum {format_shape(sa)} dim {dim} v {v}")
+                assert same_cost(S.cost_report(), wc)
+                seen["sum"] += 1
+                if got.shape().has_unknown():
+                    cs, ct, _ = oracle.clean_unknowns(ws, wt, s)
+                    C = tt.clean_unknowns(got)
+                    assert_bitwise(C.tiles(), ct, f"clean {format_shape(ws)}")
+                    seen["clean"] += 1
+                    d = got.shape().dim(dim - 1)
+                    if d.n == 1 and d.t > 1:
+                        rs, rt, _ = oracle.replicate_dim(cs, ct, s, dim)
+                        R = tt.replicate_dim(C, dim)
+                        assert_bitwise(R.tiles(), rt, f"replicate {format_shape(cs)} dim {dim}")
+                        seen["replicate"] += 1
+            if ok:
+                try:
+                    ws, wt, wc = oracle.mul_sum(sa, ta, sb, tb, s, dim)
+                except Exception:
+                    continue
+                got = tt.tt_mul_sum(A, B, dim)
+                assert_bitwise(got.tiles(), wt, f"mul_sum {format_shape(sa)} x {format_shape(sb)} {dim}")
+                seen["mul_sum"] += 1
+        cases += 1
+    print(seen)
+    assert seen["sum"] >= 40 and seen["clean"] >= 5 and seen["replicate"] >= 3 and seen["mul_sum"] >= 10
