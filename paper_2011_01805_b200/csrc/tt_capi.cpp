@@ -827,7 +827,22 @@ int tt_batch_affine(tt_session* s, const double* in, int64_t n_in, int64_t n_out
       check_cuda(cudaMemcpyAsync(d_w, w, b_w, cudaMemcpyHostToDevice, c.stream), "layer upload");
     }
     check_cuda(cudaMemcpyAsync(d_bias, bias, b_bias, cudaMemcpyHostToDevice, c.stream), "layer upload");
-    launch_batch_affine(c, in, s->slots, n_out, d_rp, d_src, d_w, d_bias, out);
+    // largest block (<= 8) of consecutive rows sharing one source list
+    int block = 1;
+    for (int cand : {8, 5, 4, 2}) {
+      bool ok = true;
+      for (int64_t o0 = 0; o0 < n_out && ok; o0 += cand) {
+        const int64_t len = row_ptr[o0 + 1] - row_ptr[o0];
+        for (int64_t r = o0 + 1; r < std::min<int64_t>(o0 + cand, n_out) && ok; ++r)
+          ok = row_ptr[r + 1] - row_ptr[r] == len &&
+               std::equal(src + row_ptr[r], src + row_ptr[r] + len, src + row_ptr[o0]);
+      }
+      if (ok) {
+        block = cand;
+        break;
+      }
+    }
+    launch_batch_affine(c, in, s->slots, n_out, d_rp, d_src, d_w, d_bias, out, block);
   });
 }
 

@@ -2284,6 +2284,108 @@ __global__ void __launch_bounds__(256) fold_range_kernel(const __grid_constant__
   }
 }
 
+// Blocked form: `ob` consecutive output tiles that share one tap source list
+// (every row of an fc layer; the filters of one window of a conv layer) are
+// folded by one thread per slot pair: each input pair is loaded once and
+// feeds ob accumulators (bias first, then + w * x in tap order -- the same
+// association per output as batch_affine_kernel).
+template <int OBMAX, int V>  // V = slots per thread (2: double2, 1: scalar for more threads)
+__global__ void __launch_bounds__(256) batch_affine_blocked_kernel(
+    const double* __restrict__ in, int64_t s, int64_t n_out, int ob, uint64_t total,
+    const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ src,
+    const double* __restrict__ w, const double* __restrict__ bias, double* __restrict__ out,
+    FastDiv64 pairs_div) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t blk = fdiv(i, pairs_div);
+    const int64_t j = static_cast<int64_t>(i - blk * pairs_div.d) * V;
+    const int64_t o0 = static_cast<int64_t>(blk) * ob;
+    const int64_t k0 = row_ptr[o0], taps = row_ptr[o0 + 1] - k0;
+    double2 acc[OBMAX];
+    int64_t wk[OBMAX];
+#pragma unroll
+    for (int r = 0; r < OBMAX; ++r) {
+      if (r < ob && o0 + r < n_out) {
+        acc[r] = make_double2(bias[o0 + r], bias[o0 + r]);
+        wk[r] = row_ptr[o0 + r];
+      }
+    }
+    for (int64_t t = 0; t < taps; ++t) {
+      const double* px = in + src[k0 + t] * s + j;
+      const double2 x = V == 2 ? __ldg(reinterpret_cast<const double2*>(px)) : make_double2(__ldg(px), 0.0);
+#pragma unroll
+      for (int r = 0; r < OBMAX; ++r) {
+        if (r < ob && o0 + r < n_out) {
+          const double wv = w[wk[r] + t];
+          acc[r].x = dadd(acc[r].x, dmul(wv, x.x));
+          if (V == 2) acc[r].y = dadd(acc[r].y, dmul(wv, x.y));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < OBMAX; ++r) {
+      if (r < ob && o0 + r < n_out) {
+        if (V == 2)
+          *reinterpret_cast<double2*>(out + (o0 + r) * s + j) = acc[r];
+        else
+          out[(o0 + r) * s + j] = acc[r].x;
+      }
+    }
+  }
+}
+
+// Shared-memory form of the blocked fold (s % 512 == 0): a work item is one
+// row block x 256 slot pairs (one CTA); weights and source indices for up to
+// kBaTaps taps are staged per CTA, then each thread folds its pair with one
+// 16-byte input load and 4 vector shared loads of weights per tap.
+constexpr int kBaTaps = 64;
+__global__ void __launch_bounds__(256) batch_affine_smem_kernel(
+    const double* __restrict__ in, int64_t s, int64_t n_out, int ob, uint64_t items,
+    const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ src,
+    const double* __restrict__ w, const double* __restrict__ bias, double* __restrict__ out,
+    FastDiv64 chunks_div) {
+  __shared__ __align__(16) double ws[kBaTaps][8];
+  __shared__ int64_t ss[kBaTaps];
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const uint64_t blk = fdiv(item, chunks_div);
+    const int64_t j = (static_cast<int64_t>(item - blk * chunks_div.d) * 256 + threadIdx.x) * 2;
+    const int64_t o0 = static_cast<int64_t>(blk) * ob;
+    const int nr = static_cast<int>(n_out - o0 < ob ? n_out - o0 : ob);
+    const int64_t k0 = row_ptr[o0], taps = row_ptr[o0 + 1] - k0;
+    double2 acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const double bv = r < nr ? bias[o0 + r] : 0.0;
+      acc[r] = make_double2(bv, bv);
+    }
+    for (int64_t t0 = 0; t0 < taps; t0 += kBaTaps) {
+      const int nt = static_cast<int>(taps - t0 < kBaTaps ? taps - t0 : kBaTaps);
+      __syncthreads();  // previous chunk consumed
+      for (int e = threadIdx.x; e < nt * 8; e += 256) {
+        const int t = e >> 3, r = e & 7;
+        ws[t][r] = r < nr ? w[row_ptr[o0 + r] + t0 + t] : 0.0;
+      }
+      for (int t = threadIdx.x; t < nt; t += 256) ss[t] = src[k0 + t0 + t];
+      __syncthreads();
+      for (int t = 0; t < nt; ++t) {
+        const double2 x = __ldg(reinterpret_cast<const double2*>(in + ss[t] * s + j));
+        const double2* wv = reinterpret_cast<const double2*>(ws[t]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 w2 = wv[q];
+          acc[2 * q].x = dadd(acc[2 * q].x, dmul(w2.x, x.x));
+          acc[2 * q].y = dadd(acc[2 * q].y, dmul(w2.x, x.y));
+          acc[2 * q + 1].x = dadd(acc[2 * q + 1].x, dmul(w2.y, x.x));
+          acc[2 * q + 1].y = dadd(acc[2 * q + 1].y, dmul(w2.y, x.y));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r < nr) *reinterpret_cast<double2*>(out + (o0 + r) * s + j) = acc[r];
+  }
+}
+
 // ---- synthetic input generator (== or_fill_uniform in oracle/tt_oracle.c) ------------
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -2497,9 +2599,38 @@ void launch_fold_range(const LaunchCtx& c, const FoldRange& fr, int64_t s, int64
 
 void launch_batch_affine(const LaunchCtx& c, const double* in, int64_t s, int64_t n_out,
                          const int64_t* row_ptr, const int64_t* src, const double* w,
-                         const double* bias, double* out) {
+                         const double* bias, double* out, int block) {
   const uint64_t total = static_cast<uint64_t>(s) * n_out;
   if (total == 0) return;
+  if (block > 1 && s % 512 == 0 && aligned16(in) && aligned16(out)) {
+    // every CTA works inside one row block: the block's weights for a run of
+    // taps are staged in shared memory once per CTA (tap-major, 8 per tap)
+    const uint64_t blocks = static_cast<uint64_t>((n_out + block - 1) / block);
+    const uint64_t items = blocks * static_cast<uint64_t>(s / 512);
+    const int grid = grid_for(c, (const void*)batch_affine_smem_kernel, 256, 0, static_cast<int64_t>(items));
+    batch_affine_smem_kernel<<<grid, 256, 0, c.stream>>>(in, s, n_out, block, items, row_ptr, src, w,
+                                                         bias, out, make_div64(static_cast<uint64_t>(s / 512)));
+    post_launch(c, "batch affine smem kernel");
+    return;
+  }
+  if (block > 1) {
+    const uint64_t blocks = static_cast<uint64_t>((n_out + block - 1) / block);
+    const bool pair = s % 2 == 0 && aligned16(in) && aligned16(out);
+    const uint64_t per = static_cast<uint64_t>(pair ? s / 2 : s);
+    const uint64_t work = blocks * per;
+    const int64_t nb = static_cast<int64_t>((work + 255) / 256);
+    if (pair) {
+      const int grid = grid_for(c, (const void*)batch_affine_blocked_kernel<8, 2>, 256, 0, nb);
+      batch_affine_blocked_kernel<8, 2><<<grid, 256, 0, c.stream>>>(in, s, n_out, block, work, row_ptr,
+                                                                    src, w, bias, out, make_div64(per));
+    } else {
+      const int grid = grid_for(c, (const void*)batch_affine_blocked_kernel<8, 1>, 256, 0, nb);
+      batch_affine_blocked_kernel<8, 1><<<grid, 256, 0, c.stream>>>(in, s, n_out, block, work, row_ptr,
+                                                                    src, w, bias, out, make_div64(per));
+    }
+    post_launch(c, "batch affine blocked kernel");
+    return;
+  }
   const int grid = grid_for(c, (const void*)batch_affine_kernel, 256, 0, (total + 255) / 256);
   batch_affine_kernel<<<grid, 256, 0, c.stream>>>(in, s, total, row_ptr, src, w, bias, out,
                                                    make_div64(static_cast<uint64_t>(s)));

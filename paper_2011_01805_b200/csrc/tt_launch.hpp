@@ -71,9 +71,11 @@ void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shap
 // out[i] = a[i] (op) b[i] over `count` slots; op 2 = a * mask (same as mul)
 // out[o] = bias[o] (+) w[k] (*) in[src[k]] over k in [row_ptr[o], row_ptr[o+1]),
 // left fold per slot; the CSR arrays are device pointers.
+// block > 1: consecutive groups of `block` rows share their source list (the
+// blocked kernel loads each input once for the whole group).
 void launch_batch_affine(const LaunchCtx& c, const double* in, int64_t s, int64_t n_out,
                          const int64_t* row_ptr, const int64_t* src, const double* w,
-                         const double* bias, double* out);
+                         const double* bias, double* out, int block);
 // Fold of a product over its summed dim for the output tiles [o0, o1) of the
 // result grid `gext` (row-major, summed dim extent 1): acc = init (when
 // given) then acc = acc + A[l]*B[l] (B optional) for l in [first, first+count)

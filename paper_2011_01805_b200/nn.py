@@ -325,6 +325,10 @@ def nn_forward(net: NetworkSpec, batch: np.ndarray) -> np.ndarray:
 # ---- tiled inference ----------------------------------------------------------------
 
 
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
 @dataclass
 class InferResult:  # nn.hpp:260-263
     logits: np.ndarray
@@ -353,10 +357,11 @@ def infer_batch_packed(net: NetworkSpec, batch: np.ndarray, session: tt.Session)
     samples; each conv / fc layer is ONE device pass (tt_batch_affine) that
     folds bias + w * x in the reference's order; zero rotations."""
     before = session.cost_report()
-    batch = np.asarray(batch, dtype=np.float64)
-    n = batch.shape[1]
+    if not _is_torch(batch):  # a device-resident torch batch is packed in place (no host copy)
+        batch = np.asarray(batch, dtype=np.float64)
+    n = int(batch.shape[1])
     s = session.slot_count()
-    packed = tt.pack(batch, TileTensorShape([DimSpec(batch.shape[0], 1, 1), DimSpec(n, 1, s)]),
+    packed = tt.pack(batch, TileTensorShape([DimSpec(int(batch.shape[0]), 1, 1), DimSpec(n, 1, s)]),
                      session)
     data, chain = packed.data(), packed.chain_index()
     for layer_no, layer in enumerate(net.layers, start=1):
@@ -410,16 +415,17 @@ def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],
     t1, t2, t3 = (int(x) for x in tile)
     if t1 * t2 * t3 != session.slot_count():
         raise ShapeError("tile extents must multiply to the slot count")
-    batch = np.asarray(batch, dtype=np.float64)
-    if batch.ndim != 2:
+    if len(batch.shape) != 2:
         raise ShapeError("batch must be [features, samples]")
-    n = batch.shape[1]
+    n = int(batch.shape[1])
     if n > t3:
         raise ShapeError("batch size exceeds the batch tile extent t3")
-    if batch.shape[0] != net.input_size():
+    if int(batch.shape[0]) != net.input_size():
         raise ShapeError("batch feature size mismatch")
     if t1 == 1 and t2 == 1:
         return infer_batch_packed(net, batch, session)
+    # the tiled path lays the batch out on the host (im2col, as the reference does)
+    batch = np.asarray(batch.detach().cpu() if _is_torch(batch) else batch, dtype=np.float64)
     before = session.cost_report()
 
     def shape3(a, b, c):
