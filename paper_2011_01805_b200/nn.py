@@ -406,24 +406,36 @@ def infer_batch_packed(net: NetworkSpec, batch: np.ndarray, session: tt.Session)
 
 
 def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],
-                     session: tt.Session) -> InferResult:
+                     session: tt.Session, lift_batch_limit: bool = False) -> InferResult:
     """nn.hpp:350-507: tile [t1, t2, t3], batch along the third dim.  A
     leading conv is folded client-side into a first-stage product (transposed
     im2col replicated per filter), fc stages alternate the two product forms
     with clean + replicate at even -> odd seams; t1 = t2 = 1 takes the
-    batch-packed path."""
+    batch-packed path.
+
+    lift_batch_limit (SURVEY 8f "n > t3 lifted"; the reference throws):
+    batches larger than t3 become several external tiles along the batch dim
+    (no rotation crosses samples, so each sample's logits equal a reference
+    run on its own t3-sized chunk bit for bit); the batch-packed path runs
+    chunks of s samples."""
     t1, t2, t3 = (int(x) for x in tile)
     if t1 * t2 * t3 != session.slot_count():
         raise ShapeError("tile extents must multiply to the slot count")
     if len(batch.shape) != 2:
         raise ShapeError("batch must be [features, samples]")
     n = int(batch.shape[1])
-    if n > t3:
+    if n > t3 and not lift_batch_limit:
         raise ShapeError("batch size exceeds the batch tile extent t3")
     if int(batch.shape[0]) != net.input_size():
         raise ShapeError("batch feature size mismatch")
     if t1 == 1 and t2 == 1:
-        return infer_batch_packed(net, batch, session)
+        if n <= t3:
+            return infer_batch_packed(net, batch, session)
+        parts = [infer_batch_packed(net, batch[:, k:k + t3], session) for k in range(0, n, t3)]
+        total = CostReport()
+        for r in parts:
+            total = CostReport(*(getattr(total, f) + getattr(r.cost, f) for f in tt._COST_FIELDS))
+        return InferResult(np.concatenate([r.logits for r in parts], axis=1), total)
     # the tiled path lays the batch out on the host (im2col, as the reference does)
     batch = np.asarray(batch.detach().cpu() if _is_torch(batch) else batch, dtype=np.float64)
     before = session.cost_report()

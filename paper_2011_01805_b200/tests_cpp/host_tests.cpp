@@ -547,6 +547,19 @@ static void nn_suite() {
       ++runs;
     }
   CHECK(runs == 28);
+  {  // lifted batch limit: n > t3 equals per-chunk runs
+    const DenseTensor batch = random_tensor({36, 21}, rng, -1, 1);
+    Session session(64, 8);
+    CHECK_THROWS_AS(cryptonets_infer(net, batch, {2, 4, 8}, session), ShapeError);
+    const auto all = cryptonets_infer(net, batch, {2, 4, 8}, session, true);
+    CHECK(all.logits.extent(1) == 21);
+    CHECK(max_rel_diff(all.logits, nn_forward(net, batch)) < 1e-6);
+    const auto bp = cryptonets_infer(net, batch, {1, 1, 64}, session, true);
+    CHECK(max_rel_diff(bp.logits, nn_forward(net, batch)) < 1e-6);
+    const auto big = random_tensor({36, 150}, rng, -1, 1);
+    const auto bp2 = cryptonets_infer(net, big, {1, 1, 64}, session, true);
+    CHECK(bp2.logits.extent(1) == 150 && max_rel_diff(bp2.logits, nn_forward(net, big)) < 1e-6);
+  }
   {  // paper-scale counts for tile [32, 256, 1]
     const NetworkSpec cn = cryptonets_network(42);
     const DenseTensor batch = random_tensor({784, 1}, rng, -1, 1);

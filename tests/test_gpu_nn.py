@@ -103,3 +103,23 @@ def test_error_contracts(gpu):
     pooled = nn.parse_network("input h=4 w=4\nfc in=16 out=4\npool mean window=2\n", "", 1)
     with pytest.raises(tt.ShapeError):
         nn.cryptonets_infer(pooled, rng.uniform(size=(16, 1)), (2, 8, 1), tt.Session(16, 8))
+
+
+def test_lifted_batch_limit(gpu, ref):
+    """lift_batch_limit: a batch of n > t3 samples (several external batch
+    tiles; several s-sized chunks when batch packed) gives, sample for
+    sample, the reference's logits for t3-sized chunks, bit for bit."""
+    net = nn.parse_network(SMALL, "", 44)
+    rng = np.random.default_rng(4321)
+    for tile in ((2, 4, 8), (4, 2, 8), (1, 1, 64)):
+        s = tile[0] * tile[1] * tile[2]
+        t3 = tile[2]
+        n = 3 * t3 + 5
+        batch = rng.uniform(-1, 1, size=(36, n))
+        S = tt.Session(s, 8)
+        with pytest.raises(tt.ShapeError):
+            nn.cryptonets_infer(net, batch, tile, S)
+        got = nn.cryptonets_infer(net, batch, tile, S, lift_batch_limit=True)
+        want = np.concatenate([ref.nn_run(1, SMALL, 44, batch[:, k:k + t3], tile, s, 8)[0]
+                               for k in range(0, n, t3)], axis=1)
+        assert _same(got.logits, want), tile
