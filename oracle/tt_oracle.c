@@ -90,7 +90,10 @@ int or_elementwise_result_shape(const tt_shape* a, const tt_shape* b, int op, tt
     const tt_dim* da = &a->dims[i];
     const tt_dim* db = &b->dims[i];
     if (da->t != db->t) return OR_SHAPE;
-    if (da->interleaved != db->interleaved) return OR_SHAPE; /* builder's `~` rule */
+    /* builder's `~` rule: an interleaved dim combines
+     * with an interleaved one or with a fully replicated (broadcast) one */
+    if (da->interleaved != db->interleaved && !fully_replicated(da) && !fully_replicated(db))
+      return OR_SHAPE;
     const int compatible = da->n == db->n || (da->n == 1 && fully_replicated(da)) ||
                            (db->n == 1 && fully_replicated(db));
     if (!compatible) return OR_SHAPE;
@@ -99,7 +102,7 @@ int or_elementwise_result_shape(const tt_shape* a, const tt_shape* b, int op, tt
     r.t = da->t;
     r.n = da->n > db->n ? da->n : db->n;
     r.d = da->d < db->d ? da->d : db->d;
-    r.interleaved = da->interleaved;
+    r.interleaved = (da->interleaved || db->interleaved) && r.d == 1;
     int unk = da->unknown || db->unknown || used_of(da) != used_of(db);
     if (op == TT_OP_MUL && unk) {
       const int64_t used_r = r.n * r.d;

@@ -565,3 +565,62 @@ def test_random_large_slot_counts(gpu, oracle):
         cases += 1
     print(seen)
     assert seen["sum"] >= 40 and seen["clean"] >= 5 and seen["replicate"] >= 3 and seen["mul_sum"] >= 10
+
+
+def test_interleaved_random(gpu, oracle):
+    """The builder's `~` tiling (not in the reference, so
+    checked against the C restatement's own definition): random shapes with
+    interleaved dims through pack, unpack, elementwise with `~` / broadcast
+    partners, sums over every dim (clean first when '?'), bit for bit."""
+    from paper_2011_01805_b200 import DimSpec, TileTensorShape
+    rng = random.Random(777)
+    nrng = np.random.default_rng(777)
+    done = 0
+    while done < 60:
+        s = rng.choice([16, 32, 64, 512])
+        rank = rng.randint(1, 3)
+        t = [1] * rank
+        rem = s
+        for i in range(rank - 1):
+            t[i] = rng.choice([x for x in (1, 2, 4, 8) if x <= rem])
+            rem //= t[i]
+        t[-1] = rem
+        dims = [DimSpec(rng.randint(1, 3 * ti), 1, ti, False, rng.random() < 0.6) for ti in t]
+        try:
+            sa = TileTensorShape(dims)
+        except tt.ShapeError:
+            continue
+        S = session(s)
+        dense = nrng.uniform(-2, 2, size=sa.tensor_extents())
+        A = tt.pack(dense, sa, S)
+        assert_bitwise(A.tiles(), oracle.pack(dense, sa, s), f"pack {format_shape(sa)}")
+        assert_bitwise(tt.unpack(A), dense, f"unpack {format_shape(sa)}")
+        # partner: same interleaving or fully replicated per dim
+        pdims = [DimSpec(d.n, 1, d.t, False, d.interleaved) if rng.random() < 0.6
+                 else DimSpec(1, d.t, d.t) for d in sa.dims()]
+        sb = TileTensorShape(pdims)
+        tb = nrng.uniform(-2, 2, size=(sb.tile_count(), s))
+        ta = A.tiles()
+        for op in (tt.OpKind.add, tt.OpKind.mul):
+            try:
+                ws, wt, _ = oracle.elementwise(int(op), sa, ta, sb, tb, s)
+            except Exception:
+                with pytest.raises(tt.ShapeError):
+                    tt.tt_elementwise(A, TileTensor(sb, tb, S), op)
+                continue
+            got = tt.tt_elementwise(A, TileTensor(sb, tb, S), op)
+            assert got.shape() == ws
+            assert_bitwise(got.tiles(), wt, f"ew {format_shape(sa)} {format_shape(sb)}")
+        for dim in range(1, rank + 1):
+            try:
+                ws, wt, wc = oracle.sum(sa, ta, s, dim)
+            except Exception:
+                with pytest.raises((tt.ShapeError, ValueError)):
+                    tt.tt_sum(A, dim)
+                continue
+            S.reset_counters()
+            got = tt.tt_sum(A, dim)
+            assert got.shape() == ws
+            assert_bitwise(got.tiles(), wt, f"sum {format_shape(sa)} dim {dim}")
+            assert same_cost(S.cost_report(), wc)
+        done += 1
