@@ -624,3 +624,55 @@ def test_interleaved_random(gpu, oracle):
             assert_bitwise(got.tiles(), wt, f"sum {format_shape(sa)} dim {dim}")
             assert same_cost(S.cost_report(), wc)
         done += 1
+
+
+def test_relaxed_and_variants_random(gpu, oracle):
+    """Relaxed shapes (tile extents multiply to less than s; the remaining
+    slots are never touched by the reference's pack) and explicit sum
+    variants (left-to-right, right-to-left, power-of-two where legal) over
+    large tiles, including '?' boundary splits: bitwise vs the oracle."""
+    from paper_2011_01805_b200 import DimSpec, TileTensorShape
+    rng = random.Random(99)
+    nrng = np.random.default_rng(99)
+    seen = 0
+    while seen < 40:
+        s = rng.choice([64, 512, 4096])
+        rank = rng.randint(1, 3)
+        budget = s // rng.choice([1, 2, 4])
+        t = []
+        rem = budget
+        for i in range(rank - 1):
+            ti = rng.choice([x for x in (1, 2, 3, 4, 8) if x <= rem])
+            t.append(ti)
+            rem //= ti
+        t.append(max(1, rem))
+        dims = [DimSpec(rng.randint(1, 2 * ti + 1), 1, ti) for ti in t]
+        relaxed = int(np.prod(t)) != s
+        try:
+            sa = TileTensorShape(dims, relaxed)
+        except tt.ShapeError:
+            continue
+        if sa.tile_slots() > s:
+            continue
+        S = session(s)
+        dense = nrng.uniform(-2, 2, size=sa.tensor_extents())
+        A = tt.pack(dense, sa, S)
+        assert_bitwise(A.tiles(), oracle.pack(dense, sa, s), f"pack {format_shape(sa)} relaxed={relaxed}")
+        assert_bitwise(tt.unpack(A), dense, f"unpack {format_shape(sa)}")
+        ta = A.tiles()
+        for dim in range(1, rank + 1):
+            for variant in (tt.SumVariant.left_to_right, tt.SumVariant.right_to_left,
+                            tt.SumVariant.power_of_two):
+                try:
+                    ws, wt, wc = oracle.sum(sa, ta, s, dim, int(variant))
+                except Exception:
+                    continue
+                S.reset_counters()
+                got = tt.tt_sum(A, dim, variant)
+                assert got.shape() == ws
+                assert_bitwise(got.tiles(), wt, f"sum {format_shape(sa)} dim {dim} {variant}")
+                assert same_cost(S.cost_report(), wc)
+                if ws.has_unknown():
+                    cs, ct, _ = oracle.clean_unknowns(ws, wt, s)
+                    assert_bitwise(tt.clean_unknowns(got).tiles(), ct, f"clean {format_shape(ws)}")
+        seen += 1
