@@ -676,3 +676,40 @@ def test_relaxed_and_variants_random(gpu, oracle):
                     cs, ct, _ = oracle.clean_unknowns(ws, wt, s)
                     assert_bitwise(tt.clean_unknowns(got).tiles(), ct, f"clean {format_shape(ws)}")
         seen += 1
+
+
+def test_odd_and_tiny_slot_counts(gpu, oracle):
+    """s = 1, odd and non-power-of-two slot counts take the scalar fallbacks
+    of every vectorised kernel (pack, elementwise, clean, rotate, folds)."""
+    from paper_2011_01805_b200 import DimSpec, TileTensorShape
+    nrng = np.random.default_rng(135)
+    for s, texts in [(1, ["[5]", "[3,4]"]), (3, ["[7/3]", "[2,5/3]"]), (5, ["[11/5,2]"]),
+                     (6, ["[7/2,5/3]", "[4/3,*/2]"]), (7, ["[15/7]"]), (9, ["[10/3,4/3]"]),
+                     (97, ["[200/97]"]), (1000, ["[3/10,250/100]"])]:
+        S = session(s)
+        for text in texts:
+            sa = parse_shape(text)
+            dense = nrng.uniform(-2, 2, size=sa.tensor_extents())
+            A = tt.pack(dense, sa, S)
+            assert_bitwise(A.tiles(), oracle.pack(dense, sa, s), f"pack {text} s={s}")
+            assert_bitwise(tt.unpack(A), dense, f"unpack {text} s={s}")
+            ta = A.tiles()
+            for op in (tt.OpKind.add, tt.OpKind.mul):
+                ws, wt, _ = oracle.elementwise(int(op), sa, ta, sa, ta, s)
+                assert_bitwise(tt.tt_elementwise(A, A, op).tiles(), wt, f"ew {text} s={s}")
+            for dim in range(1, sa.rank() + 1):
+                ws, wt, wc = oracle.sum(sa, ta, s, dim)
+                S.reset_counters()
+                got = tt.tt_sum(A, dim)
+                assert_bitwise(got.tiles(), wt, f"sum {text} dim {dim} s={s}")
+                assert same_cost(S.cost_report(), wc)
+                ms, mt, _ = oracle.mul_sum(sa, ta, sa, ta, s, dim)
+                assert_bitwise(tt.tt_mul_sum(A, A, dim).tiles(), mt, f"mul_sum {text} {dim} s={s}")
+                if ws.has_unknown():
+                    cs, ct, _ = oracle.clean_unknowns(ws, wt, s)
+                    assert_bitwise(tt.clean_unknowns(got).tiles(), ct, f"clean {text} s={s}")
+            for off in (1, s // 2 + 1, -1):
+                r = ((off % s) + s) % s
+                want = np.roll(ta, -r, axis=1)
+                got = tt.tiles_rotate(S, ta, off)
+                assert_bitwise(got.detach().cpu().numpy(), want, f"rotate s={s} off={off}")
