@@ -597,7 +597,7 @@ def main():
     ap.add_argument("--skip-extra", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-pinned", type=int, default=1)
-    ap.add_argument("--cpu-slab-tiles", type=int, default=8)
+    ap.add_argument("--cpu-slab-tiles", type=int, default=48)  # ~10 s of reference CPU work
     ap.add_argument("--ref-slab-tiles", type=int, default=4)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
