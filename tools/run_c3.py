@@ -47,6 +47,43 @@ if "--time" in sys.argv:
         e1.record()
         torch.cuda.synchronize()
         print(f"  {name}: {e0.elapsed_time(e1) / n * 1e3:.1f} us")
+if "--timeline" in sys.argv:
+    # per-kernel durations and the idle gaps between them (CUPTI via the torch
+    # profiler): how much of the chain is launch / ramp rather than kernel time
+    from torch.profiler import ProfilerActivity, profile
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        r = chain()
+    g.replay()
+    torch.cuda.synchronize()
+    for mode in ("api", "graph"):
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(20):
+                if mode == "api":
+                    r = chain()
+                else:
+                    g.replay()
+            torch.cuda.synchronize()
+        ev = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+                     and "Memcpy" not in e.name and "Memset" not in e.name),
+                    key=lambda e: e.time_range.start)
+        per = len(ev) // 20
+        rows = {}
+        for i in range(per, len(ev)):  # skip the first chain
+            e, prev = ev[i], ev[i - 1]
+            k = i % per
+            d = rows.setdefault(k, [e.name[:60], 0.0, 0.0, 0])
+            d[1] += e.time_range.end - e.time_range.start
+            d[2] += e.time_range.start - prev.time_range.end
+            d[3] += 1
+        print(f"[{mode}] kernels per chain: {per}")
+        tot_k = tot_g = 0.0
+        for k in sorted(rows):
+            name, dur, gap, c = rows[k]
+            tot_k += dur / c
+            tot_g += gap / c
+            print(f"  {dur / c:7.2f} us  gap-before {gap / c:6.2f} us  {name}")
+        print(f"  kernels {tot_k:.1f} us + gaps {tot_g:.1f} us per chain")
 if "--host" in sys.argv:
     import time
     import cProfile
