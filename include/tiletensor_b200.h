@@ -170,6 +170,17 @@ int tt_sum(tt_session* s, const tt_shape* in_shape, const double* tin, int dim, 
 int tt_mul_sum(tt_session* s, const tt_shape* a, const double* ta, int64_t chain_a,
                const tt_shape* b, const double* tb, int64_t chain_b, int dim, int variant,
                tt_shape* out_shape, double* out, int64_t* out_chain);
+/* A fully connected stage of cryptonets_infer's tiled branch nn.hpp:468-490
+ * (and the c4 layer): r = tt_sum(tt_mul(a,b), dim, variant); if c is not NULL
+ * r = tt_add(r, c); if square r = tt_mul(r, r) -- one device pass for the tail
+ * where the reduction ends in a tree pass, else consecutive kernels.  Shapes,
+ * chain index, counters and errors equal the three-call composition (which
+ * runs as such when c would broadcast the sum to a larger grid or the square
+ * would exhaust the depth). */
+int tt_mul_sum_affine(tt_session* s, const tt_shape* a, const double* ta, int64_t chain_a,
+                      const tt_shape* b, const double* tb, int64_t chain_b, int dim, int variant,
+                      const tt_shape* c, const double* tc, int64_t chain_c, int square,
+                      tt_shape* out_shape, double* out, int64_t* out_chain);
 /* matvec_a/matvec_b/matmul_a/matmul_b linalg.hpp:41-73 (adds the rank and
  * replication preconditions of linalg.hpp:32-37 to tt_mul_sum).
  * which: 0=matvec_a 1=matvec_b 2=matmul_a 3=matmul_b. */

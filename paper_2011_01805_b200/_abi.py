@@ -80,6 +80,8 @@ SIGNATURES = {
     "tt_sum": (_I, [_P, _SP, _P, _I, _I, _SP, _P]),
     "tt_mul_sum": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64, _I, _I, _SP, _P, _I64P]),
     "tt_linalg_product": (_I, [_P, _I, _SP, _P, _I64, _SP, _P, _I64, _I, _SP, _P, _I64P]),
+    "tt_mul_sum_affine": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64, _I, _I, _SP, _P, _I64, _I, _SP, _P,
+                               _I64P]),
     "tt_clean_unknowns": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64P]),
     "tt_replicate_dim": (_I, [_P, _SP, _P, _I, _SP, _P]),
     "tt_tiles_binary": (_I, [_P, _I, _P, _P, _P, _I64, _I64P, _I64P, _I64P]),

@@ -13,9 +13,11 @@
 // BACK: rotations by -e*stride (replicate_tile_dim's right-to-left schedule):
 // the column is read mirrored (m -> T-1-m), which turns them into the forward
 // levels below with the same operand order.  `in` may equal `out`.
-template <int T, bool BACK = false>
+// EPI: the reduction's elementwise tail (+ C, square) applied before the store.
+template <int T, bool BACK = false, bool EPI = false>
 __global__ void __launch_bounds__(256) col_tree_kernel(const double* in, double* out, int64_t n_tiles,
-                                                       int64_t stride, int64_t s, FastDiv64 cdiv) {
+                                                       int64_t stride, int64_t s, FastDiv64 cdiv,
+                                                       const __grid_constant__ EpiDev epi) {
   const uint64_t total = static_cast<uint64_t>(n_tiles) * stride;
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -33,6 +35,12 @@ __global__ void __launch_bounds__(256) col_tree_kernel(const double* in, double*
       for (int m = 0; m < T; ++m) nv[m] = dadd(v[m], v[(m + e) % T]);
 #pragma unroll
       for (int m = 0; m < T; ++m) v[m] = nv[m];
+    }
+    if (EPI) {
+      const double* ct = epi_tile(epi, tile, s);
+      if (ct) ct += col;
+#pragma unroll
+      for (int m = 0; m < T; ++m) v[m] = epi_apply(epi, v[m], ct, m * stride);
     }
 #pragma unroll
     for (int m = 0; m < T; ++m) base[(BACK ? T - 1 - m : m) * stride] = v[m];
@@ -56,10 +64,12 @@ __device__ __forceinline__ void row_shift(double (&v)[NR], int D) {
 // halo rows owned by other warps, so the pass cannot run in place.
 // BACK: the tile is read and written mirrored (slot p -> s-1-p), which turns
 // rotations by -d (replicate schedules) into the forward offsets d handled here.
-template <int HR, int R = 16, bool BACK = false>
+// EPI: the reduction's elementwise tail (+ C, square) applied before the store.
+template <int HR, int R = 16, bool BACK = false, bool EPI = false>
 __global__ void __launch_bounds__(256) row_tree_kernel(const double* __restrict__ in,
                                                        double* __restrict__ out, int64_t n_tiles,
-                                                       int64_t s, int nlevels, int4 lv0, int4 lv1) {
+                                                       int64_t s, int nlevels, int4 lv0, int4 lv1,
+                                                       const __grid_constant__ EpiDev epi) {
   constexpr int NR = R + HR;
   const int lane = threadIdx.x & 31;
   const int rows = static_cast<int>(s / 32);
@@ -103,10 +113,11 @@ __global__ void __launch_bounds__(256) row_tree_kernel(const double* __restrict_
         }
       }
     }
+    const double* ct = EPI ? epi_tile(epi, tile, s) : nullptr;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int64_t p = (rb + i) * 32 + lane;
-      o[BACK ? s - 1 - p : p] = v[i];
+      o[BACK ? s - 1 - p : p] = EPI ? epi_apply(epi, v[i], ct, p) : v[i];
     }
   }
 }
@@ -158,5 +169,29 @@ __global__ void __launch_bounds__(kTreeThreads, 2) smem_tree_kernel(double* __re
     }
 #pragma unroll
     for (int i = 0; i < PER; ++i) t[tid + i * T] = v[i];
+  }
+}
+
+// (D) the reduction's elementwise tail alone (paths without a tree pass): in
+// place over the output tiles; VEC = slot pairs (16-byte accesses).
+template <bool VEC>
+__global__ void __launch_bounds__(256) epilogue_kernel(double* __restrict__ tiles, int64_t n_tiles,
+                                                       int64_t s, FastDiv64 per_tile,
+                                                       const __grid_constant__ EpiDev epi) {
+  const uint64_t total = static_cast<uint64_t>(n_tiles) * per_tile.d;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t tile = fdiv(w, per_tile);
+    const int64_t j = static_cast<int64_t>(w - tile * per_tile.d) * (VEC ? 2 : 1);
+    const double* ct = epi_tile(epi, tile, s);
+    double* t = tiles + tile * s + j;
+    if (VEC) {
+      double2 x = *reinterpret_cast<double2*>(t);
+      x.x = epi_apply(epi, x.x, ct, j);
+      x.y = epi_apply(epi, x.y, ct, j + 1);
+      *reinterpret_cast<double2*>(t) = x;
+    } else {
+      *t = epi_apply(epi, *t, ct, j);
+    }
   }
 }

@@ -170,7 +170,8 @@ GroupSpec make_group_spec(const std::vector<int64_t>& ext, int di,
 // Shared body of tt_sum / tt_mul_sum for a non-degenerate summed dim.
 void run_reduction(tt_session* s, const Shape& prod, int di, int variant, const double* ta,
                    const std::vector<int64_t>& a_st, const double* tb,
-                   const std::vector<int64_t>& b_st, double* out) {
+                   const std::vector<int64_t>& b_st, double* out,
+                   const Epilogue* epi = nullptr) {
   const Dim& ds = prod.dims[di];
   if (ds.interleaved && ds.unknown && ds.used() < prod.ext(di) * ds.t)
     shape_error("sum over an unknown interleaved dimension requires clean_unknowns first");
@@ -188,7 +189,7 @@ void run_reduction(tt_session* s, const Shape& prod, int di, int variant, const 
   const Program& prog = *it->second;
   const GroupSpec g = make_group_spec(ext, di, a_st, b_st, tb != nullptr);
   add_cost(s, prog.per_group, static_cast<uint64_t>(g.groups));
-  launch_group_program(ctx_of(s), prog, g, s->slots, ta, tb, out);
+  launch_group_program(ctx_of(s), prog, g, s->slots, ta, tb, out, epi);
 }
 
 void require_slots(const tt_session* s, const Shape& sh, const char* who) {
@@ -594,6 +595,119 @@ int tt_mul_sum(tt_session* s, const tt_shape* a, const double* ta, int64_t chain
     operand_strides(sa, ast);
     operand_strides(sb, bst);
     run_reduction(s, prod, di, variant, ta, ast, tb, bst, out);
+  });
+}
+
+int tt_mul_sum_affine(tt_session* s, const tt_shape* a, const double* ta, int64_t chain_a,
+                      const tt_shape* b, const double* tb, int64_t chain_b, int dim, int variant,
+                      const tt_shape* c, const double* tc, int64_t chain_c, int square,
+                      tt_shape* out_shape, double* out, int64_t* out_chain) {
+  // Validate the whole composition first; anything the fused pass does not
+  // cover (C broadcasting the sum to a larger grid, a depth error at the
+  // square, a C from the wrong slot count) runs as the plain composition so
+  // that counters and errors match it call for call.
+  bool fused = true;
+  Shape sa, sb, prod, so, sr;
+  int64_t chain1 = 0, chain2 = 0;
+  int rc = guarded([&] {
+    need_session(s);
+    sa = from_c(a);
+    sb = from_c(b);
+    prod = elementwise_result_shape(sa, sb, TT_OP_MUL);
+    require_slots(s, sa, "tt_mul");
+    require_slots(s, sb, "tt_mul");
+    check_tiles_addressable(prod);
+    chain1 = mul_chain(chain_a, chain_b);
+    so = sum_result_shape(prod, dim);
+  });
+  if (rc != TT_OK) return rc;
+  sr = so;
+  chain2 = chain1;
+  if (c != nullptr) {
+    try {
+      const Shape sc = from_c(c);
+      require_slots(s, sc, "elementwise");
+      sr = elementwise_result_shape(so, sc, TT_OP_ADD);
+      chain2 = std::min(chain1, chain_c);
+      if (sr.tile_count() != so.tile_count()) fused = false;
+    } catch (const std::exception&) {
+      fused = false;
+    }
+  }
+  if (square && chain2 < 1) fused = false;
+  if (square && fused) {
+    try {
+      sr = elementwise_result_shape(sr, sr, TT_OP_MUL);
+    } catch (const std::exception&) {
+      fused = false;
+    }
+  }
+  if (!fused) {  // the composition, through the public entry points
+    void* tmp[2] = {nullptr, nullptr};
+    auto alloc_tiles = [&](const tt_shape* sh, int k) {
+      return tt_device_alloc(s, std::max<int64_t>(1, tt_shape_tile_count(sh)) * s->slots * 8, &tmp[k]);
+    };
+    tt_shape cur{}, next{};
+    int64_t ch = 0;
+    to_c(so, &cur);
+    rc = alloc_tiles(&cur, 0);
+    if (rc == TT_OK)
+      rc = tt_mul_sum(s, a, ta, chain_a, b, tb, chain_b, dim, variant, &cur,
+                      static_cast<double*>(tmp[0]), &ch);
+    const double* src = static_cast<double*>(tmp[0]);
+    if (rc == TT_OK && c != nullptr) {
+      rc = tt_shape_elementwise_result(&cur, c, TT_OP_ADD, &next);
+      if (rc == TT_OK && square) rc = alloc_tiles(&next, 1);
+      double* dst = square ? static_cast<double*>(tmp[1]) : out;
+      if (rc == TT_OK)
+        rc = tt_elementwise(s, TT_OP_ADD, &cur, src, ch, c, tc, chain_c, &next, dst, &ch);
+      src = dst;
+      cur = next;
+    }
+    if (rc == TT_OK) {
+      if (square)
+        rc = tt_elementwise(s, TT_OP_MUL, &cur, src, ch, &cur, src, ch, out_shape, out, &ch);
+      else
+        *out_shape = cur;
+    }
+    if (rc == TT_OK && out_chain) *out_chain = ch;
+    const std::string err = g_error;
+    const int64_t pos = g_error_pos;
+    for (void* t : tmp)
+      if (t) tt_device_free(s, t);
+    if (rc != TT_OK) set_error(rc, err, pos);
+    return rc;
+  }
+  return guarded([&] {
+    to_c(sr, out_shape);
+    if (out_chain) *out_chain = square ? chain2 - 1 : chain2;
+    s->muls += static_cast<uint64_t>(prod.tile_count());
+    std::lock_guard<std::mutex> lk(s->mu);
+    Epilogue epi;
+    epi.square = square != 0;
+    const auto ext = so.external();
+    epi.nd = static_cast<int>(ext.size());
+    for (int i = 0; i < epi.nd; ++i) epi.ext[i] = ext[i];
+    if (c != nullptr) {
+      std::vector<int64_t> cst;
+      operand_strides(from_c(c), cst);
+      epi.c = tc;
+      for (int i = 0; i < epi.nd; ++i) epi.c_stride[i] = cst[i];
+    }
+    const int di = dim - 1;
+    const Dim& ds = prod.dims[di];
+    if (ds.n == 1 && ds.d > 1) {  // degenerate sum: the product itself, then the tail
+      launch_elementwise(ctx_of(s), TT_OP_MUL, prod, sa, sb, s->slots, ta, tb, out);
+      launch_epilogue(ctx_of(s), epi, s->slots, out, so.tile_count());
+    } else {
+      std::vector<int64_t> ast, bst;
+      operand_strides(sa, ast);
+      operand_strides(sb, bst);
+      run_reduction(s, prod, di, variant, ta, ast, tb, bst, out, &epi);
+    }
+    // the tail's counters: one tt_add and one tt_mul over the result tiles
+    if (c != nullptr) s->adds += static_cast<uint64_t>(sr.tile_count());
+    if (square) s->muls += static_cast<uint64_t>(sr.tile_count());
   });
 }
 

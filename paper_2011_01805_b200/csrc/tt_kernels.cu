@@ -146,6 +146,47 @@ void post_launch(const LaunchCtx& c, const char* what) {
   check_cuda(cudaGetLastError(), what);
 }
 
+// Device form of an Epilogue (tt_launch.hpp): the add operand's tile for
+// output tile l is C + (sum_i coord_i(l) * cst[i]) * s, coordinates of l in
+// the row-major output grid (divisors innermost last).
+struct EpiDev {
+  const double* c = nullptr;
+  int nd = 0;
+  int square = 0;
+  FastDiv64 ext[TT_MAX_RANK];
+  int64_t cst[TT_MAX_RANK] = {};
+};
+
+EpiDev make_epi_dev(const Epilogue& e) {
+  EpiDev d;
+  d.c = e.c;
+  d.square = e.square ? 1 : 0;
+  d.nd = e.nd;
+  for (int i = 0; i < e.nd; ++i) {
+    d.ext[i] = make_div64(static_cast<uint64_t>(e.ext[i]));
+    d.cst[i] = e.c_stride[i];
+  }
+  return d;
+}
+
+__device__ __forceinline__ const double* epi_tile(const EpiDev& e, uint64_t tile, int64_t s) {
+  if (!e.c) return nullptr;
+  int64_t ci = 0;
+  for (int i = e.nd - 1; i >= 0; --i) {
+    const uint64_t q = fdiv(tile, e.ext[i]);
+    ci += static_cast<int64_t>(tile - q * e.ext[i].d) * e.cst[i];
+    tile = q;
+  }
+  return e.c + ci * s;
+}
+
+// tt_add(x, C) then tt_mul(x, x), each separately rounded, as the composition
+__device__ __forceinline__ double epi_apply(const EpiDev& e, double x, const double* ct, int64_t j) {
+  if (ct) x = dadd(x, __ldg(ct + j));
+  if (e.square) x = dmul(x, x);
+  return x;
+}
+
 #include "kernels/stream.cuh"
 #include "kernels/group.cuh"
 #include "kernels/gemm.cuh"
@@ -893,9 +934,14 @@ TreePass plan_tree_pass(const GroupParams& p2, int64_t s, size_t smem_optin) {
   return tp;
 }
 
+// epi (optional, kinds 1 and 2 only): the reduction's elementwise tail, fused
+// into the tree pass's store.
 void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2, int64_t n_tiles,
-                   int64_t s, const double* folded, double* tout) {
+                   int64_t s, const double* folded, double* tout, const Epilogue* epi = nullptr) {
+  const bool fuse = epi != nullptr && epi->active();
+  const EpiDev ed = fuse ? make_epi_dev(*epi) : EpiDev{};
   if (tp.kind == 3) {  // in place: folded == tout
+    if (fuse) invalid_argument("tree epilogue: the shared-memory pass takes none");
     int lv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int i = 0; i < p2.nlevels; ++i) lv[i] = static_cast<int>(p2.rots[i]);
     const size_t smem = static_cast<size_t>(s) * sizeof(double);
@@ -916,23 +962,26 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
     const uint64_t total = static_cast<uint64_t>(n_tiles) * stride0;
     const FastDiv64 cd = make_div64(static_cast<uint64_t>(stride0));
     const int64_t work = static_cast<int64_t>((total + 255) / 256);
-#define TT_COL(TV, BK)                                                                       \
-  {                                                                                         \
-    const int grid = grid_for(c, (const void*)col_tree_kernel<TV, BK>, 256, 0, work);       \
-    col_tree_kernel<TV, BK><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, stride0, s, cd); \
+#define TT_COL(TV, BK, EP)                                                                       \
+  {                                                                                             \
+    const int grid = grid_for(c, (const void*)col_tree_kernel<TV, BK, EP>, 256, 0, work);       \
+    col_tree_kernel<TV, BK, EP><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, stride0, s, cd, ed); \
   }
-#define TT_COL_T(BK)              \
-  switch (tp.t) {                 \
-    case 2: TT_COL(2, BK) break;   \
-    case 4: TT_COL(4, BK) break;   \
-    case 8: TT_COL(8, BK) break;   \
-    case 16: TT_COL(16, BK) break; \
-    default: TT_COL(32, BK) break; \
+#define TT_COL_T(BK, EP)              \
+  switch (tp.t) {                     \
+    case 2: TT_COL(2, BK, EP) break;   \
+    case 4: TT_COL(4, BK, EP) break;   \
+    case 8: TT_COL(8, BK, EP) break;   \
+    case 16: TT_COL(16, BK, EP) break; \
+    default: TT_COL(32, BK, EP) break; \
   }
     if (tp.back) {
-      TT_COL_T(true)
+      if (fuse) invalid_argument("tree epilogue: mirrored passes take none");
+      TT_COL_T(true, false)
+    } else if (fuse) {
+      TT_COL_T(false, true)
     } else {
-      TT_COL_T(false)
+      TT_COL_T(false, false)
     }
 #undef TT_COL_T
 #undef TT_COL
@@ -948,11 +997,16 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
     constexpr int HR = decltype(hr_c)::value, RR = decltype(r_c)::value;
     const int64_t work = (n_tiles * (s / 32 / RR) + 7) / 8;
     if (tp.back) {
+      if (fuse) invalid_argument("tree epilogue: mirrored passes take none");
       const int grid = grid_for(c, (const void*)row_tree_kernel<HR, RR, true>, 256, 0, work);
-      row_tree_kernel<HR, RR, true><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
+      row_tree_kernel<HR, RR, true><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1, ed);
+    } else if (fuse) {
+      const int grid = grid_for(c, (const void*)row_tree_kernel<HR, RR, false, true>, 256, 0, work);
+      row_tree_kernel<HR, RR, false, true><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
+                                                                       lv1, ed);
     } else {
       const int grid = grid_for(c, (const void*)row_tree_kernel<HR, RR, false>, 256, 0, work);
-      row_tree_kernel<HR, RR, false><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1);
+      row_tree_kernel<HR, RR, false><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1, ed);
     }
   };
   using I1 = std::integral_constant<int, 1>;
@@ -973,16 +1027,18 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
   post_launch(c, "row tree pass");
 }
 
+// Returns true when `epi` was applied (fused into a tree pass); the caller
+// runs it as a separate pass otherwise.
 template <bool HAS_B>
-void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
-                         const double* ta, const double* tb, double* tout) {
+bool launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
+                         const double* ta, const double* tb, double* tout, const Epilogue* epi) {
   GroupParams p = make_group_params(prog, g, s);
-  if (g.groups == 0) return;
+  if (g.groups == 0) return true;
   const size_t tile_bytes = static_cast<size_t>(s) * sizeof(double);
   // 1) No in-tile schedule: the fold is the whole program.
   if (prog.ops.size() == 1 && prog.ops[0].kind == GOP_FOLD && prog.ops[0].dst == BUF_OUT) {
     launch_fold_best<HAS_B>(c, p, ta, tb, tout);
-    return;
+    return false;
   }
   const BlockPlan bplan = block_plan(g, HAS_B);
   const bool matmul_like = HAS_B && bplan.ia >= 0 && bplan.ib >= 0;
@@ -1015,7 +1071,7 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
       const TreePass tdirect = identity ? plan_tree_pass(p, s, c.smem_optin) : TreePass{};
       if ((tdirect.kind == 1 || tdirect.kind == 2) && (tdirect.kind == 1 || ta != tout)) {
         run_tree_pass(c, tdirect, p, g.groups, s, ta, tout);
-        return;
+        return false;
       }
     }
     // Too few groups to occupy every SM: fold over the whole grid first
@@ -1042,12 +1098,13 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
                             aligned16(tb);
       if (fuse_col) {
         launch_fold_blocked<HAS_B>(c, p, bplan, ta, tb, tout, true);
-        return;
+        return false;
       }
       if (tpass.kind != 0) {
         launch_fold_best<HAS_B>(c, p, ta, tb, fold_dst);
-        run_tree_pass(c, tpass, p, g.groups, s, fold_dst, tout);
-        return;
+        const bool fuse_epi = tpass.kind == 1 || tpass.kind == 2;
+        run_tree_pass(c, tpass, p, g.groups, s, fold_dst, tout, fuse_epi ? epi : nullptr);
+        return fuse_epi;
       }
       launch_fold_best<HAS_B>(c, p, ta, tb, tout);
       // phase 2 reads its group's folded tile from OUT: a = out tile index
@@ -1069,7 +1126,7 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
         dispatch_pow2<false, true>(c, p2, threads, vmax, tile_bytes, tout, nullptr, tout);
       else
         dispatch_pow2<false, false>(c, p2, threads, vmax, tile_bytes, tout, nullptr, tout);
-      return;
+      return false;
     }
     int64_t halo = 0;
     for (int i = 0; i < p.nlevels; ++i) halo += p.rots[i];
@@ -1082,7 +1139,7 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
       dispatch_pow2<HAS_B, true>(c, p, threads, vmax, tile_bytes, ta, tb, tout);
     else
       dispatch_pow2<HAS_B, false>(c, p, threads, vmax, tile_bytes, ta, tb, tout);
-    return;
+    return false;
   }
   // 3) Generic interpreter.
   const int gthreads = static_cast<int>(std::min<int64_t>(512, ((s + 31) / 32) * 32));
@@ -1100,6 +1157,7 @@ void launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
   if (!p.use_smem) scratch = c.scratch(c.scratch_owner, phys * static_cast<size_t>(grid));
   k<<<grid, gthreads, smem, c.stream>>>(p, ta, tb, tout, scratch);
   post_launch(c, "group generic kernel");
+  return false;
 }
 
 }  // namespace
@@ -1108,11 +1166,28 @@ void set_kernel_path(int path) { g_forced_path.store(path, std::memory_order_rel
 int kernel_path() { return forced_path(); }
 
 void launch_group_program(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
-                          const double* ta, const double* tb, double* tout) {
-  if (tb != nullptr)
-    launch_program_impl<true>(c, prog, g, s, ta, tb, tout);
-  else
-    launch_program_impl<false>(c, prog, g, s, ta, tb, tout);
+                          const double* ta, const double* tb, double* tout, const Epilogue* epi) {
+  if (epi != nullptr && !epi->active()) epi = nullptr;
+  const bool applied = tb != nullptr ? launch_program_impl<true>(c, prog, g, s, ta, tb, tout, epi)
+                                     : launch_program_impl<false>(c, prog, g, s, ta, tb, tout, epi);
+  if (epi != nullptr && !applied) launch_epilogue(c, *epi, s, tout, g.groups);
+}
+
+void launch_epilogue(const LaunchCtx& c, const Epilogue& e, int64_t s, double* tiles,
+                     int64_t n_tiles) {
+  if (!e.active() || n_tiles <= 0) return;
+  const EpiDev ed = make_epi_dev(e);
+  const bool vec = s % 2 == 0 && aligned16(tiles) && (e.c == nullptr || aligned16(e.c));
+  const int64_t per = vec ? s / 2 : s;
+  const int64_t work = (n_tiles * per + 255) / 256;
+  if (vec) {
+    const int grid = grid_for(c, (const void*)epilogue_kernel<true>, 256, 0, work);
+    epilogue_kernel<true><<<grid, 256, 0, c.stream>>>(tiles, n_tiles, s, make_div64(static_cast<uint64_t>(per)), ed);
+  } else {
+    const int grid = grid_for(c, (const void*)epilogue_kernel<false>, 256, 0, work);
+    epilogue_kernel<false><<<grid, 256, 0, c.stream>>>(tiles, n_tiles, s, make_div64(static_cast<uint64_t>(per)), ed);
+  }
+  post_launch(c, "epilogue kernel");
 }
 
 }  // namespace ttb

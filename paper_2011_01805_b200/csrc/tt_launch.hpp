@@ -99,9 +99,28 @@ void launch_rotate(const LaunchCtx& c, const double* in, double* out, int64_t s,
 // out = in * used-mask(shape)   (tile_tensor.hpp:364-380)
 void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const double* in,
                   double* out);
-// Runs `prog` for every group of `g`; `tb` may be null (no fused multiply).
+// Elementwise tail of a reduction -- tt_add(r, C) then tt_mul(r, r), each
+// optional -- over the reduction's output grid `ext` (row-major, outermost
+// first): out tile l = (r_l + C[sum_i coord_i(l) * c_stride[i]]) squared.
+// c_stride[i] is C's tile-index stride along output dim i (0 where C
+// broadcasts).  Fused into the tree pass when the reduction ends in one,
+// else a separate in-place pass over the output tiles.
+struct Epilogue {
+  const double* c = nullptr;
+  bool square = false;
+  int nd = 0;
+  int64_t ext[TT_MAX_RANK] = {};
+  int64_t c_stride[TT_MAX_RANK] = {};
+  bool active() const { return c != nullptr || square; }
+};
+// Runs `prog` for every group of `g`; `tb` may be null (no fused multiply);
+// `epi` (optional) is applied to every output tile.
 void launch_group_program(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
-                          const double* ta, const double* tb, double* tout);
+                          const double* ta, const double* tb, double* tout,
+                          const Epilogue* epi = nullptr);
+// The epilogue alone, in place over n_tiles output tiles.
+void launch_epilogue(const LaunchCtx& c, const Epilogue& e, int64_t s, double* tiles,
+                     int64_t n_tiles);
 // Synthetic input generator shared with oracle/tt_oracle.c or_fill_uniform.
 void launch_fill_uniform(const LaunchCtx& c, double* out, int64_t count, uint64_t seed,
                          int64_t offset, double lo, double hi);

@@ -241,6 +241,31 @@ inline TileTensor tt_mul_sum(const TileTensor& a, const TileTensor& b, int dim,
   return TileTensor(TileTensorShape::from_c(co), out, s, chain);
 }
 
+// One fully connected stage of cryptonets_infer's tiled branch (nn.hpp:468-490):
+// tt_sum(tt_mul(a, b), dim), then tt_add(., *c) when c is given, then
+// tt_mul(., .) when square -- the tail fused into the reduction's tree pass.
+// Shapes, chain index, counters and errors equal the three-call composition.
+inline TileTensor tt_mul_sum_affine(const TileTensor& a, const TileTensor& b, int dim,
+                                    const TileTensor* c, bool square,
+                                    std::optional<SumVariant> variant = std::nullopt) {
+  if (&a.session() != &b.session() || (c && &c->session() != &a.session()))
+    throw std::invalid_argument("operands belong to different sessions");
+  Session& s = a.session();
+  TileTensorShape res = sum_result_shape(elementwise_result_shape(a.shape(), b.shape(), OpKind::mul), dim);
+  if (c) res = elementwise_result_shape(res, c->shape(), OpKind::add);
+  auto out = detail::alloc_tiles(s, res.tile_count());
+  const tt_shape ca = a.shape().to_c(), cb = b.shape().to_c();
+  const tt_shape cc = c ? c->shape().to_c() : tt_shape{};
+  tt_shape co;
+  std::int64_t chain = 0;
+  detail::check(tt_mul_sum_affine(s.handle(), &ca, a.device_data(), a.chain_index(), &cb,
+                                  b.device_data(), b.chain_index(), dim,
+                                  detail::variant_code(variant), c ? &cc : nullptr,
+                                  c ? c->device_data() : nullptr, c ? c->chain_index() : 0,
+                                  square ? 1 : 0, &co, out->get(), &chain));
+  return TileTensor(TileTensorShape::from_c(co), out, s, chain);
+}
+
 inline TileTensor clean_unknowns(const TileTensor& t) {
   if (!t.shape().has_unknown()) return t;
   Session& s = t.session();

@@ -465,7 +465,11 @@ def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],
     data: Optional[TileTensor] = None
     perm = None
     stage = 0
+    fused_square = False
     for layer_no, layer in enumerate(net.layers, start=1):
+        if fused_square:  # applied with the preceding linear stage
+            fused_square = False
+            continue
         try:
             if isinstance(layer, ConvLayer):
                 c = layer
@@ -486,7 +490,11 @@ def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],
                 bf = np.repeat(c.bias, windows)
                 tw = tt.pack(np.ascontiguousarray(wf).reshape(kk, fold, 1),
                              shape3((kk, 1, t1), (fold, 1, t2), (1, t3, t3)), session)
-                data = tt.tt_add(tt.tt_mul_sum(tw, td, 1), pack_bias(bf, True))
+                tb = pack_bias(bf, True)
+                nxt = net.layers[layer_no] if layer_no < len(net.layers) else None
+                depth_after = min(min(tw.chain_index(), td.chain_index()) - 1, tb.chain_index())
+                fused_square = isinstance(nxt, SquareLayer) and depth_after >= 1
+                data = tt.tt_mul_sum_affine(tw, td, 1, tb, square=fused_square)
                 # the oracle flattens window-major, the folded layout is filter-major
                 perm = (np.arange(windows)[None, :] * c.filters +
                         np.arange(c.filters)[:, None]).reshape(-1)
@@ -506,8 +514,14 @@ def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],
                         data = tt.replicate_dim(data, 2)
                 tw = pack_weights(np.asarray(f.weights, dtype=np.float64), odd, perm)
                 perm = None
-                data = tt.tt_mul_sum(tw, data, 1 if odd else 2)
-                data = tt.tt_add(data, pack_bias(np.asarray(f.bias, dtype=np.float64), odd))
+                tb = pack_bias(np.asarray(f.bias, dtype=np.float64), odd)
+                # a following square activation runs in the same device pass
+                # (tt_mul_sum_affine) unless it would exhaust the depth, which
+                # must then be reported against the square layer itself
+                nxt = net.layers[layer_no] if layer_no < len(net.layers) else None
+                depth_after = min(min(tw.chain_index(), data.chain_index()) - 1, tb.chain_index())
+                fused_square = isinstance(nxt, SquareLayer) and depth_after >= 1
+                data = tt.tt_mul_sum_affine(tw, data, 1 if odd else 2, tb, square=fused_square)
             elif isinstance(layer, SquareLayer):
                 if data is None:
                     raise ShapeError("activation before any linear layer")

@@ -384,6 +384,26 @@ static void linalg() {
                                       TileTensorShape({DimSpec{b, 1, t1}, DimSpec{1, t2, t2}, DimSpec{c, 1, t3}}), session);
           ++runs;
           if (max_rel_diff(unpack(matmul_b(tat, tbb)).reshape({a, c}), expect) >= 1e-9) ++fails;
+          if (it == 0) {  // fused FC stage == tt_mul(tt_add(matmul_a, bias)) bit for bit
+            const TileTensor bias = pack(random_tensor({a, 1, c}, rng, -1, 1),
+                                         TileTensorShape({DimSpec{a, 1, t1}, DimSpec{1, t2, t2}, DimSpec{c, 1, t3}}), session);
+            session.reset_counters();
+            TileTensor want = tt_add(tt_mul_sum(ta, tb, 2), bias);
+            want = tt_mul(want, want);
+            const CostReport wc = session.cost_report();
+            session.reset_counters();
+            const TileTensor got = tt_mul_sum_affine(ta, tb, 2, &bias, true);
+            const CostReport gc = session.cost_report();
+            bool same = format_shape(got.shape()) == format_shape(want.shape()) &&
+                        got.chain_index() == want.chain_index() && gc.additions == wc.additions &&
+                        gc.multiplications == wc.multiplications && gc.rotations == wc.rotations &&
+                        got.tiles().size() == want.tiles().size();
+            for (std::size_t i = 0; same && i < got.tiles().size(); ++i)
+              same = std::memcmp(got.tiles()[i].slots().data(), want.tiles()[i].slots().data(),
+                                 8 * got.tiles()[i].slots().size()) == 0;
+            ++runs;
+            if (!same) ++fails;
+          }
         }
       }
   }

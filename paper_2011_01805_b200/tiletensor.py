@@ -606,6 +606,35 @@ def tt_mul_sum(a: TileTensor, b: TileTensor, dim: int,
     return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
 
 
+def tt_mul_sum_affine(a: TileTensor, b: TileTensor, dim: int, c: Optional[TileTensor] = None,
+                      square: bool = False, variant: Optional[SumVariant] = None) -> TileTensor:
+    """One fully connected stage of cryptonets_infer's tiled branch (nn.hpp:468-490):
+    tt_sum(tt_mul(a, b), dim), then tt_add(., c) when c is given, then tt_mul(., .) when
+    square -- the tail fused into the reduction's tree pass.  Shapes, chain index,
+    counters and errors equal the three-call composition."""
+    s = _same_session(a, b)
+    if c is not None:
+        _same_session(a, c)
+
+    def count():
+        r = sum_result_shape(elementwise_result_shape(a.shape(), b.shape(), OpKind.mul), dim)
+        if c is not None:
+            r = elementwise_result_shape(r, c.shape(), OpKind.add)
+        return r.tile_count()
+    n_out = _result_tiles(("mulsum_affine", a.shape(), b.shape(), int(dim),
+                           None if c is None else c.shape()), count)
+    out = s.empty_tiles(n_out)
+    so = CShape()
+    chain = ctypes.c_int64()
+    _check(lib().tt_mul_sum_affine(
+        s.handle, ctypes.byref(a.shape().to_c()), _ptr(a.data()), a.chain_index(),
+        ctypes.byref(b.shape().to_c()), _ptr(b.data()), b.chain_index(), int(dim), _variant(variant),
+        None if c is None else ctypes.byref(c.shape().to_c()), None if c is None else _ptr(c.data()),
+        0 if c is None else c.chain_index(), 1 if square else 0, ctypes.byref(so), _ptr(out),
+        ctypes.byref(chain)))
+    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
+
+
 _PRODUCT_TILES: dict = {}
 
 

@@ -1,0 +1,147 @@
+"""tt_mul_sum_affine (one fully connected stage of cryptonets_infer's tiled branch,
+nn.hpp:468-490: tt_sum(tt_mul(a, b)), + bias, square) against the three-call
+composition on the GPU -- tiles bit for bit, result shape, chain index, cost
+counters and errors -- over every path the tail can take: fused into the column
+tree pass (config 4 layer 1), the row-shift tree pass (matmul_a shapes), a
+separate epilogue pass after the fused group kernels and the tiny single-launch
+reduction, a degenerate sum, and the composition fallbacks (bias broadcasting
+the sum to a larger grid, a square that exhausts the depth, incompatible bias)."""
+import numpy as np
+import pytest
+
+import paper_2011_01805_b200 as tt
+from golden_cases import bitwise_equal
+from paper_2011_01805_b200 import configs, parse_shape
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand(shape, seed):
+    return np.random.default_rng(seed).uniform(-1, 1, size=shape)
+
+
+def _compose(a, b, dim, c, square):
+    r = tt.tt_mul_sum(a, b, dim)
+    if c is not None:
+        r = tt.tt_add(r, c)
+    if square:
+        r = tt.tt_mul(r, r)
+    return r
+
+
+def _check(S, a, b, dim, c, square):
+    S.reset_counters()
+    want = _compose(a, b, dim, c, square)
+    want_cost = S.cost_report()
+    S.reset_counters()
+    got = tt.tt_mul_sum_affine(a, b, dim, c, square=square)
+    got_cost = S.cost_report()
+    assert tt.format_shape(got.shape()) == tt.format_shape(want.shape())
+    assert got.chain_index() == want.chain_index()
+    assert bitwise_equal(got.tiles(), want.tiles())
+    assert got_cost == want_cost, (got_cost, want_cost)
+    return got
+
+
+def _pack(S, spec, dense_shape, seed):
+    return tt.pack(_rand(dense_shape, seed), parse_shape(spec), S)
+
+
+@pytest.mark.parametrize("square", [False, True])
+def test_config4_layer1_column_tree(gpu, oracle, square):
+    case = configs.config4(False)
+    S = tt.Session(8192, 8)
+    T = {k: tt.pack(case.tensors[k], parse_shape(v), S) for k, v in case.shapes.items()}
+    got = _check(S, T["W1t"], T["X"], 1, T["b1"], square)
+    # and against the CPU oracle's composition
+    s = 8192
+    ps = {k: parse_shape(v) for k, v in case.shapes.items()}
+    p = {k: oracle.pack(case.tensors[k], ps[k], s) for k in ("W1t", "X", "b1")}
+    s1, o1, _ = oracle.mul_sum(ps["W1t"], p["W1t"], ps["X"], p["X"], s, 1)
+    s2, o2, _ = oracle.elementwise(0, s1, o1, ps["b1"], p["b1"], s)
+    if square:
+        s2, o2, _ = oracle.elementwise(1, s2, o2, s2, o2, s)
+    assert bitwise_equal(got.tiles(), o2)
+
+
+@pytest.mark.parametrize("bias", ["[64/16,*/32,*/16]", "[64/16,*/32,64/16]", None])
+def test_matmul_a_row_tree(gpu, bias):
+    S = tt.Session(8192, 8)
+    a = _pack(S, "[64/16,128/32,*/16]", (64, 128, 1), 1)
+    b = _pack(S, "[*/16,128/32,64/16]", (1, 128, 64), 2)
+    c = None
+    if bias is not None:
+        dshape = tuple(1 if "*" in d else int(d.split("/")[0]) for d in bias[1:-1].split(","))
+        c = _pack(S, bias, dshape, 3)
+    for square in (False, True):
+        _check(S, a, b, 2, c, square)
+
+
+def test_config1_single_launch(gpu):
+    c1 = configs.config1()
+    S = tt.Session(512, 8)
+    a = tt.pack(c1.tensors["A"], parse_shape(c1.shapes["A"]), S)
+    b = tt.pack(c1.tensors["B"], parse_shape(c1.shapes["B"]), S)
+    c = _pack(S, "[100/16,*/32]", (100, 1), 4)
+    for square in (False, True):
+        _check(S, a, b, 2, c, square)
+    _check(S, a, b, 2, None, True)
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_group_kernels_separate_tail(gpu, dim):
+    """c5-like shapes: the fused group kernels (TMA ring / window) end the
+    reduction, the tail runs as its own in-place pass."""
+    S = tt.Session(16384, 8)
+    x = _pack(S, "[256/16,256/32,64/32]", (256, 256, 64), 5)
+    w = _pack(S, "[*/16,256/32,64/32]", (1, 256, 64), 6)
+    r = tt.tt_mul_sum(x, w, dim)
+    dense = tuple(1 if d.n == 1 else d.n for d in r.shape().dims())
+    spec = tt.format_shape(r.shape()).replace("1?", "1")
+    c = _pack(S, spec, dense, 7)
+    _check(S, x, w, dim, c, True)
+
+
+def test_degenerate_sum(gpu):
+    S = tt.Session(512, 8)
+    a = _pack(S, "[*/16,200/32]", (1, 200), 8)
+    b = _pack(S, "[*/16,200/32]", (1, 200), 9)
+    c = _pack(S, "[*/16,200/32]", (1, 200), 10)
+    _check(S, a, b, 1, c, True)
+
+
+def test_composition_fallbacks(gpu):
+    S = tt.Session(512, 8)
+    a = _pack(S, "[64/16,64/32]", (64, 64), 11)
+    b = _pack(S, "[64/16,64/32]", (64, 64), 12)
+    # the bias broadcasts the sum [*/16,64/32] (1 x 2 tiles) to 4 x 2 tiles
+    big = _pack(S, "[64/16,64/32]", (64, 64), 13)
+    got = _check(S, a, b, 1, big, True)
+    assert got.shape().tile_count() == 8
+    # incompatible bias: the same ShapeError as the composition's tt_add
+    bad = _pack(S, "[64/16,64/32]", (64, 64), 14)
+    with pytest.raises(tt.ShapeError) as e1:
+        _compose(a, b, 2, bad, True)
+    S.reset_counters()
+    with pytest.raises(tt.ShapeError) as e2:
+        tt.tt_mul_sum_affine(a, b, 2, bad, square=True)
+    assert str(e1.value) == str(e2.value)
+
+
+def test_square_exhausts_depth(gpu):
+    S = tt.Session(512, 1)  # packed tensors have chain index 1; after the product 0
+    a = _pack(S, "[64/16,64/32]", (64, 64), 15)
+    b = _pack(S, "[64/16,64/32]", (64, 64), 16)
+    c = _pack(S, "[64/16,*/32]", (64, 1), 17)
+    S.reset_counters()
+    with pytest.raises(tt.DepthExhaustedError) as e1:
+        _compose(a, b, 2, c, True)
+    want_cost = S.cost_report()
+    S.reset_counters()
+    with pytest.raises(tt.DepthExhaustedError) as e2:
+        tt.tt_mul_sum_affine(a, b, 2, c, square=True)
+    assert S.cost_report() == want_cost
+    assert str(e1.value) == str(e2.value)
+    # without the square the stage itself is fine
+    _check(S, a, b, 2, c, False)
+
