@@ -590,3 +590,195 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
     }
   }
 }
+
+// Warp-specialised variant of fold_gemm_tma_kernel: the same units, tensor-map
+// boxes, ring layout and epilogue, but the TMA issue runs on its own producer
+// warp (warp kW, one elected lane) instead of on consumer warp 0's lane 0.
+// The producer alone waits for a ring buffer to be released (empty barrier);
+// consumer warps only wait for data (full barrier), so no consumer is held
+// back to the slowest one at every stage.  Measured with the operands already
+// in shared memory (tools/micro/gemm_loop.cu) the consumer loop itself runs the
+// FP64 pipe at 92%; the ring machinery is what this variant trims.
+template <int BC, int SL, int kTgSteps, int kTgStages, int SC, int PB = kGemmBlk>
+__global__ void __launch_bounds__((tg_warps<BC, SL, SC, PB>() + 1) * 32, 3)
+    fold_gemm_ws_kernel(const __grid_constant__ CUtensorMap mapA,
+                        const __grid_constant__ CUtensorMap mapB,
+                        const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
+                        const __grid_constant__ TgSpec ts, double* __restrict__ OUT,
+                        unsigned int* __restrict__ sched, int wait_mode) {
+  // wait_mode (TT_GEMM_WAIT): 0 = every mbarrier waiter spins on try_wait,
+  // 1 = the producer sleeps on try_wait's suspend hint, 2 = every waiter does
+  constexpr int kW = tg_warps<BC, SL, SC, PB>();  // consumer warps
+  constexpr int kA = kTgSteps * PB * SL;           // doubles per stage
+  constexpr int kB = kTgSteps * BC * SL;
+  constexpr int kStage = kA + kB;
+  extern __shared__ __align__(1024) double tsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + kTgStages * kStage);
+  uint64_t* empty = full + kTgStages;
+  uint64_t* stage_unit = empty + kTgStages;  // unit loaded into each stage (~0: no more)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTgStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t s = p.s;
+  const int cnt = static_cast<int>(p.count);
+  const int nst = (cnt + kTgSteps - 1) / kTgSteps;  // stages per unit
+  const uint64_t units = static_cast<uint64_t>(bs.units);
+
+  if (warp == kW) {  // ---- producer ----
+    if (lane != 0) return;
+    uint64_t lu = blockIdx.x;
+    int lk = 0, lstage = 0;
+    uint32_t lphase = 0;
+    int rc[2] = {0, 0};
+    TgUnit lt{};
+    auto load_unit = [&]() {
+      lt = (ts.small && !ts.chunk_major) ? tg_decode32(ts, static_cast<uint32_t>(lu))
+                                         : tg_decode(bs, lu, ts.chunk_major);
+      uint64_t v = lt.rest;
+#pragma unroll
+      for (int i = 1; i >= 0; --i) {
+        if (i < ts.nrest) {
+          const uint64_t q = fdiv(v, p.gdiv[i]);
+          rc[i] = static_cast<int>(v - q * p.gdiv[i].d);
+          v = q;
+        }
+      }
+    };
+    if (lu < units) load_unit();
+    for (;;) {
+      // every consumer warp has released it (asleep meanwhile: a spinning
+      // probe here took ~25% of the SM's issue slots)
+      if (wait_mode >= 1)
+        mbar_wait_sleep(&empty[lstage], lphase ^ 1);
+      else
+        mbar_wait(&empty[lstage], lphase ^ 1);
+      if (lu >= units) {
+        stage_unit[lstage] = ~uint64_t{0};
+        mbar_arrive(&full[lstage]);
+        break;
+      }
+      stage_unit[lstage] = lu;
+      mbar_arrive_expect_tx(&full[lstage], kStage * sizeof(double));
+      double* st = tsm + lstage * kStage;
+      const int j0 = static_cast<int>(lt.chunk * SL);
+      tma_load_5d(st, &mapA, j0, static_cast<int>(lt.pb * PB), lk * kTgSteps,
+                  ts.a_act[0] ? rc[0] : 0, ts.a_act[1] ? rc[1] : 0, &full[lstage]);
+      tma_load_5d(st + kA, &mapB, j0, static_cast<int>(lt.qb * BC), lk * kTgSteps,
+                  ts.b_act[0] ? rc[0] : 0, ts.b_act[1] ? rc[1] : 0, &full[lstage]);
+      if (++lstage == kTgStages) {
+        lstage = 0;
+        lphase ^= 1;
+      }
+      if (++lk == nst) {
+        lk = 0;
+        lu = sched ? gridDim.x + atomicAdd(&sched[0], 1u) : lu + gridDim.x;
+        if (lu < units) load_unit();
+      }
+    }
+    // the last CTA done taking units leaves the queue counters at zero
+    if (sched) {
+      __threadfence();
+      if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
+        sched[0] = 0;
+        sched[1] = 0;
+        __threadfence();
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  const int sub = warp * (32 / SL) + lane / SL, slot = lane % SL;
+  const int r0 = (sub / (BC / SC)) * 8, c0 = (sub % (BC / SC)) * SC;
+  const int64_t rstep = bs.out_ia * s;
+  int64_t coff[SC];
+#pragma unroll
+  for (int k = 0; k < SC; ++k) coff[k] = k * bs.out_ib * s;
+  const uint64_t keep = policy_evict_last();
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    if (wait_mode >= 2)
+      mbar_wait_sleep(&full[stage], phase);
+    else
+      mbar_wait(&full[stage], phase);
+    const uint64_t u = stage_unit[stage];
+    if (u == ~uint64_t{0}) break;
+    const TgUnit t = (ts.small && !ts.chunk_major) ? tg_decode32(ts, static_cast<uint32_t>(u))
+                                                   : tg_decode(bs, u, ts.chunk_major);
+    const int np = static_cast<int>(bs.ext_ia - t.pb * PB < PB ? bs.ext_ia - t.pb * PB : PB);
+    const int nq = static_cast<int>(bs.ext_ib - t.qb * BC < BC ? bs.ext_ib - t.qb * BC : BC);
+    // a sub-block wholly outside a partial edge block folds nothing (its
+    // rows / columns are TMA zero fill and never stored)
+    const bool idle = r0 >= np || c0 >= nq;
+    double acc[8][SC];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int k = 0; k < SC; ++k) acc[i][k] = -0.0;  // exact identity: -0 + x == x
+    auto fold_step = [&](const double* sA, const double* sB) {
+      double a[8], b[SC];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = sA[i * SL];
+#pragma unroll
+      for (int k = 0; k < SC; ++k) b[k] = sB[k * SL];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int k = 0; k < SC; ++k) acc[i][k] = dadd(acc[i][k], dmul(a[i], b[k]));
+    };
+    for (int k = 0; k < nst; ++k) {
+      if (k > 0) {
+        if (wait_mode >= 2)
+          mbar_wait_sleep(&full[stage], phase);
+        else
+          mbar_wait(&full[stage], phase);
+      }
+      if (!idle) {
+        const double* sA = tsm + stage * kStage + r0 * SL + slot;
+        const double* sB = tsm + stage * kStage + kA + c0 * SL + slot;
+        const int nsteps = cnt - k * kTgSteps;
+        if (nsteps >= kTgSteps) {
+#pragma unroll
+          for (int h = 0; h < kTgSteps; ++h) fold_step(sA + h * PB * SL, sB + h * BC * SL);
+        } else {
+          for (int h = 0; h < nsteps; ++h) fold_step(sA + h * PB * SL, sB + h * BC * SL);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kTgStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (idle) continue;
+    const int64_t gout = ts.nrest ? group_base(p, t.rest).out : 0;
+    double* orow = OUT + (gout + (t.pb * PB + r0) * bs.out_ia + (t.qb * BC + c0) * bs.out_ib) * s +
+                   t.chunk * SL + slot;
+    if (np == PB && nq == BC) {  // interior block: no bounds tests
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+#pragma unroll
+        for (int k = 0; k < SC; ++k) st_keep(orow + coff[k], acc[i][k], keep);
+        orow += rstep;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (r0 + i < np) {
+#pragma unroll
+          for (int k = 0; k < SC; ++k)
+            if (c0 + k < nq) st_keep(orow + coff[k], acc[i][k], keep);
+        }
+        orow += rstep;
+      }
+    }
+  }
+}

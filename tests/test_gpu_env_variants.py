@@ -57,6 +57,15 @@ VARIANTS = [
     {"TT_GEMM_CFG": "4"},
     {"TT_GEMM_CFG": "5"},
     {"TT_GEMM_CFG": "6"},
+    {"TT_GEMM_CFG": "7"},
+    {"TT_GEMM_CFG": "8"},
+    {"TT_GEMM_CFG": "9"},
+    {"TT_GEMM_CFG": "10"},
+    {"TT_GEMM_CFG": "11"},
+    {"TT_GEMM_WAIT": "0"},
+    {"TT_GEMM_WAIT": "2"},
+    {"TT_GEMM_GRID": "200"},
+    {"TT_GEMM_CFG": "11", "TT_GEMM_DYNAMIC": "0"},
     {"TT_TREE_SMEM": "1"},
     {"TT_ROW_ROWS": "32"},
     {"TT_ROW_ROWS": "64"},
