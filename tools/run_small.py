@@ -23,6 +23,13 @@ elif which == "c2":
     V = tt.pack(c2.tensors["V"], tt.parse_shape(c2.shapes["V"]), S)
     for _ in range(3):
         tt.matvec_a(M, V)
+elif which == "c4f":  # one call per layer (tt_mul_sum_affine), as the bench
+    c4 = configs.config4(True)
+    S = tt.Session(8192, 8)
+    T = {k: tt.pack(c4.tensors[k], tt.parse_shape(v), S) for k, v in c4.shapes.items()}
+    for _ in range(2):
+        h = tt.tt_mul_sum_affine(T["W1t"], T["X"], 1, T["b1"], square=True)
+        tt.tt_mul_sum_affine(T["W2"], h, 2, T["b2"])
 else:
     c4 = configs.config4(True)
     S = tt.Session(8192, 8)
