@@ -145,3 +145,56 @@ def test_square_exhausts_depth(gpu):
     # without the square the stage itself is fine
     _check(S, a, b, 2, c, False)
 
+
+
+def _pack_random(S, shape, nrng):
+    ext = tuple(d.n for d in shape.dims())
+    return tt.pack(nrng.uniform(-2, 2, size=ext), shape, S)
+
+
+@pytest.mark.parametrize("s", [16, 64, 512, 8192])
+def test_random_shapes_match_composition(gpu, s):
+    """Random operand pairs (the reference's random_pack_shape / partner draws),
+    every summed dim, random bias partners of the sum's shape (compatible or
+    not) and square on/off: the fused call equals the composition in tiles,
+    shape, chain, counters -- or raises the same error."""
+    import random
+    from shapes import partner_shape, random_pack_shape
+    rng = random.Random(9000 + s)
+    nrng = np.random.default_rng(s)
+    S = tt.Session(s, 8)
+    runs = errors = 0
+    for _ in range(40 if s < 8192 else 12):
+        sa = random_pack_shape(rng, s, rng.randint(1, 3))
+        sb = partner_shape(rng, sa)
+        a, b = _pack_random(S, sa, nrng), _pack_random(S, sb, nrng)
+        dim = rng.randint(1, sa.rank())
+        try:
+            so = tt.sum_result_shape(tt.elementwise_result_shape(sa, sb, tt.OpKind.mul), dim)
+        except tt.ShapeError:
+            continue
+        plain = tt.TileTensorShape([tt.DimSpec(d.n, d.d, d.t) for d in so.dims()])
+        sc = partner_shape(rng, plain)
+        c = _pack_random(S, sc, nrng)
+        square = rng.random() < 0.5
+        S.reset_counters()
+        try:
+            want = _compose(a, b, dim, c, square)
+            werr = None
+        except (tt.ShapeError, tt.DepthExhaustedError) as e:
+            want, werr = None, e
+        want_cost = S.cost_report()
+        S.reset_counters()
+        if werr is not None:
+            with pytest.raises(type(werr)) as ge:
+                tt.tt_mul_sum_affine(a, b, dim, c, square=square)
+            assert str(ge.value) == str(werr)
+            errors += 1
+            continue
+        got = tt.tt_mul_sum_affine(a, b, dim, c, square=square)
+        assert S.cost_report() == want_cost
+        assert tt.format_shape(got.shape()) == tt.format_shape(want.shape())
+        assert got.chain_index() == want.chain_index()
+        assert bitwise_equal(got.tiles(), want.tiles()), (tt.format_shape(sa), tt.format_shape(sb), dim)
+        runs += 1
+    assert runs >= 5
