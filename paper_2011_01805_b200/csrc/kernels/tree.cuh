@@ -66,7 +66,7 @@ __device__ __forceinline__ void row_shift(double (&v)[NR], int D) {
 // rotations by -d (replicate schedules) into the forward offsets d handled here.
 // EPI: the reduction's elementwise tail (+ C, square) applied before the store.
 template <int HR, int R = 16, bool BACK = false, bool EPI = false>
-__global__ void __launch_bounds__(256) row_tree_kernel(const double* __restrict__ in,
+__global__ void __launch_bounds__(256, (HR <= 8 ? 3 : 2)) row_tree_kernel(const double* __restrict__ in,
                                                        double* __restrict__ out, int64_t n_tiles,
                                                        int64_t s, int nlevels, int4 lv0, int4 lv1,
                                                        const __grid_constant__ EpiDev epi) {
