@@ -303,21 +303,50 @@ __global__ void __launch_bounds__(256) clean_chunk_kernel(const __grid_constant_
           const int64_t k = u * 256 + threadIdx.x;
           if (2 * k < n) x[u] = __ldg(s2 + k);
         }
+        if (n == kCleanChunk && g.tile_slots == g.s) {
+          // h = base + 512 u + o with o = 2 tid + e < 512 and base + 512 u a
+          // multiple of 512, so the coordinate of a cut dim with stride 2^sh
+          // splits into an item/u part and a per-thread part:
+          //   sh <= 9: ((base + 512 u) >> sh) + (o >> sh)   (no carry)
+          //   sh >  9: (base + 512 u) >> sh                  (o below bit 9)
+          // Per thread the o-parts are fixed; per u one shift per dim.
+          int ob[RK][2];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t k = u * 256 + threadIdx.x;
-          if (2 * k < n) {
-            double m[2];
+          for (int i = 0; i < RK; ++i)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int64_t h = base + 2 * k + e;
-              bool ok = h < g.tile_slots;
+            for (int e = 0; e < 2; ++e) ob[i][e] = sh[i] <= 9 ? (2 * static_cast<int>(threadIdx.x) + e) >> sh[i] : 0;
 #pragma unroll
-              for (int i = 0; i < RK; ++i)
-                if (cut[i]) ok = ok && ((h >> sh[i]) & (g.t[i] - 1)) < v[i];
-              m[e] = ok ? 1.0 : 0.0;
+          for (int u = 0; u < U; ++u) {
+            const int64_t k = u * 256 + threadIdx.x;
+            const int64_t hu = base + 512 * u;
+            bool ok0 = true, ok1 = true;
+#pragma unroll
+            for (int i = 0; i < RK; ++i) {
+              if (cut[i]) {
+                const int64_t a = hu >> sh[i];
+                ok0 = ok0 && ((a + ob[i][0]) & (g.t[i] - 1)) < v[i];
+                ok1 = ok1 && ((a + ob[i][1]) & (g.t[i] - 1)) < v[i];
+              }
             }
-            d2[k] = make_double2(dmul(x[u].x, m[0]), dmul(x[u].y, m[1]));
+            d2[k] = make_double2(dmul(x[u].x, ok0 ? 1.0 : 0.0), dmul(x[u].y, ok1 ? 1.0 : 0.0));
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t k = u * 256 + threadIdx.x;
+            if (2 * k < n) {
+              double m[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int64_t h = base + 2 * k + e;
+                bool ok = h < g.tile_slots;
+#pragma unroll
+                for (int i = 0; i < RK; ++i)
+                  if (cut[i]) ok = ok && ((h >> sh[i]) & (g.t[i] - 1)) < v[i];
+                m[e] = ok ? 1.0 : 0.0;
+              }
+              d2[k] = make_double2(dmul(x[u].x, m[0]), dmul(x[u].y, m[1]));
+            }
           }
         }
       } else {

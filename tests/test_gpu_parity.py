@@ -188,8 +188,15 @@ def test_mul_sum_matches_composition(gpu, oracle):
 
 def test_clean_and_replicate(gpu, oracle):
     nrng = np.random.default_rng(107)
+    # the first four: small tiles; the rest: 4096-slot chunks of the chunked
+    # clean kernel with cut dims of in-tile stride below, at and above 512
+    # slots (its per-thread / per-chunk split of the mask coordinates)
     for text, s in [("[5/2,1?/4]", 8), ("[18?/8,4/16]", 128), ("[3?/4,2/2,7?/4]", 32),
-                    ("[1?/8,3/4]", 32)]:
+                    ("[1?/8,3/4]", 32),
+                    ("[40/16,70/32,1?/32]", 16384), ("[40/16,1?/32,70/32]", 16384),
+                    ("[1?/16,70/32,40/32]", 16384), ("[20?/16,3?/32,7?/32]", 16384),
+                    ("[9/8,5?/16,100?/32]", 4096), ("[13?/64,2/2,19?/32]", 4096),
+                    ("[3/4,5?/1024,2?/4]", 16384)]:
         shape = parse_shape(text)
         S = session(s)
         tiles = nrng.uniform(-5, 5, size=(shape.tile_count(), s))
