@@ -720,3 +720,23 @@ def test_odd_and_tiny_slot_counts(gpu, oracle):
                 want = np.roll(ta, -r, axis=1)
                 got = tt.tiles_rotate(S, ta, off)
                 assert_bitwise(got.detach().cpu().numpy(), want, f"rotate s={s} off={off}")
+
+
+def test_interleaved_kats_on_gpu(gpu):
+    """The `~` known answers of tests/test_shape_algebra.py through the CUDA pack /
+    unpack and the fused fold + tree (no oracle involved: hand-worked values)."""
+    from test_shape_algebra import INTERLEAVED_KATS
+    for text, dense, want in INTERLEAVED_KATS:
+        sh = parse_shape(text)
+        s = len(want[0])
+        S = session(s)
+        t = tt.pack(np.asarray(dense, dtype=np.float64), sh, S)
+        assert t.tiles().tolist() == [[float(v) for v in row] for row in want], text
+        assert tt.unpack(t).tolist() == np.asarray(dense, dtype=np.float64).tolist()
+    S = session(4)
+    S.reset_counters()
+    r = tt.tt_sum(tt.pack(np.arange(1, 9, dtype=np.float64), parse_shape("[8~/4]"), S), 1)
+    assert tt.format_shape(r.shape()) == "[*/4]"
+    assert r.tiles().tolist() == [[36.0, 36.0, 36.0, 36.0]]
+    c = S.cost_report()
+    assert (c.additions, c.rotations) == (3, 2)

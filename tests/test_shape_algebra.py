@@ -7,6 +7,8 @@ itself when oracle/_ref is built).
 """
 import random
 
+import numpy as np
+
 import pytest
 
 import paper_2011_01805_b200 as tt
@@ -216,3 +218,37 @@ def test_interleaved_notation():
         elementwise_result_shape(parse_shape("[8~/4]"), parse_shape("[8/4]"), OpKind.add)
     assert format_shape(elementwise_result_shape(parse_shape("[8~/4]"), parse_shape("[*/4]"),
                                                  OpKind.mul)) == "[8~/4]"
+
+
+# Known answers of the builder's `~` tiling, worked by
+# hand: element j of an n~/t dim with e = ceil(n/t) external tiles sits in tile
+# j mod e at in-tile coordinate j div e; slots past n stay +0.0.
+INTERLEAVED_KATS = [
+    # (shape, dense values, expected tiles)
+    ("[10~/4]", list(range(10)), [[0, 3, 6, 9], [1, 4, 7, 0], [2, 5, 8, 0]]),
+    ("[8~/4]", list(range(1, 9)), [[1, 3, 5, 7], [2, 4, 6, 8]]),
+    # 2-D: dim 1 plain [3/2] (tiles by rows 0-1, 2), dim 2 interleaved [5~/2] (e = 3)
+    ("[3/2,5~/2]", [[r * 10 + c for c in range(5)] for r in range(3)],
+     [[0, 3, 10, 13], [1, 4, 11, 14], [2, 0, 12, 0],
+      [20, 23, 0, 0], [21, 24, 0, 0], [22, 0, 0, 0]]),
+]
+
+
+@pytest.mark.parametrize("text,dense,want", INTERLEAVED_KATS)
+def test_interleaved_pack_kats(oracle, text, dense, want):
+    sh = parse_shape(text)
+    s = len(want[0])
+    got = oracle.pack(np.asarray(dense, dtype=np.float64), sh, s)
+    assert got.tolist() == [[float(v) for v in row] for row in want]
+    assert oracle.unpack(sh, s, got).tolist() == np.asarray(dense, dtype=np.float64).tolist()
+
+
+def test_interleaved_sum_kat(oracle):
+    """tt_sum over a `~` dim: the external fold adds the e tiles in order, then the
+    in-tile power-of-two tree; [8~/4] holding 1..8 -> every slot 36, shape [*/4]."""
+    sh = parse_shape("[8~/4]")
+    tiles = oracle.pack(np.arange(1, 9, dtype=np.float64), sh, 4)
+    so, out, cost = oracle.sum(sh, tiles, 4, 1)
+    assert format_shape(so) == "[*/4]"
+    assert out.tolist() == [[36.0, 36.0, 36.0, 36.0]]
+    assert (cost.additions, cost.rotations) == (1 + 2, 2)
