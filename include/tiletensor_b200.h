@@ -245,6 +245,18 @@ int tt_fold_shape(const tt_shape* a, const tt_shape* b, int dim, tt_shape* out);
 int tt_batch_affine(tt_session* s, const double* in, int64_t n_in, int64_t n_out,
                     const int64_t* row_ptr, const int64_t* src, const double* w,
                     const double* bias, double* out, int64_t chain_in, int64_t* chain_out);
+/* The same layer uploaded once and kept on the device (repeated inference with
+ * fixed weights: no per-call validation, tap-list scan or H2D).  create takes
+ * the arguments of tt_batch_affine (host arrays, same checks and errors);
+ * apply runs it with tt_batch_affine's semantics, counters and chain rule;
+ * destroy frees it (after the session's queued work that uses it). */
+typedef struct tt_affine_layer tt_affine_layer;
+int tt_affine_layer_create(tt_session* s, int64_t n_in, int64_t n_out, const int64_t* row_ptr,
+                           const int64_t* src, const double* w, const double* bias,
+                           tt_affine_layer** out);
+int tt_affine_layer_apply(tt_session* s, const tt_affine_layer* layer, const double* in,
+                          double* out, int64_t chain_in, int64_t* chain_out);
+void tt_affine_layer_destroy(tt_session* s, tt_affine_layer* layer);
 
 /* ---- diagnostics ------------------------------------------------------- */
 /* Force the reduction kernel path (tests / A-B measurement): 0 = best

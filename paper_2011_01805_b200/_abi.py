@@ -86,6 +86,9 @@ SIGNATURES = {
     "tt_replicate_dim": (_I, [_P, _SP, _P, _I, _SP, _P]),
     "tt_tiles_binary": (_I, [_P, _I, _P, _P, _P, _I64, _I64P, _I64P, _I64P]),
     "tt_batch_affine": (_I, [_P, _P, _I64, _I64, _P, _P, _P, _P, _P, _I64, _I64P]),
+    "tt_affine_layer_create": (_I, [_P, _I64, _I64, _P, _P, _P, _P, _P]),
+    "tt_affine_layer_apply": (_I, [_P, _P, _P, _P, _I64, _I64P]),
+    "tt_affine_layer_destroy": (None, [_P, _P]),
     "tt_mul_fold": (_I, [_P, _P, _P, _I64, _P, _P, _I64, _I, _I64, _I64, _P, _P, _I64P]),
     "tt_fold_shape": (_I, [_P, _P, _I, _P]),
     "tt_tiles_mask_mul": (_I, [_P, _P, _P, _P, _I64, _I64P, _I64P]),

@@ -960,6 +960,122 @@ int tt_batch_affine(tt_session* s, const double* in, int64_t n_in, int64_t n_out
   });
 }
 
+}  // extern "C"
+
+struct tt_affine_layer {
+  int device = 0;
+  int64_t n_in = 0, n_out = 0, nnz = 0;
+  int block = 1;
+  unsigned char* dev = nullptr;  // row_ptr | src | w | bias
+  const int64_t* d_rp = nullptr;
+  const int64_t* d_src = nullptr;
+  const double* d_w = nullptr;
+  const double* d_bias = nullptr;
+};
+
+namespace {
+
+void check_affine_layer(int64_t n_in, int64_t n_out, const int64_t* row_ptr, const int64_t* src,
+                        const double* w, const double* bias) {
+  if (n_in < 0 || n_out < 0) invalid_argument("negative tile count");
+  if (n_out > 0 && (!row_ptr || !bias)) invalid_argument("null layer arrays");
+  if (n_out > 0 && row_ptr[0] != 0) invalid_argument("row_ptr must start at 0");
+  for (int64_t o = 0; o < n_out; ++o)
+    if (row_ptr[o + 1] < row_ptr[o]) invalid_argument("row_ptr must be non-decreasing");
+  const int64_t nnz = n_out > 0 ? row_ptr[n_out] : 0;
+  if (nnz > 0 && (!src || !w)) invalid_argument("null tap arrays");
+  for (int64_t k = 0; k < nnz; ++k)
+    if (src[k] < 0 || src[k] >= n_in) invalid_argument("tap source tile out of range");
+}
+
+// largest block (<= 8) of consecutive rows sharing one source list
+int affine_block(int64_t n_out, const int64_t* row_ptr, const int64_t* src) {
+  for (int cand : {8, 5, 4, 2}) {
+    bool ok = true;
+    for (int64_t o0 = 0; o0 < n_out && ok; o0 += cand) {
+      const int64_t len = row_ptr[o0 + 1] - row_ptr[o0];
+      for (int64_t r = o0 + 1; r < std::min<int64_t>(o0 + cand, n_out) && ok; ++r)
+        ok = row_ptr[r + 1] - row_ptr[r] == len &&
+             std::equal(src + row_ptr[r], src + row_ptr[r] + len, src + row_ptr[o0]);
+    }
+    if (ok) return cand;
+  }
+  return 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tt_affine_layer_create(tt_session* s, int64_t n_in, int64_t n_out, const int64_t* row_ptr,
+                           const int64_t* src, const double* w, const double* bias,
+                           tt_affine_layer** out) {
+  return guarded([&] {
+    need_session(s);
+    if (!out) invalid_argument("null layer handle");
+    check_affine_layer(n_in, n_out, row_ptr, src, w, bias);
+    auto* L = new tt_affine_layer;
+    L->device = s->device;
+    L->n_in = n_in;
+    L->n_out = n_out;
+    L->nnz = n_out > 0 ? row_ptr[n_out] : 0;
+    if (n_out > 0) {
+      L->block = affine_block(n_out, row_ptr, src);
+      const size_t b_rp = static_cast<size_t>(n_out + 1) * sizeof(int64_t);
+      const size_t b_src = static_cast<size_t>(L->nnz) * sizeof(int64_t);
+      const size_t b_w = static_cast<size_t>(L->nnz) * sizeof(double);
+      const size_t b_bias = static_cast<size_t>(n_out) * sizeof(double);
+      try {
+        check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+        check_cuda(cudaMalloc(&L->dev, b_rp + b_src + b_w + b_bias), "layer allocation");
+        L->d_rp = reinterpret_cast<const int64_t*>(L->dev);
+        L->d_src = reinterpret_cast<const int64_t*>(L->dev + b_rp);
+        L->d_w = reinterpret_cast<const double*>(L->dev + b_rp + b_src);
+        L->d_bias = reinterpret_cast<const double*>(L->dev + b_rp + b_src + b_w);
+        check_cuda(cudaMemcpy(L->dev, row_ptr, b_rp, cudaMemcpyHostToDevice), "layer upload");
+        if (L->nnz > 0) {
+          check_cuda(cudaMemcpy(L->dev + b_rp, src, b_src, cudaMemcpyHostToDevice), "layer upload");
+          check_cuda(cudaMemcpy(L->dev + b_rp + b_src, w, b_w, cudaMemcpyHostToDevice), "layer upload");
+        }
+        check_cuda(cudaMemcpy(L->dev + b_rp + b_src + b_w, bias, b_bias, cudaMemcpyHostToDevice),
+                   "layer upload");
+      } catch (...) {
+        if (L->dev) cudaFree(L->dev);
+        delete L;
+        throw;
+      }
+    }
+    *out = L;
+  });
+}
+
+int tt_affine_layer_apply(tt_session* s, const tt_affine_layer* L, const double* in, double* out,
+                          int64_t chain_in, int64_t* chain_out) {
+  return guarded([&] {
+    need_session(s);
+    if (!L) invalid_argument("null layer");
+    if (L->device != s->device) invalid_argument("layer belongs to another device");
+    if (L->n_in > 0 && L->n_out > 0 && in && out && out < in + L->n_in * s->slots &&
+        in < out + L->n_out * s->slots)
+      invalid_argument("batch affine output must not overlap its input");
+    if (L->nnz > 0 && chain_in < 1) depth_error("multiplication at chain index 0 (bootstrap required)");
+    if (chain_out) *chain_out = L->nnz > 0 ? chain_in - 1 : s->depth;
+    s->muls += static_cast<uint64_t>(L->nnz);
+    s->adds += static_cast<uint64_t>(L->nnz);
+    if (L->n_out == 0) return;
+    std::lock_guard<std::mutex> lk(s->mu);
+    launch_batch_affine(ctx_of(s), in, s->slots, L->n_out, L->d_rp, L->d_src, L->d_w, L->d_bias, out,
+                        L->block);
+  });
+}
+
+void tt_affine_layer_destroy(tt_session* s, tt_affine_layer* L) {
+  if (!L) return;
+  if (s && s->stream) cudaStreamSynchronize(s->stream);
+  if (L->dev) cudaFree(L->dev);
+  delete L;
+}
+
 int tt_tiles_mask_mul(tt_session* s, const double* a, const double* mask, double* out,
                       int64_t n_tiles, const int64_t* chain_a, int64_t* chain_out) {
   return guarded([&] {

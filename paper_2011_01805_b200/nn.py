@@ -352,10 +352,61 @@ def _batch_affine(session: tt.Session, data, chain: int, n_in: int, row_ptr, src
     return out[:n_out], co.value
 
 
-def infer_batch_packed(net: NetworkSpec, batch: np.ndarray, session: tt.Session) -> InferResult:
-    """nn.hpp:270-346: every network scalar is one tile carrying it for all
-    samples; each conv / fc layer is ONE device pass (tt_batch_affine) that
-    folds bias + w * x in the reference's order; zero rotations."""
+def _batch_packed_plan(net: NetworkSpec) -> list:
+    """The batch-packed branch's layers as device work: ("affine", n_in, row_ptr,
+    src, w, bias) -- one tt_batch_affine pass, taps in the reference's order --
+    or ("square",).  Layer-size errors are raised when the layer is reached."""
+    plan = []
+    n_tiles = net.input_size()
+    for layer in net.layers:
+        if isinstance(layer, ConvLayer):
+            c = layer
+            h, w = net.input_h, net.input_w
+            idx = _im2col_index(h, w, c.kh, c.kw, c.stride, c.pad)  # [windows, kk]
+            windows, kk = idx.shape
+            # output (window, filter): taps over (ky, kx) in order, padding skipped
+            valid = idx >= 0
+            counts = np.repeat(valid.sum(axis=1), c.filters)
+            row_ptr = np.concatenate([[0], np.cumsum(counts)])
+            src = np.concatenate([np.tile(idx[wi][valid[wi]], c.filters) for wi in range(windows)])
+            wts = np.concatenate([c.weights[:, valid[wi]].reshape(-1) for wi in range(windows)])
+            bias = np.tile(c.bias, windows)
+            plan.append(("affine", h * w, row_ptr, src, wts, bias))
+            n_tiles = len(bias)
+        elif isinstance(layer, FcLayer):
+            f = layer
+            if n_tiles != f.inp:
+                plan.append(("error", ShapeError("fc input size mismatch")))
+                break
+            row_ptr = np.arange(f.out + 1, dtype=np.int64) * f.inp
+            src = np.tile(np.arange(f.inp, dtype=np.int64), f.out)
+            plan.append(("affine", f.inp, row_ptr, src, np.asarray(f.weights).reshape(-1),
+                         np.asarray(f.bias)))
+            n_tiles = f.out
+        elif isinstance(layer, SquareLayer):
+            plan.append(("square",))
+        else:
+            plan.append(("error", ShapeError("unsupported layer for inference")))
+            break
+    return plan
+
+
+def _arrays(row_ptr, src, w, bias):
+    return (np.ascontiguousarray(row_ptr, dtype=np.int64), np.ascontiguousarray(src, dtype=np.int64),
+            np.ascontiguousarray(w, dtype=np.float64), np.ascontiguousarray(bias, dtype=np.float64))
+
+
+def _square(session: tt.Session, data, chain: int):
+    # session.mul(t, t) per tile (chains are uniform across the layer)
+    if chain < 1:
+        raise DepthExhaustedError("multiplication at chain index 0 (bootstrap required)")
+    out = session.empty_tiles(data.shape[0])
+    _check(lib().tt_tiles_binary(session.handle, int(tt.OpKind.mul), _ptr(data), _ptr(data),
+                                 _ptr(out), int(data.shape[0]), None, None, None))
+    return out, chain - 1
+
+
+def _run_batch_packed(plan: list, batch, session: tt.Session, affine) -> InferResult:
     before = session.cost_report()
     if not _is_torch(batch):  # a device-resident torch batch is packed in place (no host copy)
         batch = np.asarray(batch, dtype=np.float64)
@@ -364,45 +415,89 @@ def infer_batch_packed(net: NetworkSpec, batch: np.ndarray, session: tt.Session)
     packed = tt.pack(batch, TileTensorShape([DimSpec(int(batch.shape[0]), 1, 1), DimSpec(n, 1, s)]),
                      session)
     data, chain = packed.data(), packed.chain_index()
-    for layer_no, layer in enumerate(net.layers, start=1):
+    for layer_no, step in enumerate(plan, start=1):
         try:
-            if isinstance(layer, ConvLayer):
-                c = layer
-                h, w = net.input_h, net.input_w
-                idx = _im2col_index(h, w, c.kh, c.kw, c.stride, c.pad)  # [windows, kk]
-                windows, kk = idx.shape
-                # output (window, filter): taps over (ky, kx) in order, padding skipped
-                valid = idx >= 0
-                counts = np.repeat(valid.sum(axis=1), c.filters)
-                row_ptr = np.concatenate([[0], np.cumsum(counts)])
-                src = np.concatenate([np.tile(idx[wi][valid[wi]], c.filters) for wi in range(windows)])
-                wts = np.concatenate([c.weights[:, valid[wi]].reshape(-1) for wi in range(windows)])
-                bias = np.tile(c.bias, windows)
-                data, chain = _batch_affine(session, data, chain, h * w, row_ptr, src, wts, bias)
-            elif isinstance(layer, FcLayer):
-                f = layer
-                if data.shape[0] != f.inp:
-                    raise ShapeError("fc input size mismatch")
-                row_ptr = np.arange(f.out + 1, dtype=np.int64) * f.inp
-                src = np.tile(np.arange(f.inp, dtype=np.int64), f.out)
-                data, chain = _batch_affine(session, data, chain, f.inp, row_ptr, src,
-                                            np.asarray(f.weights).reshape(-1), f.bias)
-            elif isinstance(layer, SquareLayer):
-                # session.mul(t, t) per tile (chains are uniform across the layer)
-                if chain < 1:
-                    raise DepthExhaustedError("multiplication at chain index 0 (bootstrap required)")
-                out = session.empty_tiles(data.shape[0])
-                _check(lib().tt_tiles_binary(session.handle, int(tt.OpKind.mul), _ptr(data),
-                                             _ptr(data), _ptr(out), int(data.shape[0]), None, None,
-                                             None))
-                data, chain = out, chain - 1
+            if step[0] == "affine":
+                data, chain = affine(layer_no - 1, step, data, chain)
+            elif step[0] == "square":
+                data, chain = _square(session, data, chain)
             else:
-                raise ShapeError("unsupported layer for inference")
+                raise step[1]
         except DepthExhaustedError as e:
             raise DepthExhaustedError(f"layer {layer_no}: {e}") from None
     shape = TileTensorShape([DimSpec(int(data.shape[0]), 1, 1), DimSpec(n, 1, s)])
     logits = tt.unpack(TileTensor(shape, data, session, chain))
     return InferResult(logits, session.cost_report().since(before))
+
+
+def infer_batch_packed(net: NetworkSpec, batch: np.ndarray, session: tt.Session) -> InferResult:
+    """nn.hpp:270-346: every network scalar is one tile carrying it for all
+    samples; each conv / fc layer is ONE device pass (tt_batch_affine) that
+    folds bias + w * x in the reference's order; zero rotations."""
+    if int(batch.shape[0]) != net.input_size():
+        raise ShapeError("batch feature size mismatch")
+
+    def affine(i, step, data, chain):
+        _, n_in, row_ptr, src, w, bias = step
+        if data.shape[0] != n_in:
+            raise ShapeError("fc input size mismatch")
+        return _batch_affine(session, data, chain, n_in, row_ptr, src, w, bias)
+    return _run_batch_packed(_batch_packed_plan(net), batch, session, affine)
+
+
+class CompiledBatchPacked:
+    """cryptonets_infer's batch-packed branch (tile [1, 1, s]) for repeated
+    inference with fixed weights: the network's layers are turned into tap lists
+    and uploaded once (tt_affine_layer_create); each infer() is then the pack,
+    one device pass per layer and the unpack.  Logits and counters equal
+    cryptonets_infer(net, batch, (1, 1, s), session) bit for bit.  The weights
+    are captured at construction (later edits to `net` are not seen)."""
+
+    def __init__(self, net: NetworkSpec, session: tt.Session):
+        self.session = session
+        self.plan = _batch_packed_plan(net)
+        self.n_in = net.input_size()
+        self.layers = {}
+        for i, step in enumerate(self.plan):
+            if step[0] != "affine":
+                continue
+            _, n_in, row_ptr, src, w, bias = step
+            rp, sr, ww, bb = _arrays(row_ptr, src, w, bias)
+            h = ctypes.c_void_p()
+            p64, pd = ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)
+            _check(lib().tt_affine_layer_create(session.handle, int(n_in), len(bb),
+                                                rp.ctypes.data_as(p64), sr.ctypes.data_as(p64),
+                                                ww.ctypes.data_as(pd), bb.ctypes.data_as(pd),
+                                                ctypes.byref(h)))
+            self.layers[i] = (h, int(n_in), len(bb))
+
+    def infer(self, batch) -> InferResult:
+        if int(batch.shape[0]) != self.n_in:
+            raise ShapeError("batch feature size mismatch")
+        if int(batch.shape[1]) > self.session.slot_count():
+            raise ShapeError("batch size exceeds the batch tile extent t3")
+
+        def affine(i, step, data, chain):
+            h, n_in, n_out = self.layers[i]
+            if data.shape[0] != n_in:
+                raise ShapeError("fc input size mismatch")
+            out = self.session.empty_tiles(max(n_out, 1))
+            co = ctypes.c_int64()
+            _check(lib().tt_affine_layer_apply(self.session.handle, h, _ptr(data), _ptr(out),
+                                               int(chain), ctypes.byref(co)))
+            return out[:n_out], co.value
+        return _run_batch_packed(self.plan, batch, self.session, affine)
+
+    def close(self) -> None:
+        for h, _, _ in self.layers.values():
+            lib().tt_affine_layer_destroy(self.session.handle, h)
+        self.layers = {}
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],

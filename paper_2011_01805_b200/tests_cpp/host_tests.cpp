@@ -580,6 +580,25 @@ static void nn_suite() {
     const auto bp2 = cryptonets_infer(net, big, {1, 1, 64}, session, true);
     CHECK(bp2.logits.extent(1) == 150 && max_rel_diff(bp2.logits, nn_forward(net, big)) < 1e-6);
   }
+  {  // layers uploaded once: CompiledBatchPacked == cryptonets_infer, bit for bit, every call
+    const NetworkSpec cn = cryptonets_network(7);
+    Session session(256, 8);
+    CompiledBatchPacked comp(cn, session);
+    for (std::int64_t n : {256, 77}) {
+      const DenseTensor batch = random_tensor({784, n}, rng, 0, 1);
+      session.reset_counters();
+      const auto want = cryptonets_infer(cn, batch, {1, 1, 256}, session);
+      const CostReport wc = session.cost_report();
+      session.reset_counters();
+      const auto got = comp.infer(batch);
+      const CostReport gc = session.cost_report();
+      bool same = got.logits.values().size() == want.logits.values().size();
+      for (std::size_t i = 0; same && i < got.logits.values().size(); ++i)
+        same = std::memcmp(&got.logits.values()[i], &want.logits.values()[i], 8) == 0;
+      CHECK(same && gc.additions == wc.additions && gc.multiplications == wc.multiplications);
+    }
+    CHECK_THROWS_AS(comp.infer(random_tensor({783, 4}, rng, 0, 1)), ShapeError);
+  }
   {  // paper-scale counts for tile [32, 256, 1]
     const NetworkSpec cn = cryptonets_network(42);
     const DenseTensor batch = random_tensor({784, 1}, rng, -1, 1);

@@ -86,6 +86,40 @@ def test_cryptonets_batch_packed_full(gpu, ref):
     assert _cost(got.cost) == _cost(wc)
 
 
+def test_compiled_batch_packed(gpu, ref):
+    """CompiledBatchPacked (layers uploaded once) equals the reference's
+    cryptonets_infer bit for bit, call after call, device or host batches;
+    a too-shallow session fails on the same layer with the same message."""
+    import torch
+    net = nn.cryptonets_network(9)
+    S = tt.Session(1024, 8)
+    comp = nn.CompiledBatchPacked(net, S)
+    rng = np.random.default_rng(19)
+    for n in (1024, 300):
+        batch = rng.uniform(0, 1, size=(784, n))
+        want, wc = ref.nn_run(1, nn.CRYPTONETS_SPEC, 9, batch, (1, 1, 1024), 1024, 8)
+        for b in (batch, torch.from_numpy(batch).cuda()):
+            got = comp.infer(b)
+            assert _same(got.logits, want)
+            assert _cost(got.cost) == _cost(wc)
+    small = nn.parse_network(SMALL, "", 43)
+    S2 = tt.Session(64, 8)
+    c2 = nn.CompiledBatchPacked(small, S2)
+    batch = rng.uniform(-1, 1, size=(36, 64))
+    want, wc = ref.nn_run(1, SMALL, 43, batch, (1, 1, 64), 64, 8)
+    got = c2.infer(batch)
+    assert _same(got.logits, want) and _cost(got.cost) == _cost(wc)
+    shallow = tt.Session(64, 2)
+    with pytest.raises(tt.DepthExhaustedError) as e1:
+        nn.cryptonets_infer(small, batch, (1, 1, 64), shallow)
+    with pytest.raises(tt.DepthExhaustedError) as e2:
+        nn.CompiledBatchPacked(small, shallow).infer(batch)
+    assert str(e1.value) == str(e2.value)
+    with pytest.raises(tt.ShapeError):
+        comp.infer(rng.uniform(0, 1, size=(783, 10)))
+    comp.close()
+
+
 def test_error_contracts(gpu):
     net = nn.parse_network(SMALL, "", 45)
     rng = np.random.default_rng(337)

@@ -28,3 +28,16 @@ for s, tile, n in ((8192, (1, 1, 8192), 8192), (8192, (32, 256, 1), 1), (8192, (
     dt = (time.perf_counter() - t0) / reps
     print(f"tile {tile} batch {n}: {dt * 1e3:.2f} ms per call ({n / dt:.0f} samples/s), "
           f"rot={r.cost.rotations} mul={r.cost.multiplications}")
+if "--compiled" in sys.argv:
+    S = tt.Session(8192, 8)
+    batch = torch.from_numpy(np.random.default_rng(1).uniform(0, 1, size=(784, 8192))).cuda()
+    comp = nn.CompiledBatchPacked(net, S)
+    comp.infer(batch)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        r = comp.infer(batch)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 10
+    print(f"compiled batch packed 8192: {dt * 1e3:.3f} ms per call ({8192 / dt:.0f} samples/s)")
+
