@@ -268,9 +268,13 @@ def run_ours(args):
     from paper_2011_01805_b200 import configs
 
     world, rank, local = dist_env()
+    # one process per GPU; more ranks than GPUs only for the gloo functional check
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = init_dist(world, "nccl")
+    # TT_BENCH_BACKEND=gloo: functional check of the N > 1 path with several
+    # ranks on one GPU (NCCL refuses duplicate devices) -- never a measurement
+    dist = init_dist(world, os.environ.get("TT_BENCH_BACKEND", "nccl"))
     stream = torch.cuda.current_stream(dev)
     hbm_peak, peak_src = peaks()
 
@@ -319,16 +323,19 @@ def run_ours(args):
         t_start.record(stream)
         for _ in range(args.steps):
             ev[0].record(stream)
-            partial = None
+            partial, work = None, None
             for k in (1, 2, 3):
                 r = tt.tt_mul_sum(X, W, k)
                 ev[k].record(stream)
                 if k == plan.shard_dim:
                     partial = r
-            if world > 1:
-                # the one real exchange: the dim-1 sum spans the ranks' slabs
-                # (NCCL over NVLink), issued after the per-launch events
-                sharding.allreduce_partial(partial.data())
+                    if world > 1:
+                        # the one real exchange: the dim-1 sum spans the ranks'
+                        # slabs (NCCL over NVLink), in flight while the dim-2
+                        # and dim-3 products run
+                        work = sharding.allreduce_partial(partial.data(), async_op=True)
+            if work is not None:
+                work.wait()
             # the sync below is per step only to read the per-launch events
             ev[3].synchronize()
             per_dim[1].append(ev[0].elapsed_time(ev[1]) / 1e3)

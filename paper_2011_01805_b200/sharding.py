@@ -84,11 +84,15 @@ def _dist():
     return dist if dist.is_available() and dist.is_initialized() else None
 
 
-def allreduce_partial(data, group=None) -> None:
-    """Sum a rank-partial result over all ranks in place (NCCL on GPUs)."""
+def allreduce_partial(data, group=None, async_op: bool = False):
+    """Sum a rank-partial result over all ranks in place (NCCL on GPUs).
+    async_op: return the collective's work handle (None when there is nothing
+    to reduce) so independent kernels can run while it is in flight; the
+    caller waits on it before using `data`."""
     dist = _dist()
     if dist is not None and dist.get_world_size(group) > 1:
-        dist.all_reduce(data, op=dist.ReduceOp.SUM, group=group)
+        return dist.all_reduce(data, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+    return None
 
 
 def broadcast_operand(data, src: int = 0, group=None) -> None:

@@ -59,6 +59,17 @@ def _worker(rank, world, port, out_dir):
         r, sharded = sharding.sharded_mul_sum(tx, wt.numpy(), dim, plan, mul_sum, lambda t: t)
         results[f"dim{dim}"] = r.numpy()
         results[f"dim{dim}_sharded"] = np.array(sharded)
+    # the bench's form: the dim-1 all-reduce in flight (async) while the
+    # other dims are computed, waited on before use -- same values
+    def mul_sum1(a, b, k):
+        so, out, _ = oracle.mul_sum(plan.local_shape, a, sw, b, S, k)
+        return torch.from_numpy(out.copy())
+    part = mul_sum1(tx, wt.numpy(), 1)
+    work = sharding.allreduce_partial(part, async_op=True)
+    assert work is not None
+    _ = mul_sum1(tx, wt.numpy(), 2)
+    work.wait()
+    results["dim1_async"] = part.numpy()
     results["begin"] = np.array(plan.begin)
     results["end"] = np.array(plan.end)
     np.savez(Path(out_dir) / f"rank{rank}.npz", **results)
@@ -83,6 +94,7 @@ def test_two_rank_gloo(tmp_path, oracle):
             for r in ranks:
                 assert not bool(r["dim1_sharded"])
                 got = r["dim1"]
+                assert np.array_equal(r["dim1_async"].view(np.uint64), got.view(np.uint64))
                 assert got.shape == want.shape
                 assert oracle.max_rel_diff(got, want) < 1e-12
                 # the meaningful (replicated) values agree with the dense sum
