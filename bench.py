@@ -604,16 +604,24 @@ def bench_matmul(tt, configs, S, stream, hbm_peak, reps):
     # the literal chain ("3a"): matmul_a(A, B) -> clean_unknowns -> replicate_dim 2 -> x C^T, sum dim 3
     TA = {k: tt.pack(c3.tensors[k], tt.parse_shape(c3.shapes[k]), S3) for k in ("B3", "Ct3")}
 
-    def chain_3a():
+    def chain_3a_calls():
         ra = tt.matmul_a(T["A3"], TA["B3"])
         rep = tt.replicate_dim(tt.clean_unknowns(ra), 2)
         return tt.tt_mul_sum(rep, TA["Ct3"], 3)
+
+    def chain_3a():  # matmul_a + clean_unknowns as one call (the pipeline seam)
+        rep = tt.replicate_dim(tt.tt_mul_sum_clean(T["A3"], TA["B3"], 2), 2)
+        return tt.tt_mul_sum(rep, TA["Ct3"], 3)
     chain_3a()
+    chain_3a_calls()
     t3a = time_events(chain_3a, reps, stream)
+    t3a_calls = time_events(chain_3a_calls, reps, stream)
     fp64_3a = 2 * 8192 * (32 * 32 * 48 + 32 * 8 * 48)  # product tiles x slots, both products
     out_3a = {"ms": t3a * 1e3, "fp64_tops": fp64_3a / t3a / 1e12, "fp64_frac": fp64_3a / t3a / FP64_PEAK_OPS,
+              "separate_calls_ms": t3a_calls * 1e3,
               "note": "literal config-3 chain: matmul_a(A3, B3) -> clean_unknowns -> replicate_dim(2) "
-                      "-> tt_mul_sum(., Ct3, 3)"}
+                      "-> tt_mul_sum(., Ct3, 3); the first two as one tt_mul_sum_clean call "
+                      "(separate_calls_ms: four calls)"}
     return {"matmul_c3a": out_3a, "matmul_c3b": {"ms": t * 1e3, "GB/s": alg / t / 1e9, "frac": alg / t / 1e9 / hbm_peak,
                            "tile_slots_per_s": prod_tiles * 8192 / t, "alg_bytes": alg,
                            "graph_replay_ms": t_graph * 1e3,

@@ -181,6 +181,14 @@ int tt_mul_sum_affine(tt_session* s, const tt_shape* a, const double* ta, int64_
                       const tt_shape* b, const double* tb, int64_t chain_b, int dim, int variant,
                       const tt_shape* c, const double* tc, int64_t chain_c, int square,
                       tt_shape* out_shape, double* out, int64_t* out_chain);
+/* clean_unknowns(tt_sum(tt_mul(a,b), dim, variant)) tile_tensor.hpp:352-386 --
+ * the odd -> even seam of pipeline() (linalg.hpp:213-260) and of config 3's
+ * literal chain -- with the mask applied in the reduction's last pass.  Shapes,
+ * chain index, counters and errors equal the two-call composition (which runs
+ * as such when the mask is not expressible in the fused pass). */
+int tt_mul_sum_clean(tt_session* s, const tt_shape* a, const double* ta, int64_t chain_a,
+                     const tt_shape* b, const double* tb, int64_t chain_b, int dim, int variant,
+                     tt_shape* out_shape, double* out, int64_t* out_chain);
 /* matvec_a/matvec_b/matmul_a/matmul_b linalg.hpp:41-73 (adds the rank and
  * replication preconditions of linalg.hpp:32-37 to tt_mul_sum).
  * which: 0=matvec_a 1=matvec_b 2=matmul_a 3=matmul_b. */

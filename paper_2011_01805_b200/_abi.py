@@ -80,6 +80,7 @@ SIGNATURES = {
     "tt_sum": (_I, [_P, _SP, _P, _I, _I, _SP, _P]),
     "tt_mul_sum": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64, _I, _I, _SP, _P, _I64P]),
     "tt_linalg_product": (_I, [_P, _I, _SP, _P, _I64, _SP, _P, _I64, _I, _SP, _P, _I64P]),
+    "tt_mul_sum_clean": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64, _I, _I, _SP, _P, _I64P]),
     "tt_mul_sum_affine": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64, _I, _I, _SP, _P, _I64, _I, _SP, _P,
                                _I64P]),
     "tt_clean_unknowns": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64P]),

@@ -36,12 +36,7 @@ __global__ void __launch_bounds__(256) col_tree_kernel(const double* in, double*
 #pragma unroll
       for (int m = 0; m < T; ++m) v[m] = nv[m];
     }
-    if (EPI) {
-      const double* ct = epi_tile(epi, tile, s);
-      if (ct) ct += col;
-#pragma unroll
-      for (int m = 0; m < T; ++m) v[m] = epi_apply(epi, v[m], ct, m * stride);
-    }
+    if (EPI) epi_apply_n<T>(epi, v, epi_tile(epi, tile, s), col, stride);
 #pragma unroll
     for (int m = 0; m < T; ++m) base[(BACK ? T - 1 - m : m) * stride] = v[m];
   }
@@ -113,11 +108,18 @@ __global__ void __launch_bounds__(256, (HR <= 8 ? 3 : 2)) row_tree_kernel(const 
         }
       }
     }
-    const double* ct = EPI ? epi_tile(epi, tile, s) : nullptr;
+    if (EPI) {
+      double w[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) w[i] = v[i];
+      epi_apply_n<R>(epi, w, epi_tile(epi, tile, s), rb * 32 + lane, 32);
+#pragma unroll
+      for (int i = 0; i < R; ++i) v[i] = w[i];
+    }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int64_t p = (rb + i) * 32 + lane;
-      o[BACK ? s - 1 - p : p] = EPI ? epi_apply(epi, v[i], ct, p) : v[i];
+      o[BACK ? s - 1 - p : p] = v[i];
     }
   }
 }
@@ -183,15 +185,17 @@ __global__ void __launch_bounds__(256) epilogue_kernel(double* __restrict__ tile
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t tile = fdiv(w, per_tile);
     const int64_t j = static_cast<int64_t>(w - tile * per_tile.d) * (VEC ? 2 : 1);
-    const double* ct = epi_tile(epi, tile, s);
+    const EpiTile et = epi_tile(epi, tile, s);
     double* t = tiles + tile * s + j;
     if (VEC) {
-      double2 x = *reinterpret_cast<double2*>(t);
-      x.x = epi_apply(epi, x.x, ct, j);
-      x.y = epi_apply(epi, x.y, ct, j + 1);
-      *reinterpret_cast<double2*>(t) = x;
+      const double2 v = *reinterpret_cast<double2*>(t);
+      double x[2] = {v.x, v.y};
+      epi_apply_n<2>(epi, x, et, j, 1);
+      *reinterpret_cast<double2*>(t) = make_double2(x[0], x[1]);
     } else {
-      *t = epi_apply(epi, *t, ct, j);
+      double x[1] = {*t};
+      epi_apply_n<1>(epi, x, et, j, 1);
+      *t = x[0];
     }
   }
 }

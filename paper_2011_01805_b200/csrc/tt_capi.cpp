@@ -711,6 +711,74 @@ int tt_mul_sum_affine(tt_session* s, const tt_shape* a, const double* ta, int64_
   });
 }
 
+int tt_mul_sum_clean(tt_session* s, const tt_shape* a, const double* ta, int64_t chain_a,
+                     const tt_shape* b, const double* tb, int64_t chain_b, int dim, int variant,
+                     tt_shape* out_shape, double* out, int64_t* out_chain) {
+  Shape sa, sb, prod, so;
+  int64_t chain1 = 0;
+  int rc = guarded([&] {
+    need_session(s);
+    sa = from_c(a);
+    sb = from_c(b);
+    prod = elementwise_result_shape(sa, sb, TT_OP_MUL);
+    require_slots(s, sa, "tt_mul");
+    require_slots(s, sb, "tt_mul");
+    check_tiles_addressable(prod);
+    chain1 = mul_chain(chain_a, chain_b);
+    so = sum_result_shape(prod, dim);
+  });
+  if (rc != TT_OK) return rc;
+  if (!so.has_unknown())  // clean_unknowns returns its input as is (tile_tensor.hpp:354)
+    return tt_mul_sum(s, a, ta, chain_a, b, tb, chain_b, dim, variant, out_shape, out, out_chain);
+  // the mask of clean_unknowns (tile_tensor.hpp:364-378) as a reduction
+  // epilogue: cut dims (used < ext * t) need power-of-two extents and strides
+  Epilogue epi;
+  bool fused = so.has_unknown() && chain1 >= 1 && !so.relaxed;
+  const Dim& ds = prod.dims[dim - 1];
+  if (ds.n == 1 && ds.d > 1) fused = false;  // degenerate sum: the product itself
+  if (fused) {
+    const auto ext = so.external();
+    const auto tst = tile_strides(so);
+    epi.nd = static_cast<int>(ext.size());
+    for (int i = 0; i < epi.nd; ++i) epi.ext[i] = ext[i];
+    for (int i = 0; i < so.rank() && fused; ++i) {
+      const Dim& d = so.dims[i];
+      if (d.used() >= ext[i] * d.t) continue;
+      const bool pow2 = (d.t & (d.t - 1)) == 0 && (tst[i] & (tst[i] - 1)) == 0;
+      if (d.interleaved || !pow2 || epi.nmask == kEpiMaskDims) {
+        fused = false;
+        break;
+      }
+      epi.mask_dim[epi.nmask] = i;
+      epi.mask_t[epi.nmask] = d.t;
+      epi.mask_stride[epi.nmask] = tst[i];
+      epi.mask_used[epi.nmask] = d.used();
+      ++epi.nmask;
+    }
+  }
+  if (!fused) {  // the composition: product + sum, then clean_unknowns in place
+    tt_shape mid{};
+    int64_t ch = 0;
+    rc = tt_mul_sum(s, a, ta, chain_a, b, tb, chain_b, dim, variant, &mid, out, &ch);
+    if (rc != TT_OK) return rc;
+    return tt_clean_unknowns(s, &mid, out, ch, out_shape, out, out_chain);
+  }
+  return guarded([&] {
+    s->muls += static_cast<uint64_t>(prod.tile_count());
+    {
+      std::lock_guard<std::mutex> lk(s->mu);
+      std::vector<int64_t> ast, bst;
+      operand_strides(sa, ast);
+      operand_strides(sb, bst);
+      run_reduction(s, prod, dim - 1, variant, ta, ast, tb, bst, out, &epi);
+    }
+    s->masks += static_cast<uint64_t>(so.tile_count());
+    for (auto& d : so.dims) d.unknown = false;
+    to_c(so, out_shape);
+    if (out_chain) *out_chain = chain1 - 1;
+  });
+}
+
 int tt_linalg_product(tt_session* s, int which, const tt_shape* a, const double* ta,
                       int64_t chain_a, const tt_shape* b, const double* tb, int64_t chain_b,
                       int variant, tt_shape* out_shape, double* out, int64_t* out_chain) {

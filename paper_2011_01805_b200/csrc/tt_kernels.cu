@@ -155,6 +155,10 @@ struct EpiDev {
   int square = 0;
   FastDiv64 ext[TT_MAX_RANK];
   int64_t cst[TT_MAX_RANK] = {};
+  // clean_unknowns mask (nmask cut dims; power-of-two extents and strides)
+  int nmask = 0;
+  int msh[kEpiMaskDims] = {}, mdim[kEpiMaskDims] = {};
+  int64_t mtm1[kEpiMaskDims] = {}, mt[kEpiMaskDims] = {}, mused[kEpiMaskDims] = {};
 };
 
 EpiDev make_epi_dev(const Epilogue& e) {
@@ -166,25 +170,77 @@ EpiDev make_epi_dev(const Epilogue& e) {
     d.ext[i] = make_div64(static_cast<uint64_t>(e.ext[i]));
     d.cst[i] = e.c_stride[i];
   }
+  d.nmask = e.nmask;
+  for (int k = 0; k < e.nmask; ++k) {
+    d.mdim[k] = e.mask_dim[k];
+    d.mt[k] = e.mask_t[k];
+    d.mtm1[k] = e.mask_t[k] - 1;
+    d.mused[k] = e.mask_used[k];
+    int sh = 0;
+    while ((int64_t{1} << sh) < e.mask_stride[k]) ++sh;
+    d.msh[k] = sh;
+  }
   return d;
 }
 
-__device__ __forceinline__ const double* epi_tile(const EpiDev& e, uint64_t tile, int64_t s) {
-  if (!e.c) return nullptr;
+// Per output tile: the add operand's tile and, for the mask, the number of
+// used coordinates left in this tile along each cut dim.
+struct EpiTile {
+  const double* ct;
+  int lim[kEpiMaskDims];  // clamped to [0, t]: 32-bit mask arithmetic (slots < 2^31)
+};
+
+__device__ __forceinline__ EpiTile epi_tile(const EpiDev& e, uint64_t tile, int64_t s) {
+  EpiTile t;
+  t.ct = nullptr;
+#pragma unroll
+  for (int k = 0; k < kEpiMaskDims; ++k) t.lim[k] = 0;
+  if (!e.c && !e.nmask) return t;
   int64_t ci = 0;
   for (int i = e.nd - 1; i >= 0; --i) {
     const uint64_t q = fdiv(tile, e.ext[i]);
-    ci += static_cast<int64_t>(tile - q * e.ext[i].d) * e.cst[i];
+    const int64_t l = static_cast<int64_t>(tile - q * e.ext[i].d);
+    ci += l * e.cst[i];
+#pragma unroll
+    for (int k = 0; k < kEpiMaskDims; ++k)
+      if (k < e.nmask && e.mdim[k] == i) {
+        const int64_t left = e.mused[k] - l * e.mt[k];
+        t.lim[k] = static_cast<int>(left < 0 ? 0 : (left > e.mt[k] ? e.mt[k] : left));
+      }
     tile = q;
   }
-  return e.c + ci * s;
+  if (e.c) t.ct = e.c + ci * s;
+  return t;
 }
 
-// tt_add(x, C) then tt_mul(x, x), each separately rounded, as the composition
-__device__ __forceinline__ double epi_apply(const EpiDev& e, double x, const double* ct, int64_t j) {
-  if (ct) x = dadd(x, __ldg(ct + j));
-  if (e.square) x = dmul(x, x);
-  return x;
+// clean_unknowns' x * (0 or 1), then tt_add(x, C), then tt_mul(x, x), each
+// separately rounded, as the composition, over N values at slots j0 + i * dj.
+// One loop per step (uniform branches), so the add's loads issue together.
+template <int N>
+__device__ __forceinline__ void epi_apply_n(const EpiDev& e, double (&x)[N], const EpiTile& t,
+                                            int64_t j0, int64_t dj) {
+  if (e.nmask) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int j = static_cast<int>(j0 + i * dj);
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < kEpiMaskDims; ++k)
+        if (k < e.nmask) ok = ok && ((j >> e.msh[k]) & static_cast<int>(e.mtm1[k])) < t.lim[k];
+      x[i] = dmul(x[i], ok ? 1.0 : 0.0);  // Session::mask_mul backend.hpp:145
+    }
+  }
+  if (t.ct) {
+    double c[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) c[i] = __ldg(t.ct + j0 + i * dj);
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = dadd(x[i], c[i]);
+  }
+  if (e.square) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = dmul(x[i], x[i]);
+  }
 }
 
 #include "kernels/stream.cuh"

@@ -105,13 +105,20 @@ void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const doubl
 // c_stride[i] is C's tile-index stride along output dim i (0 where C
 // broadcasts).  Fused into the tree pass when the reduction ends in one,
 // else a separate in-place pass over the output tiles.
+// The tail may also start with clean_unknowns' mask (nmask > 0): slot h of
+// output tile l is kept iff l_i * t_i + ((h / stride_i) mod t_i) < used_i for
+// each cut dim i (power-of-two t_i and strides, not interleaved).
+constexpr int kEpiMaskDims = 3;
 struct Epilogue {
   const double* c = nullptr;
   bool square = false;
   int nd = 0;
   int64_t ext[TT_MAX_RANK] = {};
   int64_t c_stride[TT_MAX_RANK] = {};
-  bool active() const { return c != nullptr || square; }
+  int nmask = 0;
+  int mask_dim[kEpiMaskDims] = {};
+  int64_t mask_t[kEpiMaskDims] = {}, mask_stride[kEpiMaskDims] = {}, mask_used[kEpiMaskDims] = {};
+  bool active() const { return c != nullptr || square || nmask > 0; }
 };
 // Runs `prog` for every group of `g`; `tb` may be null (no fused multiply);
 // `epi` (optional) is applied to every output tile.

@@ -241,6 +241,26 @@ inline TileTensor tt_mul_sum(const TileTensor& a, const TileTensor& b, int dim,
   return TileTensor(TileTensorShape::from_c(co), out, s, chain);
 }
 
+// clean_unknowns(tt_sum(tt_mul(a, b), dim)) with the mask applied in the
+// reduction's last pass (pipeline()'s odd -> even seam, linalg.hpp:213-260).
+// Shapes, chain index, counters and errors equal the two-call composition.
+inline TileTensor tt_mul_sum_clean(const TileTensor& a, const TileTensor& b, int dim,
+                                   std::optional<SumVariant> variant = std::nullopt) {
+  if (&a.session() != &b.session())
+    throw std::invalid_argument("operands belong to different sessions");
+  Session& s = a.session();
+  const TileTensorShape res =
+      sum_result_shape(elementwise_result_shape(a.shape(), b.shape(), OpKind::mul), dim);
+  auto out = detail::alloc_tiles(s, res.tile_count());
+  const tt_shape ca = a.shape().to_c(), cb = b.shape().to_c();
+  tt_shape co;
+  std::int64_t chain = 0;
+  detail::check(tt_mul_sum_clean(s.handle(), &ca, a.device_data(), a.chain_index(), &cb,
+                                 b.device_data(), b.chain_index(), dim, detail::variant_code(variant),
+                                 &co, out->get(), &chain));
+  return TileTensor(TileTensorShape::from_c(co), out, s, chain);
+}
+
 // One fully connected stage of cryptonets_infer's tiled branch (nn.hpp:468-490):
 // tt_sum(tt_mul(a, b), dim), then tt_add(., *c) when c is given, then
 // tt_mul(., .) when square -- the tail fused into the reduction's tree pass.

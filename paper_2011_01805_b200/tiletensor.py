@@ -606,6 +606,24 @@ def tt_mul_sum(a: TileTensor, b: TileTensor, dim: int,
     return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
 
 
+def tt_mul_sum_clean(a: TileTensor, b: TileTensor, dim: int,
+                     variant: Optional[SumVariant] = None) -> TileTensor:
+    """clean_unknowns(tt_sum(tt_mul(a, b), dim)) with the mask applied in the
+    reduction's last pass (pipeline()'s odd -> even seam, linalg.hpp:213-260).
+    Shapes, chain index, counters and errors equal the two-call composition."""
+    s = _same_session(a, b)
+    n_out = _result_tiles(("mulsum", a.shape(), b.shape(), int(dim)), lambda: sum_result_shape(
+        elementwise_result_shape(a.shape(), b.shape(), OpKind.mul), dim).tile_count())
+    out = s.empty_tiles(n_out)
+    so = CShape()
+    chain = ctypes.c_int64()
+    _check(lib().tt_mul_sum_clean(s.handle, ctypes.byref(a.shape().to_c()), _ptr(a.data()),
+                                  a.chain_index(), ctypes.byref(b.shape().to_c()), _ptr(b.data()),
+                                  b.chain_index(), int(dim), _variant(variant), ctypes.byref(so),
+                                  _ptr(out), ctypes.byref(chain)))
+    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
+
+
 def tt_mul_sum_affine(a: TileTensor, b: TileTensor, dim: int, c: Optional[TileTensor] = None,
                       square: bool = False, variant: Optional[SumVariant] = None) -> TileTensor:
     """One fully connected stage of cryptonets_infer's tiled branch (nn.hpp:468-490):
@@ -956,11 +974,14 @@ def pipeline(matrices: Sequence, v, tile: Sequence[int], session: Session) -> Pi
                 data = matvec_b(tm, data)
             else:
                 tm = pack(m, _shape2(m.shape[0], 1, t1, m.shape[1], 1, t2), session)
-                data = matvec_a(tm, data)
                 if k + 1 < len(mats):
-                    data = clean_unknowns(data)
+                    # matvec_a + clean_unknowns in one pass (operands valid by
+                    # construction: the same result, counters and errors)
+                    data = tt_mul_sum_clean(tm, data, 2)
                     if data.shape().dim(1).d < t2:
                         data = replicate_dim(data, 2)
+                else:
+                    data = matvec_a(tm, data)
         except DepthExhaustedError as e:
             raise DepthExhaustedError(f"pipeline stage {k + 1}: {e}") from None
     return PipelineResult(data, session.cost_report().since(before))

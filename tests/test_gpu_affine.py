@@ -198,3 +198,94 @@ def test_random_shapes_match_composition(gpu, s):
         assert bitwise_equal(got.tiles(), want.tiles()), (tt.format_shape(sa), tt.format_shape(sb), dim)
         runs += 1
     assert runs >= 5
+
+
+# ---- tt_mul_sum_clean: clean_unknowns(tt_sum(tt_mul(a, b), dim)) ---------------------
+
+
+def _check_clean(S, a, b, dim):
+    S.reset_counters()
+    want = tt.clean_unknowns(tt.tt_mul_sum(a, b, dim))
+    want_cost = S.cost_report()
+    S.reset_counters()
+    got = tt.tt_mul_sum_clean(a, b, dim)
+    assert S.cost_report() == want_cost, (S.cost_report(), want_cost)
+    assert tt.format_shape(got.shape()) == tt.format_shape(want.shape())
+    assert got.chain_index() == want.chain_index()
+    assert bitwise_equal(got.tiles(), want.tiles())
+    return got
+
+
+def test_clean_seam_config3_literal(gpu, oracle):
+    """matmul_a(A, B) -> clean_unknowns (config 3's literal chain): GEMM fold +
+    row-shift tree with the mask in its store; bitwise vs the oracle too."""
+    c3 = configs.config3()
+    s = 8192
+    S = tt.Session(s, 8)
+    sh = {k: parse_shape(c3.shapes[k]) for k in ("A3", "B3")}
+    T = {k: tt.pack(c3.tensors[k], sh[k], S) for k in sh}
+    got = _check_clean(S, T["A3"], T["B3"], 2)
+    assert tt.format_shape(got.shape()) == "[512/16,1/32,768/16]"
+    p = {k: oracle.pack(c3.tensors[k], sh[k], s) for k in sh}
+    so, o, _ = oracle.mul_sum(sh["A3"], p["A3"], sh["B3"], p["B3"], s, 2)
+    sc, oc, _ = oracle.clean_unknowns(so, o, s)
+    assert bitwise_equal(got.tiles(), oc)
+
+
+def test_clean_seam_paths(gpu):
+    # c1: two cut dims (100 = 6 x 16 + 4 rows, and the summed 1?/32), one launch
+    c1 = configs.config1()
+    S = tt.Session(512, 8)
+    a = tt.pack(c1.tensors["A"], parse_shape(c1.shapes["A"]), S)
+    b = tt.pack(c1.tensors["B"], parse_shape(c1.shapes["B"]), S)
+    _check_clean(S, a, b, 2)
+    _check_clean(S, a, b, 1)
+    # config-5-like group kernels (TMA ring / window), every dim
+    S = tt.Session(16384, 8)
+    x = _pack(S, "[200/16,256/32,64/32]", (200, 256, 64), 21)
+    w = _pack(S, "[*/16,256/32,64/32]", (1, 256, 64), 22)
+    for dim in (1, 2, 3):
+        _check_clean(S, x, w, dim)
+    # config 2: matvec (fold + row tree), and no '?' (clean is the identity)
+    c2 = configs.config2()
+    S = tt.Session(8192, 8)
+    m = tt.pack(c2.tensors["M"], parse_shape(c2.shapes["M"]), S)
+    v = tt.pack(c2.tensors["V"], parse_shape(c2.shapes["V"]), S)
+    _check_clean(S, m, v, 2)
+    _check_clean(S, m, m, 1)
+
+
+def test_clean_seam_depth(gpu):
+    S = tt.Session(512, 1)  # the product leaves chain 0: clean must fail after it
+    a = _pack(S, "[64/16,64/32]", (64, 64), 23)
+    b = _pack(S, "[64/16,64/32]", (64, 64), 24)
+    S.reset_counters()
+    with pytest.raises(tt.DepthExhaustedError) as e1:
+        tt.clean_unknowns(tt.tt_mul_sum(a, b, 2))
+    want = S.cost_report()
+    S.reset_counters()
+    with pytest.raises(tt.DepthExhaustedError) as e2:
+        tt.tt_mul_sum_clean(a, b, 2)
+    assert S.cost_report() == want and str(e1.value) == str(e2.value)
+
+
+@pytest.mark.parametrize("s", [16, 64, 512, 8192])
+def test_clean_seam_random(gpu, s):
+    import random
+    from shapes import partner_shape, random_pack_shape
+    rng = random.Random(7000 + s)
+    nrng = np.random.default_rng(70 + s)
+    S = tt.Session(s, 8)
+    runs = 0
+    for _ in range(40 if s < 8192 else 12):
+        sa = random_pack_shape(rng, s, rng.randint(1, 3))
+        sb = partner_shape(rng, sa)
+        a, b = _pack_random(S, sa, nrng), _pack_random(S, sb, nrng)
+        dim = rng.randint(1, sa.rank())
+        try:
+            tt.sum_result_shape(tt.elementwise_result_shape(sa, sb, tt.OpKind.mul), dim)
+        except tt.ShapeError:
+            continue
+        _check_clean(S, a, b, dim)
+        runs += 1
+    assert runs >= 5

@@ -33,6 +33,8 @@ def chains():
     T3.update({k: tt.pack(c3.tensors[k], tt.parse_shape(c3.shapes[k]), S3) for k in ("B3", "Ct3")})
     out["c3a"] = lambda: tt.tt_mul_sum(tt.replicate_dim(tt.clean_unknowns(
         tt.matmul_a(T3["A3"], T3["B3"])), 2), T3["Ct3"], 3)
+    out["c3af"] = lambda: tt.tt_mul_sum(tt.replicate_dim(
+        tt.tt_mul_sum_clean(T3["A3"], T3["B3"], 2), 2), T3["Ct3"], 3)
     c4 = configs.config4(True)
     S4 = tt.Session(8192, 8)
     T4 = {k: tt.pack(c4.tensors[k], tt.parse_shape(v), S4) for k, v in c4.shapes.items()}
