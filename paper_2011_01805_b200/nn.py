@@ -531,6 +531,22 @@ def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],
         for r in parts:
             total = CostReport(*(getattr(total, f) + getattr(r.cost, f) for f in tt._COST_FIELDS))
         return InferResult(np.concatenate([r.logits for r in parts], axis=1), total)
+    return _infer_tiled(net, batch, (t1, t2, t3), session, None)
+
+
+def _infer_tiled(net: NetworkSpec, batch, tile, session: tt.Session, cache) -> InferResult:
+    """The tiled branch of cryptonets_infer (nn.hpp:418-507).  cache: None, or a
+    dict keeping the packed weight / bias tensors across calls (CompiledTiled)."""
+    t1, t2, t3 = tile
+    n = int(batch.shape[1])
+
+    def cached(key, make):
+        if cache is None:
+            return make()
+        if key not in cache:
+            cache[key] = make()
+        return cache[key]
+
     # the tiled path lays the batch out on the host (im2col, as the reference does)
     batch = np.asarray(batch.detach().cpu() if _is_torch(batch) else batch, dtype=np.float64)
     before = session.cost_report()
@@ -583,9 +599,10 @@ def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],
                              session)
                 wf = np.broadcast_to(c.weights.T[:, :, None], (kk, c.filters, windows))
                 bf = np.repeat(c.bias, windows)
-                tw = tt.pack(np.ascontiguousarray(wf).reshape(kk, fold, 1),
-                             shape3((kk, 1, t1), (fold, 1, t2), (1, t3, t3)), session)
-                tb = pack_bias(bf, True)
+                tw = cached((layer_no, "w"), lambda: tt.pack(
+                    np.ascontiguousarray(wf).reshape(kk, fold, 1),
+                    shape3((kk, 1, t1), (fold, 1, t2), (1, t3, t3)), session))
+                tb = cached((layer_no, "b"), lambda: pack_bias(bf, True))
                 nxt = net.layers[layer_no] if layer_no < len(net.layers) else None
                 depth_after = min(min(tw.chain_index(), td.chain_index()) - 1, tb.chain_index())
                 fused_square = isinstance(nxt, SquareLayer) and depth_after >= 1
@@ -607,9 +624,10 @@ def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],
                         data = tt.clean_unknowns(data)
                     if data.shape().dim(1).d < t2:
                         data = tt.replicate_dim(data, 2)
-                tw = pack_weights(np.asarray(f.weights, dtype=np.float64), odd, perm)
+                tw = cached((layer_no, "w"), lambda: pack_weights(
+                    np.asarray(f.weights, dtype=np.float64), odd, perm))
                 perm = None
-                tb = pack_bias(np.asarray(f.bias, dtype=np.float64), odd)
+                tb = cached((layer_no, "b"), lambda: pack_bias(np.asarray(f.bias, dtype=np.float64), odd))
                 # a following square activation runs in the same device pass
                 # (tt_mul_sum_affine) unless it would exhaust the depth, which
                 # must then be reported against the square layer itself
@@ -632,6 +650,35 @@ def cryptonets_infer(net: NetworkSpec, batch: np.ndarray, tile: Sequence[int],
     raw = tt.unpack(data)
     out_size = raw.shape[1] if stage % 2 == 1 else raw.shape[0]
     return InferResult(raw.reshape(out_size, n), session.cost_report().since(before))
+
+
+class CompiledTiled:
+    """cryptonets_infer's tiled branch (tile [t1, t2, t3], t1 * t2 > 1) for
+    repeated inference: the weight and bias tensors are packed on the device
+    by the first infer() and reused by later calls (only the batch is packed
+    per call).  Logits and counters equal cryptonets_infer(net, batch, tile,
+    session, lift_batch_limit) bit for bit; the weights are captured on first
+    use."""
+
+    def __init__(self, net: NetworkSpec, tile: Sequence[int], session: tt.Session,
+                 lift_batch_limit: bool = False):
+        t1, t2, t3 = (int(x) for x in tile)
+        if t1 * t2 * t3 != session.slot_count():
+            raise ShapeError("tile extents must multiply to the slot count")
+        if t1 == 1 and t2 == 1:
+            raise ShapeError("tile [1, 1, s] is the batch-packed branch: use CompiledBatchPacked")
+        self.net, self.tile, self.session = net, (t1, t2, t3), session
+        self.lift = lift_batch_limit
+        self._cache: dict = {}
+
+    def infer(self, batch) -> InferResult:
+        if len(batch.shape) != 2:
+            raise ShapeError("batch must be [features, samples]")
+        if int(batch.shape[1]) > self.tile[2] and not self.lift:
+            raise ShapeError("batch size exceeds the batch tile extent t3")
+        if int(batch.shape[0]) != self.net.input_size():
+            raise ShapeError("batch feature size mismatch")
+        return _infer_tiled(self.net, batch, self.tile, self.session, self._cache)
 
 
 # ---- bootstrap lower bound (nn.hpp:511-531) ------------------------------------------

@@ -157,3 +157,30 @@ def test_lifted_batch_limit(gpu, ref):
         want = np.concatenate([ref.nn_run(1, SMALL, 44, batch[:, k:k + t3], tile, s, 8)[0]
                                for k in range(0, n, t3)], axis=1)
         assert _same(got.logits, want), tile
+
+
+def test_compiled_tiled(gpu, ref):
+    """CompiledTiled (weights / biases packed once) equals the reference's
+    cryptonets_infer bit for bit across calls and tile choices."""
+    net = nn.parse_network(SMALL, "", 44)
+    rng = np.random.default_rng(4242)
+    s = 64
+    for tile in ((2, 32, 1), (4, 4, 4), (8, 1, 8)):
+        S = tt.Session(s, 8)
+        comp = nn.CompiledTiled(net, tile, S)
+        for _ in range(3):
+            batch = rng.uniform(-1, 1, size=(36, tile[2]))
+            got = comp.infer(batch)
+            want, wc = ref.nn_run(1, SMALL, 44, batch, tile, s, 8)
+            assert _same(got.logits, want), tile
+            assert _cost(got.cost) == _cost(wc), tile
+    cn = nn.cryptonets_network(42)
+    S = tt.Session(8192, 8)
+    comp = nn.CompiledTiled(cn, (32, 256, 1), S)
+    for seed in (1, 2):
+        batch = np.random.default_rng(seed).uniform(-1, 1, size=(784, 1))
+        got = comp.infer(batch)
+        want = nn.cryptonets_infer(cn, batch, (32, 256, 1), S)
+        assert _same(got.logits, want.logits) and _cost(got.cost) == _cost(want.cost)
+    with pytest.raises(tt.ShapeError):
+        nn.CompiledTiled(cn, (1, 1, 8192), S)

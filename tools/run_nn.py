@@ -40,4 +40,16 @@ if "--compiled" in sys.argv:
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / 10
     print(f"compiled batch packed 8192: {dt * 1e3:.3f} ms per call ({8192 / dt:.0f} samples/s)")
+if "--compiled" in sys.argv:
+    S = tt.Session(8192, 8)
+    comp = nn.CompiledTiled(net, (32, 256, 1), S)
+    one = np.random.default_rng(1).uniform(0, 1, size=(784, 1))
+    comp.infer(one)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        r = comp.infer(one)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 10
+    print(f"compiled tiled (32, 256, 1), 1 sample: {dt * 1e3:.3f} ms per call")
 
