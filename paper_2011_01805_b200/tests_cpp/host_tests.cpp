@@ -599,6 +599,26 @@ static void nn_suite() {
     }
     CHECK_THROWS_AS(comp.infer(random_tensor({783, 4}, rng, 0, 1)), ShapeError);
   }
+  {  // tiled branch with weights packed once: CompiledTiled == cryptonets_infer, every call
+    for (const auto& tile : {std::array<std::int64_t, 3>{2, 32, 1}, std::array<std::int64_t, 3>{4, 4, 4}}) {
+      Session session(64, 8);
+      CompiledTiled comp(net, tile, session);
+      for (int rep = 0; rep < 3; ++rep) {
+        const DenseTensor batch = random_tensor({36, tile[2]}, rng, -1, 1);
+        session.reset_counters();
+        const auto want = cryptonets_infer(net, batch, tile, session);
+        const CostReport wc = session.cost_report();
+        session.reset_counters();
+        const auto got = comp.infer(batch);
+        const CostReport gc = session.cost_report();
+        bool same = got.logits.values().size() == want.logits.values().size();
+        for (std::size_t i = 0; same && i < got.logits.values().size(); ++i)
+          same = std::memcmp(&got.logits.values()[i], &want.logits.values()[i], 8) == 0;
+        CHECK(same && gc.additions == wc.additions && gc.rotations == wc.rotations &&
+              gc.multiplications == wc.multiplications);
+      }
+    }
+  }
   {  // paper-scale counts for tile [32, 256, 1]
     const NetworkSpec cn = cryptonets_network(42);
     const DenseTensor batch = random_tensor({784, 1}, rng, -1, 1);
