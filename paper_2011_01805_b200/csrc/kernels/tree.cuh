@@ -60,30 +60,49 @@ __device__ __forceinline__ void row_shift(double (&v)[NR], int D) {
 // BACK: the tile is read and written mirrored (slot p -> s-1-p), which turns
 // rotations by -d (replicate schedules) into the forward offsets d handled here.
 // EPI: the reduction's elementwise tail (+ C, square) applied before the store.
-template <int HR, int R = 16, bool BACK = false, bool EPI = false>
+// C > 1: a warp takes a chain of C consecutive row blocks of one tile, last
+// block first, and carries each block's raw (pre-tree) rows over as the halo of
+// the block before it -- rows are read (C + HR/R) / C times instead of twice.
+template <int HR, int R = 16, bool BACK = false, bool EPI = false, int C = 1>
 __global__ void __launch_bounds__(256, (HR <= 8 ? 3 : 2)) row_tree_kernel(const double* __restrict__ in,
                                                        double* __restrict__ out, int64_t n_tiles,
                                                        int64_t s, int nlevels, int4 lv0, int4 lv1,
                                                        const __grid_constant__ EpiDev epi) {
   constexpr int NR = R + HR;
+  static_assert(C == 1 || HR <= R, "the carried halo comes from one block");
   const int lane = threadIdx.x & 31;
   const int rows = static_cast<int>(s / 32);
-  const int blocks_per_tile = rows / R;
-  const uint64_t total = static_cast<uint64_t>(n_tiles) * blocks_per_tile;
+  const int chains_per_tile = rows / R / C;
+  const uint64_t total = static_cast<uint64_t>(n_tiles) * chains_per_tile;
   const int lvl[8] = {lv0.x, lv0.y, lv0.z, lv0.w, lv1.x, lv1.y, lv1.z, lv1.w};
   for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
        u < total; u += static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5)) {
-    const uint64_t tile = u / blocks_per_tile;
-    const int rb = static_cast<int>(u - tile * blocks_per_tile) * R;
+    const uint64_t tile = u / chains_per_tile;
+    const int b0 = static_cast<int>(u - tile * chains_per_tile) * C;
     const double* t = in + tile * s;
     double* o = out + tile * s;
+    double halo[HR];  // raw rows following the current block (cyclic over the tile)
+#pragma unroll
+    for (int i = 0; i < HR; ++i) {
+      int row = (b0 + C) * R + i;
+      if (row >= rows) row -= rows;
+      const int64_t p = row * 32 + lane;
+      halo[i] = __ldg(t + (BACK ? s - 1 - p : p));
+    }
+#pragma unroll 1
+    for (int kk = C - 1; kk >= 0; --kk) {
+    const int rb = (b0 + kk) * R;
     double v[NR];
 #pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      int row = rb + i;
-      if (row >= rows) row -= rows;  // cyclic halo
-      const int64_t p = row * 32 + lane;
+    for (int i = 0; i < R; ++i) {
+      const int64_t p = (rb + i) * 32 + lane;
       v[i] = __ldg(t + (BACK ? s - 1 - p : p));
+    }
+#pragma unroll
+    for (int i = 0; i < HR; ++i) v[R + i] = halo[i];
+    if (C > 1) {
+#pragma unroll
+      for (int i = 0; i < HR; ++i) halo[i] = v[i < R ? i : 0];
     }
     for (int k = 0; k < nlevels; ++k) {
       const int d = lvl[k];
@@ -120,6 +139,7 @@ __global__ void __launch_bounds__(256, (HR <= 8 ? 3 : 2)) row_tree_kernel(const 
     for (int i = 0; i < R; ++i) {
       const int64_t p = (rb + i) * 32 + lane;
       o[BACK ? s - 1 - p : p] = v[i];
+    }
     }
   }
 }
