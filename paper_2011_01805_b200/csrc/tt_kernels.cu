@@ -966,9 +966,10 @@ const int g_tree_smem = [] {
   return e ? std::atoi(e) : 0;
 }();
 
-// TT_ROW_CHAIN=1: chains of 4 row blocks per warp with the halo carried over
-// (rows read 1.25x instead of 2x) -- measured slower (c3 stage-2 tree 12.4 ->
-// 14.5 us: the serial chain leaves fewer loads in flight), so off by default
+// TT_ROW_CHAIN=2 / 4: chains of 2 / 4 row blocks per warp with the halo
+// carried over (rows read 1.5x / 1.25x instead of 2x) -- measured slower with 4
+// (c3 stage-2 tree 12.4 -> 14.5 us: the serial chain leaves fewer loads in
+// flight), so off (1) by default
 const int g_row_chain = [] {
   const char* e = std::getenv("TT_ROW_CHAIN");
   return e ? std::atoi(e) : 0;
@@ -1091,26 +1092,34 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
   const int4 lv1 = make_int4(lv[4], lv[5], lv[6], lv[7]);
   // chains of 4 blocks per warp (halo rows carried, not re-read) when that
   // still leaves >= 8 warps per SM
-  const bool chain4 = g_row_chain && s % (32 * 16 * 4) == 0 &&
-                      n_tiles * (s / 32 / 16 / 4) >= 8 * static_cast<int64_t>(c.sm_count);
+  const int chain = (g_row_chain == 2 || g_row_chain == 4) ? g_row_chain : 1;
+  const bool chained = chain > 1 && s % (32 * 16 * chain) == 0 &&
+                       n_tiles * (s / 32 / 16 / chain) >= 8 * static_cast<int64_t>(c.sm_count);
+  auto launch_chain = [&](auto hr_c, auto c_c) {
+    constexpr int HR = decltype(hr_c)::value, CC = decltype(c_c)::value;
+    const int64_t work = (n_tiles * (s / 32 / 16 / CC) + 7) / 8;
+    if (tp.back) {
+      const int grid = grid_for(c, (const void*)row_tree_kernel<HR, 16, true, false, CC>, 256, 0, work);
+      row_tree_kernel<HR, 16, true, false, CC><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
+                                                                            lv1, ed);
+    } else if (fuse) {
+      const int grid = grid_for(c, (const void*)row_tree_kernel<HR, 16, false, true, CC>, 256, 0, work);
+      row_tree_kernel<HR, 16, false, true, CC><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
+                                                                            lv1, ed);
+    } else {
+      const int grid = grid_for(c, (const void*)row_tree_kernel<HR, 16, false, false, CC>, 256, 0, work);
+      row_tree_kernel<HR, 16, false, false, CC><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
+                                                                             lv1, ed);
+    }
+  };
   auto row = [&](auto hr_c, auto r_c) {
     constexpr int HR = decltype(hr_c)::value, RR = decltype(r_c)::value;
     if constexpr (RR == 16) {
-      if (chain4) {
-        const int64_t work = (n_tiles * (s / 32 / 16 / 4) + 7) / 8;
-        if (tp.back) {
-          const int grid = grid_for(c, (const void*)row_tree_kernel<HR, 16, true, false, 4>, 256, 0, work);
-          row_tree_kernel<HR, 16, true, false, 4><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
-                                                                               lv1, ed);
-        } else if (fuse) {
-          const int grid = grid_for(c, (const void*)row_tree_kernel<HR, 16, false, true, 4>, 256, 0, work);
-          row_tree_kernel<HR, 16, false, true, 4><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
-                                                                               lv1, ed);
-        } else {
-          const int grid = grid_for(c, (const void*)row_tree_kernel<HR, 16, false, false, 4>, 256, 0, work);
-          row_tree_kernel<HR, 16, false, false, 4><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
-                                                                                lv1, ed);
-        }
+      if (chained) {
+        if (chain == 2)
+          launch_chain(hr_c, std::integral_constant<int, 2>{});
+        else
+          launch_chain(hr_c, std::integral_constant<int, 4>{});
         return;
       }
     }

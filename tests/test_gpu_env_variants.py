@@ -67,7 +67,8 @@ VARIANTS = [
     {"TT_GEMM_GRID": "200"},
     {"TT_GEMM_CFG": "11", "TT_GEMM_DYNAMIC": "0"},
     {"TT_TREE_SMEM": "1"},
-    {"TT_ROW_CHAIN": "1"},
+    {"TT_ROW_CHAIN": "2"},
+    {"TT_ROW_CHAIN": "4"},
     {"TT_ROW_ROWS": "32"},
     {"TT_ROW_ROWS": "64"},
 ]
