@@ -83,11 +83,17 @@ gpu = {}
 S = tt.Session(512, 8)
 T = {k: tt.pack(c1.tensors[k], sh1[k], S) for k in sh1}
 gpu["c1"] = gpu_time(lambda: tt.tt_mul_sum(T["A"], T["B"], 2), reps * 10)
+del T
+torch.cuda.empty_cache()
 S = tt.Session(8192, 8)
 T = {k: tt.pack(c2.tensors[k], sh2[k], S) for k in sh2}
 gpu["c2"] = gpu_time(lambda: tt.matvec_a(T["M"], T["V"]), reps * 5)
+del T
+torch.cuda.empty_cache()
 T = {k: tt.pack(c3.tensors[k], sh3[k], S) for k in ("A3", "Bt3", "C3")}
 gpu["c3"] = gpu_time(lambda: tt.matmul_a(T["A3"], tt.matmul_b(T["Bt3"], T["C3"])), reps)
+del T
+torch.cuda.empty_cache()
 T = {k: tt.pack(c4.tensors[k], sh4[k], S) for k in sh4}
 gpu["c4"] = gpu_time(lambda: tt.tt_mul_sum_affine(
     T["W2"], tt.tt_mul_sum_affine(T["W1t"], T["X"], 1, T["b1"], square=True), 2, T["b2"]), reps)
