@@ -113,6 +113,63 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Few groups, long folds (config 4's second layer: 16 groups x 100 steps;
+// config 2's matvec): one thread per slot pair, the pair's operands streamed
+// through a kFoldRing-deep shared-memory ring with 16-byte cp.async (no
+// register dependency, no barrier: a thread only reads what it copied), so
+// kFoldRing fold steps of loads are in flight per thread.  A CTA owns 256
+// consecutive slots of one group (s % 256 == 0, 16-byte aligned operands).
+constexpr int kFoldRing = 8;
+template <bool HAS_B>
+__global__ void __launch_bounds__(128) fold_ring_kernel(const __grid_constant__ FoldParams p,
+                                                        const double* __restrict__ A,
+                                                        const double* __restrict__ B,
+                                                        double* __restrict__ OUT, FastDiv64 runs_div) {
+  __shared__ __align__(16) double2 ring[kFoldRing][HAS_B ? 2 : 1][128];
+  const int64_t s = p.s;
+  const int64_t count = p.count;
+  const int64_t sa = p.g.astep * s;
+  const int64_t sb = p.g.bstep * s;
+  const bool b_moves = HAS_B && sb != 0;
+  const int t = threadIdx.x;
+  const uint64_t total = static_cast<uint64_t>(p.g.groups) * runs_div.d;
+  for (uint64_t r = blockIdx.x; r < total; r += gridDim.x) {
+    const uint64_t v = fdiv(r, runs_div);
+    const int64_t j0 = static_cast<int64_t>(r - v * runs_div.d) * 256 + 2 * t;
+    const GroupBase gb = group_base(p, v);
+    const double* pa = A + (gb.a + p.first * p.g.astep) * s + j0;
+    const double* pb = HAS_B ? B + (gb.b + p.first * p.g.bstep) * s + j0 : nullptr;
+    double2 wfix = make_double2(0.0, 0.0);
+    if (HAS_B && !b_moves) wfix = __ldg(reinterpret_cast<const double2*>(pb));
+#pragma unroll
+    for (int k = 0; k < kFoldRing; ++k) {
+      if (k < count) {
+        cp_async16(&ring[k][0][t], pa + k * sa);
+        if (b_moves) cp_async16(&ring[k][HAS_B ? 1 : 0][t], pb + k * sb);
+      }
+      cp_async_commit();
+    }
+    double2 acc = make_double2(0.0, 0.0);
+    int slot = 0;
+    for (int64_t c = 0; c < count; ++c) {
+      cp_async_wait<kFoldRing - 1>();  // step c has landed
+      const double2 x = ring[slot][0][t];
+      const double2 y = HAS_B ? (b_moves ? ring[slot][HAS_B ? 1 : 0][t] : wfix) : make_double2(0.0, 0.0);
+      const double2 pr = HAS_B ? make_double2(dmul(x.x, y.x), dmul(x.y, y.y)) : x;
+      acc = c == 0 ? pr : make_double2(dadd(acc.x, pr.x), dadd(acc.y, pr.y));
+      const int64_t f = c + kFoldRing;  // refill this slot with step c + ring
+      if (f < count) {
+        cp_async16(&ring[slot][0][t], pa + f * sa);
+        if (b_moves) cp_async16(&ring[slot][HAS_B ? 1 : 0][t], pb + f * sb);
+      }
+      cp_async_commit();
+      if (++slot == kFoldRing) slot = 0;
+    }
+    cp_async_wait<0>();
+    *reinterpret_cast<double2*>(OUT + gb.out * s + j0) = acc;
+  }
+}
+
 // BC = block columns (groups along ib): 16 (512 threads) or 8 (256 threads,
 // more and smaller work units when the 16 x 16 grid would leave SMs idle).
 // COLTREE: the reduction is over the first dim with t = 16 (s = 16 * stride):

@@ -577,6 +577,15 @@ int forced_path() {
   return v;
 }
 
+// Few-group folds stream their operands through a cp.async ring
+// (fold_ring_kernel) when the streamed operand is larger than ~half the L2:
+// config 4's layer-2 fold 36 -> 22 us; an L2-resident one (config 2, 32 MiB)
+// is ~0.5 us faster without.  TT_FOLD_RING=0 / 1 forces it off / on.
+const int g_fold_ring = [] {
+  const char* e = std::getenv("TT_FOLD_RING");
+  return e ? std::atoi(e) : -1;
+}();
+
 template <bool HAS_B>
 void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
                  double* tout) {
@@ -591,6 +600,14 @@ void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, con
     const int64_t work = (p.g.groups * static_cast<int64_t>(units) + 7) / 8;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, true>, 256, 0, work);
     fold_kernel<HAS_B, true><<<grid, 256, 0, c.stream>>>(to_fold(p), ta, tb, tout, make_div64(units));
+  } else if ((g_fold_ring == 1 ||
+              (g_fold_ring < 0 && p.g.groups * p.ops[0].y * s * 8 > (int64_t{48} << 20))) &&
+             s % 256 == 0 && p.ops[0].y > 1 && aligned16(ta) && (!HAS_B || aligned16(tb)) &&
+             aligned16(tout)) {
+    const int64_t runs = s / 256;
+    const int grid = grid_for(c, (const void*)fold_ring_kernel<HAS_B>, 128, 0, p.g.groups * runs);
+    fold_ring_kernel<HAS_B><<<grid, 128, 0, c.stream>>>(to_fold(p), ta, tb, tout,
+                                                        make_div64(static_cast<uint64_t>(runs)));
   } else {
     const int64_t work = (p.g.groups * s + 255) / 256;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, false>, 256, 0, work);

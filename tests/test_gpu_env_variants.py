@@ -40,9 +40,17 @@ for i, (k, v) in enumerate(sorted(shapes.items())):
     T[k] = TileTensor(sh, rng.uniform(-1, 1, size=(sh.tile_count(), 8192)), S)
 s1 = tt.matmul_b(T["Bt"], T["C"])
 r = tt.matmul_a(T["A"], s1)
-print(json.dumps({"s1": hashlib.sha256(np.ascontiguousarray(s1.tiles()).tobytes()).hexdigest(),
-                  "r": hashlib.sha256(np.ascontiguousarray(r.tiles()).tobytes()).hexdigest()}))
+F = {}
+for i, (k, v) in enumerate(sorted(json.loads(sys.argv[3]).items())):
+    sh = parse_shape(v)
+    rng = np.random.default_rng(200 + i)
+    F[k] = TileTensor(sh, rng.uniform(-1, 1, size=(sh.tile_count(), 8192)), S)
+folds = [tt.tt_mul_sum(F["M"], F["V"], 1), tt.tt_mul_sum(F["M"], F["W"], 1), tt.tt_sum(F["M"], 1)]
+h = lambda t: hashlib.sha256(np.ascontiguousarray(t.tiles()).tobytes()).hexdigest()
+print(json.dumps({"s1": h(s1), "r": h(r), "folds": [h(f) for f in folds]}))
 """
+# few-group folds (t = 1 summed dim, 40 steps): the plain and the cp.async-ring fold
+FOLD_SHAPES = {"M": "[40,2/2,4096/4096]", "V": "[40,2/2,4096/4096]", "W": "[*,2/2,4096/4096]"}
 
 VARIANTS = [
     {},
@@ -67,6 +75,8 @@ VARIANTS = [
     {"TT_GEMM_GRID": "200"},
     {"TT_GEMM_CFG": "11", "TT_GEMM_DYNAMIC": "0"},
     {"TT_TREE_SMEM": "1"},
+    {"TT_FOLD_RING": "1"},
+    {"TT_FOLD_RING": "0"},
     {"TT_ROW_CHAIN": "2"},
     {"TT_ROW_CHAIN": "4"},
     {"TT_ROW_ROWS": "32"},
@@ -87,7 +97,14 @@ def expected(oracle):
         T[k] = (sh, rng.uniform(-1, 1, size=(sh.tile_count(), S)))
     s1s, s1t, _ = oracle.mul_sum(*T["Bt"], *T["C"], S, 1)
     rs, rt, _ = oracle.mul_sum(*T["A"], s1s, s1t, S, 2)
-    return {"s1": _digest(s1t), "r": _digest(rt)}
+    F = {}
+    for i, (k, v) in enumerate(sorted(FOLD_SHAPES.items())):
+        sh = parse_shape(v)
+        rng = np.random.default_rng(200 + i)
+        F[k] = (sh, rng.uniform(-1, 1, size=(sh.tile_count(), S)))
+    folds = [oracle.mul_sum(*F["M"], *F["V"], S, 1)[1], oracle.mul_sum(*F["M"], *F["W"], S, 1)[1],
+             oracle.sum(*F["M"], S, 1)[1]]
+    return {"s1": _digest(s1t), "r": _digest(rt), "folds": [_digest(f) for f in folds]}
 
 
 @pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items())
@@ -95,7 +112,8 @@ def expected(oracle):
 def test_matmul_chain_variant(gpu, expected, env):
     full = dict(os.environ)
     full.update(env)
-    out = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), json.dumps(SHAPES)],
+    out = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), json.dumps(SHAPES),
+                          json.dumps(FOLD_SHAPES)],
                          env=full, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     got = json.loads(out.stdout.strip().splitlines()[-1])
