@@ -680,7 +680,8 @@ def _product(which: int, a: TileTensor, b: TileTensor, variant) -> TileTensor:
                                    b.chain_index(), _variant(variant), ctypes.byref(so),
                                    _ptr(out), ctypes.byref(chain)))
     shape = TileTensorShape.from_c(so)
-    return TileTensor(shape, out[:shape.tile_count()], s, chain.value)
+    n = shape.tile_count()
+    return TileTensor._wrap(shape, out if n == out.shape[0] else out[:n], s, chain.value)
 
 
 def matvec_a(m: TileTensor, v: TileTensor, variant=None) -> TileTensor:  # linalg.hpp:41
