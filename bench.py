@@ -5,21 +5,25 @@ Workload (BASELINE.json config 5, the throughput sweep):
   W = [*/16,2048/32,512/32] (replicated along dim 1, 1024 tiles, 128 MiB).
   One step = tt_sum(tt_mul(X, W), k) for k = 1, 2, 3 in turn, each ONE fused
   sm_100a launch (external left fold + in-tile rotate-and-sum, product never
-  stored).  value = streamed tile-slots per second = 3 * 2^31 per step per rank.
+  stored).  value = streamed tile-slots per second over ALL ranks
+  (3 * 2^31 per step for the whole job).
 
-Weak scaling (one process per GPU): rank r owns external tiles
-[128r, 128r+128) of dim 1 of a global [N*2048, 2048, 512] tensor (its own
-seeded slab); sums over dims 2 and 3 need no communication, the sum over
-dim 1 spans ranks and finishes with one NCCL all-reduce of the 128 MiB
-partial result.
+Strong scaling (default for N > 1, config 5 as named): the one 16 GiB X is
+block-partitioned along external dim 1 -- rank r owns 128/N external rows --
+and W is held whole on every rank.  Sums over dims 2 and 3 are local; the sum
+over dim 1 spans ranks and finishes with one NCCL all-reduce of the 128 MiB
+partial result (in flight while dims 2 and 3 run); its exact form (the left
+folds chained rank to rank, sharding.chain_mul_sum) is timed beside it.
+`--scaling weak`: every rank owns a whole 2048-row slab of [2048*N,2048,512].
 
 Inputs (16 GiB) exceed the 126 MB L2, so no flush is needed between steps.
 Timing: CUDA events on the launching stream, barrier + synchronize around the
-K timed steps, max over ranks.  `e2e` repeats the step through the public
+K timed steps (no host sync inside), max over ranks.  `e2e` repeats the step through the public
 API from pinned HOST buffers (H2D of the dense input, pack, the three fused
 products, unpack, D2H of the results).  `--impl reference` times the
 reference's own CPU implementation (oracle/_ref, else the C restatement) on
-a bounded slab of the same workload.
+a bounded slab of the same workload, all host threads, the same three products
+per step (pack / unpack reported separately); it never imports the product.
 """
 from __future__ import annotations
 
@@ -141,106 +145,225 @@ def max_over_ranks(x: float, dist, device) -> float:
     return float(t.item())
 
 
-# ---- CPU baseline (reference) ----------------------------------------------------------
+# ---- CPU reference legs (no import of the product package) ---------------------------
+#
+# The reference arm and the cpu_baseline leg load ONLY oracle/_ref/libttref.so
+# (the unmodified reference headers compiled here, oracle/Makefile) -- or, when
+# it is absent, the C restatement oracle/_build/libttoracle.so ("port").  The
+# seeded inputs come from a local copy of the shared counter-based generator
+# (splitmix64, bit-identical to tt_fill_uniform on the device), and shapes are
+# plain tt_shape structs, so paper_2011_01805_b200 is never imported here.
+
+import ctypes
 
 
-_REF = {}
+class _CDim(ctypes.Structure):  # tt_dim, include/tiletensor_b200.h
+    _fields_ = [("n", ctypes.c_int64), ("d", ctypes.c_int64), ("t", ctypes.c_int64),
+                ("unknown", ctypes.c_int32), ("interleaved", ctypes.c_int32)]
 
 
-def _ref_lib(threads: int):
-    """oracle/_ref (the reference compiled here), with W packed once."""
-    import ctypes
-    if "lib" not in _REF:
-        ref_lib = ROOT / "oracle" / "_ref" / "libttref.so"
-        if not ref_lib.exists():
-            _REF["lib"] = None
-            return None
-        lib = ctypes.CDLL(str(ref_lib))
-        lib.ref_set_threads(int(threads))  # TILETENSOR_THREADS, read once (tile_tensor.hpp:53-61)
-        _REF["lib"] = lib
-    return _REF["lib"]
+class _CShape(ctypes.Structure):  # tt_shape
+    _fields_ = [("rank", ctypes.c_int32), ("relaxed", ctypes.c_int32), ("dims", _CDim * 8)]
 
 
-def cpu_slab_pipeline(slab_tiles: int, threads: int):
-    """Reference CPU path on the config-5 slab X[0:16*slab_tiles]: pack X,
-    tt_sum(tt_mul(X, W), k) for k = 1, 2, 3, unpack (W packed once, outside).
-    Returns (kind, cores, seconds dict, streamed tile-slots)."""
-    import ctypes
+def _cshape(dims):
+    sh = _CShape()
+    sh.rank, sh.relaxed = len(dims), 0
+    for i, (n, d, t) in enumerate(dims):
+        sh.dims[i] = _CDim(n, d, t, 0, 0)
+    return sh
 
+
+C5_SEED_X, C5_SEED_W = 13, 14   # == paper_2011_01805_b200.configs
+
+
+def _uniform_at(idx, seed, lo, hi):
     import numpy as np
+    m1, m2, gold = np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB), np.uint64(0x9E3779B97F4A7C15)
 
-    from paper_2011_01805_b200 import configs, parse_shape
-    from paper_2011_01805_b200.tiletensor import DimSpec, TileTensorShape
+    def sm(x):
+        with np.errstate(over="ignore"):
+            x = x + gold
+            x = (x ^ (x >> np.uint64(30))) * m1
+            x = (x ^ (x >> np.uint64(27))) * m2
+            return x ^ (x >> np.uint64(31))
+    key = sm(np.array([seed], dtype=np.uint64))[0]
+    u = sm(np.asarray(idx, dtype=np.uint64) ^ key)
+    return lo + (hi - lo) * ((u >> np.uint64(11)).astype(np.float64) * (2.0 ** -53))
 
-    rows = 16 * slab_tiles
-    x = np.ascontiguousarray(configs.c5_x_slab(slice(0, rows)))
-    sx = TileTensorShape([DimSpec(rows, 1, 16), DimSpec(2048, 1, 32), DimSpec(512, 1, 32)])
-    sw = parse_shape(configs.C5_W_SHAPE)
-    streamed = 3 * sx.tile_count() * S5
-    lib = _ref_lib(threads)
+
+def _c5_x_rows(r0, r1):
+    import numpy as np
+    idx = np.arange(r0 * 2048 * 512, r1 * 2048 * 512, dtype=np.uint64)
+    return _uniform_at(idx, C5_SEED_X, -1.0, 1.0).reshape(r1 - r0, 2048, 512)
+
+
+def _c5_w():
+    import numpy as np
+    return _uniform_at(np.arange(2048 * 512, dtype=np.uint64), C5_SEED_W, -1.0, 1.0).reshape(1, 2048, 512)
+
+
+def cpu_leg(slab_tiles: int, steps: int, warmup: int):
+    """The reference's CPU path on the config-5 slab X[0:16*slab_tiles]
+    (slab_tiles external rows of dim 1 = slab_tiles*1024 tiles): pack X once,
+    then `warmup` + `steps` x [tt_sum(tt_mul(X, W), k) for k = 1, 2, 3] --
+    the same three products as one GPU step -- then unpack the results once.
+    Threads: TILETENSOR_THREADS from the environment (read once per process
+    by the reference, tile_tensor.hpp:53-61).  Returns a dict."""
+    import numpy as np
     dp = ctypes.POINTER(ctypes.c_double)
-    if lib is not None:
-        if "w" not in _REF:
-            w = np.ascontiguousarray(configs.c5_w())
-            if lib.ref_bench_prepare_w(w.ctypes.data_as(dp), ctypes.byref(sw.to_c()),
-                                       ctypes.c_int64(S5)) != 0:
-                raise RuntimeError("reference W pack failed")
-            _REF["w"] = True
-        dims = (ctypes.c_int * 3)(1, 2, 3)
+    rows = 16 * slab_tiles
+    x = np.ascontiguousarray(_c5_x_rows(0, rows))
+    w = np.ascontiguousarray(_c5_w())
+    sx = _cshape([(rows, 1, 16), (2048, 1, 32), (512, 1, 32)])
+    sw = _cshape([(1, 16, 16), (2048, 1, 32), (512, 1, 32)])
+    x_tiles = slab_tiles * 64 * 16
+    ref_lib = ROOT / "oracle" / "_ref" / "libttref.so"
+    out = {"slab_tiles": x_tiles, "streamed_slots_per_step": 3 * x_tiles * S5}
+    if ref_lib.exists():
+        lib = ctypes.CDLL(str(ref_lib))
         secs = (ctypes.c_double * 4)()
-        rc = lib.ref_bench_step(x.ctypes.data_as(dp), ctypes.byref(sx.to_c()), dims, 3, secs)
-        if rc != 0:
-            raise RuntimeError("reference pipeline failed")
-        return ("reference", int(lib.ref_thread_hint()),
-                {"pack": secs[0], "mul_sum": secs[1], "unpack": secs[2]}, streamed)
-    # fall back to the C restatement (single-threaded port)
-    sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_lib import Oracle
-    o = Oracle()
-    if "w_port" not in _REF:
-        _REF["w_port"] = o.pack(np.ascontiguousarray(configs.c5_w()), sw, S5)
-    tw = _REF["w_port"]
+        if lib.ref_bench_prepare_w(w.ctypes.data_as(dp), ctypes.byref(sw), ctypes.c_int64(S5)) != 0:
+            raise RuntimeError("reference W pack failed")
+        if lib.ref_bench_pack_x(x.ctypes.data_as(dp), ctypes.byref(sx), secs) != 0:
+            raise RuntimeError("reference X pack failed")
+        out["pack_s"] = secs[0]
+        dims = (ctypes.c_int * 3)(1, 2, 3)
+        times = []
+        for i in range(warmup + steps):
+            if lib.ref_bench_mul_sum(dims, 3, secs) != 0:
+                raise RuntimeError("reference mul+sum failed")
+            if i >= warmup:
+                times.append(secs[0])
+        if lib.ref_bench_unpack(secs) != 0:
+            raise RuntimeError("reference unpack failed")
+        out.update(kind="reference", cores=int(lib.ref_thread_hint()), unpack_s=secs[0],
+                   mul_sum_s=times)
+        return out
+    # the C restatement (single-threaded port of the same algorithm)
+    lib = ctypes.CDLL(str(ROOT / "oracle" / "_build" / "libttoracle.so"))
+    lib.or_tile_count.restype = ctypes.c_int64
+    tx = np.zeros((x_tiles, S5))
+    tw = np.zeros((lib.or_tile_count(ctypes.byref(sw)), S5))
+    lib.or_pack(w.ctypes.data_as(dp), ctypes.byref(sw), ctypes.c_int64(S5), tw.ctypes.data_as(dp))
     t0 = time.perf_counter()
-    tx = o.pack(x, sx, S5)
-    t1 = time.perf_counter()
-    outs = [o.mul_sum(sx, tx, sw, tw, S5, k) for k in (1, 2, 3)]
-    t2 = time.perf_counter()
-    for so, ot, _ in outs:
-        o.unpack(so, S5, ot)
-    t3 = time.perf_counter()
-    return ("port", 1, {"pack": t1 - t0, "mul_sum": t2 - t1, "unpack": t3 - t2}, streamed)
+    lib.or_pack(x.ctypes.data_as(dp), ctypes.byref(sx), ctypes.c_int64(S5), tx.ctypes.data_as(dp))
+    out["pack_s"] = time.perf_counter() - t0
+    prod = np.zeros((x_tiles, S5))
+    sp, so = _CShape(), _CShape()
+    cost = (ctypes.c_uint64 * 6)()
+    res = []
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        res = []
+        for k in (1, 2, 3):
+            lib.or_elementwise(1, ctypes.byref(sx), tx.ctypes.data_as(dp), ctypes.byref(sw),
+                               tw.ctypes.data_as(dp), ctypes.c_int64(S5), ctypes.byref(sp),
+                               prod.ctypes.data_as(dp), cost)
+            r = np.zeros((x_tiles, S5))
+            lib.or_sum(ctypes.byref(sp), prod.ctypes.data_as(dp), ctypes.c_int64(S5), k, -1,
+                       ctypes.byref(so), r.ctypes.data_as(dp), cost)
+            res.append((so, r))
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    out.update(kind="port", cores=1, unpack_s=0.0, mul_sum_s=times)
+    return out
+
+
+def cpu_leg_subprocess(threads: int, slab_tiles: int, steps: int, warmup: int):
+    """cpu_leg in a fresh process with TILETENSOR_THREADS=threads (the
+    reference reads it once per process)."""
+    env = dict(os.environ, TILETENSOR_THREADS=str(threads))
+    proc = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--cpu-leg",
+                           f"{slab_tiles},{steps},{warmup}"], env=env, capture_output=True,
+                          text=True, timeout=900)
+    if proc.returncode != 0:
+        raise RuntimeError(f"cpu leg failed: {proc.stderr[-400:]}")
+    return json.loads(proc.stdout.strip().splitlines()[-1])
+
+
+def _leg_summary(leg):
+    tps = leg["streamed_slots_per_step"] * len(leg["mul_sum_s"]) / sum(leg["mul_sum_s"])
+    return tps, (f"reference tt_sum(tt_mul(X,W),k) k=1,2,3 on the config-5 slab "
+                 f"({leg['slab_tiles']} of 131072 X tiles), {len(leg['mul_sum_s'])} step(s) of "
+                 f"{statistics.mean(leg['mul_sum_s']):.3f} s; pack of the slab {leg['pack_s']:.2f} s, "
+                 f"unpack of the results {leg['unpack_s']:.2f} s (reported, not in value)")
+
+
+def host_threads() -> int:
+    return min(64, os.cpu_count() or 1)  # the reference clamps to [1, 64]
+
+
+def cpu_baseline_block(slab_all: int, slab_one: int):
+    """cpu_baseline of the GPU arm: all host threads, plus 1 thread."""
+    leg = cpu_leg_subprocess(host_threads(), slab_all, 1, 0)
+    tps, sample = _leg_summary(leg)
+    out = {"value": tps, "unit": "tile-slots/s", "cores": leg["cores"], "kind": leg["kind"],
+           "sample": sample, "pack_tile_slots_per_s": leg["slab_tiles"] * S5 / leg["pack_s"]}
+    try:
+        one = cpu_leg_subprocess(1, slab_one, 1, 0)
+        tps1, sample1 = _leg_summary(one)
+        out["one_thread"] = {"value": tps1, "unit": "tile-slots/s", "cores": 1, "sample": sample1,
+                             "pack_tile_slots_per_s": one["slab_tiles"] * S5 / one["pack_s"]}
+    except Exception as exc:
+        out["one_thread"] = {"error": repr(exc)}
+    return out
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU path, all host threads,
+    on rank 0 only; the same config dict, metric and step content (the three
+    fused products' work) as our arm."""
     world, rank, _ = dist_env()
     if world > 1 and rank != 0:
         return  # rank 0 alone runs the CPU reference
-    threads = min(64, os.cpu_count() or 1)
-    slab = args.ref_slab_tiles
-    for _ in range(args.warmup):
-        cpu_slab_pipeline(slab, threads)
-    times = []
-    kind, cores, streamed = "reference", threads, 0
-    for _ in range(args.steps):
-        kind, cores, secs, streamed = cpu_slab_pipeline(slab, threads)
-        times.append(secs["pack"] + secs["mul_sum"] + secs["unpack"])
-    total = sum(times)
-    value = streamed * len(times) / total
-    sample = (f"config-5 slab X[0:{16 * slab}] ({slab * 64 * 16} of 131072 tiles): pack X, "
-              "tt_sum(tt_mul(X,W),k) k=1,2,3, unpack, per step (W packed once)")
+    threads = host_threads()
+    os.environ["TILETENSOR_THREADS"] = str(threads)  # before the reference library loads
+    leg = cpu_leg(args.ref_slab_tiles, args.steps, args.warmup)
+    value, sample = _leg_summary(leg)
+    one = None
+    try:
+        o = cpu_leg_subprocess(1, args.ref_slab_tiles, 1, 0)
+        v1, s1 = _leg_summary(o)
+        one = {"value": v1, "unit": "tile-slots/s", "cores": 1, "sample": s1}
+    except Exception as exc:
+        one = {"error": repr(exc)}
+    scaling = resolve_scaling(args, world)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tile-slots/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 U[-1,1])",
-        "config": {"workload": "c5 [2048/16,2048/32,512/32] x [*/16,2048/32,512/32], sum dims 1,2,3 (CPU slab)",
-                   "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": "tile-slots/s", "cores": cores, "kind": kind,
-                         "sample": sample},
+        "ms_per_step": 1e3 * statistics.mean(leg["mul_sum_s"]), "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": workload_config(world, scaling),
+        "cpu_baseline": {"value": value, "unit": "tile-slots/s", "cores": leg["cores"],
+                         "kind": leg["kind"], "sample": sample, "one_thread": one},
         "e2e": {"value": value, "unit": "tile-slots/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "phases": {"pack_s": leg["pack_s"], "unpack_s": leg["unpack_s"],
+                   "pack_tile_slots_per_s": leg["slab_tiles"] * S5 / leg["pack_s"]},
     }
     print(json.dumps(line), flush=True)
+
+
+DATA = ("synthetic: seeded splitmix64 U[-1,1] (bit-identical host/device generator); "
+        "16 GiB input > 126 MB L2 (no flush needed)")
+
+
+def resolve_scaling(args, world):
+    if args.scaling != "auto":
+        return args.scaling
+    return "strong"   # config 5 as named: the one 16 GiB X split over the ranks
+
+
+def workload_config(world, scaling):
+    rows = 2048 * world if scaling == "weak" else 2048
+    return {"workload": "c5: tt_sum(tt_mul(X[2048/16,2048/32,512/32], W[*/16,2048/32,512/32]), k) "
+                        "for k=1,2,3",
+            "slots": S5, "global_x": [rows, 2048, 512], "x_tiles_total": 64 * rows,
+            "parallelism": (f"shard external dim 1 over {world} rank(s); dims 2, 3 local; "
+                            "dim-1 sum: NCCL all-reduce of the partial result"),
+            "l2": "inputs larger than L2"}
 
 
 # ---- our arm ----------------------------------------------------------------------------
@@ -261,11 +384,10 @@ def time_events(fn, reps, stream):
 
 
 def run_ours(args):
-    import numpy as np
     import torch
 
     import paper_2011_01805_b200 as tt
-    from paper_2011_01805_b200 import configs
+    from paper_2011_01805_b200 import configs, sharding
 
     world, rank, local = dist_env()
     # one process per GPU; more ranks than GPUs only for the gloo functional check
@@ -274,45 +396,58 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     # TT_BENCH_BACKEND=gloo: functional check of the N > 1 path with several
     # ranks on one GPU (NCCL refuses duplicate devices) -- never a measurement
-    dist = init_dist(world, os.environ.get("TT_BENCH_BACKEND", "nccl"))
+    backend = os.environ.get("TT_BENCH_BACKEND", "nccl")
+    dist = init_dist(world, backend)
     stream = torch.cuda.current_stream(dev)
     hbm_peak, peak_src = peaks()
+    scaling = resolve_scaling(args, world)
 
-    from paper_2011_01805_b200 import sharding
     S = tt.Session(S5, 8, device=local)
-    # weak scaling: the global X is [2048*N, 2048, 512]; rank r owns external
-    # tiles [128r, 128r+128) of dim 1 (its own 16 GiB slab); W broadcasts.
-    sx_global = tt.TileTensorShape([tt.DimSpec(2048 * world, 1, 16), tt.DimSpec(2048, 1, 32),
+    # strong (default): config 5 as named, X = [2048/16,2048/32,512/32] split
+    # along dim 1 -- rank r owns external rows [begin, end) (128/N of them);
+    # weak: every rank owns a whole 2048-row slab of a [2048*N,2048,512] X.
+    # W (e1 = 1) broadcasts along dim 1: every rank holds it whole.
+    cfg = workload_config(world, scaling)
+    rows_global = cfg["global_x"][0]
+    sx_global = tt.TileTensorShape([tt.DimSpec(rows_global, 1, 16), tt.DimSpec(2048, 1, 32),
                                     tt.DimSpec(512, 1, 32)])
     plan = sharding.plan(sx_global, 1, world, rank)
     sx = plan.local_shape
     sw = tt.parse_shape(configs.C5_W_SHAPE)
-    assert sharding.operand_plan(sw, plan) is None and sx.tile_count() == X_TILES
+    assert sharding.operand_plan(sw, plan) is None
+    x_tiles = sx.tile_count()
+    out_tiles = {1: W_TILES, 2: x_tiles // 64, 3: x_tiles // 16}
+    rows = plan.row_slice.stop - plan.row_slice.start
     # inputs generated on the device with the shared counter-based generator
-    x_dense = torch.empty(configs.C5_DIMS, dtype=torch.float64, device=dev)
+    x_dense = torch.empty((rows, 2048, 512), dtype=torch.float64, device=dev)
     w_dense = torch.empty((1, 2048, 512), dtype=torch.float64, device=dev)
-    rank_offset = plan.row_slice.start * (2048 * 512)
-    tt.fill_uniform(S, x_dense, configs.C5_SEED_X, -1.0, 1.0, offset=rank_offset)
+    tt.fill_uniform(S, x_dense, configs.C5_SEED_X, -1.0, 1.0, offset=plan.row_slice.start * 2048 * 512)
     tt.fill_uniform(S, w_dense, configs.C5_SEED_W, -1.0, 1.0)  # same W on every rank
     X = tt.pack(x_dense, sx, S)
     W = tt.pack(w_dense, sw, S)
 
-    def mul_sum(a, b, k):
-        return tt.tt_mul_sum(a, b, k)
-
     def step():
-        return [sharding.sharded_mul_sum(X, W, k, plan, mul_sum, lambda r: r.data())[0]
-                for k in (1, 2, 3)]
+        outs, work = [], None
+        for k in (1, 2, 3):
+            r = tt.tt_mul_sum(X, W, k)
+            if k == plan.shard_dim and world > 1:
+                # the one real exchange: the dim-1 sum spans the ranks' slabs
+                # (NCCL over NVLink), in flight while dims 2 and 3 run
+                work = sharding.allreduce_partial(r.data(), async_op=True)
+            outs.append(r)
+        return outs, work
 
     for _ in range(args.warmup):
-        step()
+        _, w = step()
+        if w is not None:
+            w.wait()
     torch.cuda.synchronize(dev)
     if dist is not None:
         dist.barrier()
 
-    # per-launch timing of the fused kernel (one launch per dim)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    per_dim = {1: [], 2: [], 3: []}
+    # per-launch CUDA events on the launching stream; read after the timed
+    # region (no host synchronisation inside it)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     launches0 = S.launches()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
@@ -321,26 +456,20 @@ def run_ours(args):
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
-        for _ in range(args.steps):
+        outs = None
+        for i in range(args.steps):
+            ev = evs[i]
             ev[0].record(stream)
-            partial, work = None, None
+            work = None
+            outs = []
             for k in (1, 2, 3):
                 r = tt.tt_mul_sum(X, W, k)
                 ev[k].record(stream)
-                if k == plan.shard_dim:
-                    partial = r
-                    if world > 1:
-                        # the one real exchange: the dim-1 sum spans the ranks'
-                        # slabs (NCCL over NVLink), in flight while the dim-2
-                        # and dim-3 products run
-                        work = sharding.allreduce_partial(partial.data(), async_op=True)
+                if k == plan.shard_dim and world > 1:
+                    work = sharding.allreduce_partial(r.data(), async_op=True)
+                outs.append(r)
             if work is not None:
-                work.wait()
-            # the sync below is per step only to read the per-launch events
-            ev[3].synchronize()
-            per_dim[1].append(ev[0].elapsed_time(ev[1]) / 1e3)
-            per_dim[2].append(ev[1].elapsed_time(ev[2]) / 1e3)
-            per_dim[3].append(ev[2].elapsed_time(ev[3]) / 1e3)
+                work.wait()   # stream-ordered: the next step's kernels queue behind it
         t_end.record(stream)
         t_end.synchronize()
         elapsed = t_start.elapsed_time(t_end) / 1e3
@@ -349,158 +478,244 @@ def run_ours(args):
             dist.barrier()
     launches = S.launches() - launches0
     elapsed_max = max_over_ranks(elapsed, dist, dev)
-    step_slots = 3 * X_TILES * S5
-    value = world * step_slots * args.steps / elapsed_max
+    per_dim = {k: [e[k - 1].elapsed_time(e[k]) / 1e3 for e in evs] for k in (1, 2, 3)}
+    step_slots_total = 3 * sx_global.tile_count() * S5   # all ranks' units per step
+    value = step_slots_total * args.steps / elapsed_max
 
-    # roofline of the dominant kernel (the fused group kernel, all three dims)
-    alg = {k: (X_TILES + W_TILES + OUT_TILES[k]) * S5 * 8 for k in (1, 2, 3)}
+    # roofline of the dominant kernel (the fused group kernel, all three dims),
+    # this rank's algorithmic bytes over this rank's launch durations
+    alg = {k: (x_tiles + W_TILES + out_tiles[k]) * S5 * 8 for k in (1, 2, 3)}
     dur = {k: sum(v) / len(v) for k, v in per_dim.items()}
     achieved = sum(alg.values()) / sum(dur.values()) / 1e9
     traffic = traffic_summary()
-    tr = traffic.get("c5_mul_sum_bytes_per_launch")
+    tr = traffic.get("c5_mul_sum_bytes_per_launch") if world == 1 or scaling == "weak" else None
 
     ops = {}
     for k in (1, 2, 3):
         gbs = alg[k] / dur[k] / 1e9
         ops[f"mul_sum_dim{k}"] = {"ms": dur[k] * 1e3, "GB/s": gbs, "frac": gbs / hbm_peak,
                                   "frac_of_8TBps": gbs / 8000.0,
-                                  "tile_slots_per_s": X_TILES * S5 / dur[k],
+                                  "tile_slots_per_s": x_tiles * S5 / dur[k],
                                   "alg_bytes": alg[k]}
 
-    # pack (dense -> tiles), same tensor
+    # the exact (bit-identical) form of the sum over the sharded dim: the
+    # ranks' left folds chained along dim 1, the in-tile tree once at the end
+    try:
+        fold, finish, n_out, new_acc = sharding.gpu_chain_ops(tt, X, W, 1)
+
+        def chain():
+            return sharding.chain_mul_sum(X, W, 1, plan, fold, finish, n_out, new_acc)
+        chain_res = chain()
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        reps = max(1, min(args.steps, 5))
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(reps):
+            chain_res = chain()
+        t1.record(stream)
+        t1.synchronize()
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        tc = max_over_ranks(t0.elapsed_time(t1) / 1e3 / reps, dist, dev)
+        ops["mul_sum_dim1_chain"] = {
+            "ms": tc * 1e3, "tile_slots_per_s": sx_global.tile_count() * S5 / tc,
+            "note": "exact cross-rank form of the dim-1 sum (sharding.chain_mul_sum: left folds "
+                    "chained rank to rank in 16 chunks, in-tile tree on the last rank); "
+                    "bit-identical to one GPU"}
+    except Exception as exc:
+        print(f"[bench] chain failed: {exc!r}", file=sys.stderr)
+        ops["mul_sum_dim1_chain"] = {"error": repr(exc)}
+        chain_res = None
+
+    if args.dump:
+        dump_results(args.dump, rank, world, plan, outs, chain_res)
+
     try:
         if not args.skip_extra:
-            t = time_events(lambda: tt.pack(x_dense, sx, S), max(1, args.steps), stream)
-            pb = 2 * X_TILES * S5 * 8
-            ops["pack"] = {"ms": t * 1e3, "GB/s": pb / t / 1e9, "frac": pb / t / 1e9 / hbm_peak,
-                           "frac_of_8TBps": pb / t / 1e12 / 8.0, "tile_slots_per_s": X_TILES * S5 / t,
-                           "alg_bytes": pb}
-            del t
-            # unfused elementwise (tt_mul with W broadcast along dim 1, tt_add): 16 GiB in, 16 GiB out
-            for name, fn, nb in (("ew_mul_bcast", lambda: tt.tt_mul(X, W), (2 * X_TILES + W_TILES) * S5 * 8),
-                                 ("ew_add", lambda: tt.tt_add(X, X), 2 * X_TILES * S5 * 8)):
-                t = time_events(fn, max(1, args.steps), stream)
-                ops[name] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak,
-                             "tile_slots_per_s": X_TILES * S5 / t, "alg_bytes": nb}
-            # the other tile passes on config-5-sized data (rows a8, a10, a12)
-            reps = max(1, min(3, args.steps))
-            for k in (1, 2, 3):
-                t = time_events(lambda: tt.tt_sum(X, k), reps, stream)
-                nb = (X_TILES + OUT_TILES[k]) * S5 * 8
-                ops[f"sum_dim{k}"] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak}
-            t = time_events(lambda: tt.tiles_rotate(S, X.data(), 5), reps, stream)
-            ops["rotate"] = {"ms": t * 1e3, "GB/s": 2 * X_TILES * S5 * 8 / t / 1e9,
-                             "frac": 2 * X_TILES * S5 * 8 / t / 1e9 / hbm_peak}
-            R3 = tt.tt_sum(X, 3)  # [2048/16,2048/32,1?/32]: 8192 boundary tiles
-            nb = 2 * OUT_TILES[3] * S5 * 8
-            t = time_events(lambda: tt.clean_unknowns(R3), 10, stream)
-            ops["clean_unknowns"] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak}
-            C3 = tt.clean_unknowns(R3)
-            t = time_events(lambda: tt.replicate_dim(C3, 3), 10, stream)
-            ops["replicate_dim"] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak}
-            del R3, C3
+            ops.update(bench_extra_ops(tt, X, W, x_dense, sx, S, stream, hbm_peak, args, out_tiles))
             ops.update(bench_matmul(tt, configs, S, stream, hbm_peak, max(3, args.steps)))
             ops.update(bench_small_configs(tt, configs, stream, hbm_peak, max(20, args.steps)))
     except Exception as exc:  # keep the bench line: report the failure instead
         print(f"[bench] extra failed: {exc!r}", file=sys.stderr)
         ops["extra_error"] = repr(exc)
 
-    # end to end from pinned host memory through the public API
     e2e = None
-    try:
-        # every local rank stages its host input (x2 briefly while pinning): use
-        # the largest slab of X (1, 1/2, 1/4, 1/8 of its dim-1 rows) that fits
-        # the host's free memory, decided once for all ranks (the block below
-        # has collectives) -- never drive the host out of memory
-        frac = 1.0
-        try:
-            import psutil
-            local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
-            avail = psutil.virtual_memory().available
-            if os.environ.get("TT_BENCH_HOST_GIB"):  # test hook: pretend a smaller host
-                avail = float(os.environ["TT_BENCH_HOST_GIB"]) * 2**30
-            while frac > 0.125 and 2.2 * x_dense.numel() * 8 * frac * local_world > avail:
-                frac /= 2
-        except Exception:
-            pass
-        frac = -max_over_ranks(-frac, dist, dev)
-        if not args.skip_e2e:
-            rows = int(x_dense.shape[0] * frac)
-            sx_e = sx if frac == 1.0 else tt.TileTensorShape(
-                [tt.DimSpec(rows, 1, 16), tt.DimSpec(2048, 1, 32), tt.DimSpec(512, 1, 32)])
-            pinned = args.e2e_pinned
-            host_x = x_dense[:rows].to("cpu")
-            if pinned:
-                try:  # fall back to pageable memory if the host cannot pin it
-                    host_x = host_x.pin_memory()
-                except RuntimeError as exc:
-                    print(f"[bench] rank {rank}: pinning the host input failed ({exc}); pageable",
-                          file=sys.stderr)
-                    pinned = False
-            host_w = w_dense.to("cpu").pin_memory() if pinned else w_dense.to("cpu")
-            del x_dense
-            torch.cuda.empty_cache()
-
-            def e2e_step():
-                Xh = tt.pack(host_x, sx_e, S)   # H2D of the dense input + pack kernel
-                Wh = tt.pack(host_w, sw, S)
-                d2h = 0
-                for k in (1, 2, 3):
-                    r, _ = sharding.sharded_mul_sum(Xh, Wh, k, plan, mul_sum, lambda t: t.data())
-                    res = tt.unpack(r)          # unpack kernel + D2H
-                    d2h += res.nbytes
-                return d2h
-            e2e_step()
-            torch.cuda.synchronize(dev)
-            reps = max(1, min(args.steps, args.e2e_steps))
-            t0 = time.perf_counter()
-            for _ in range(reps):
-                d2h = e2e_step()
-            torch.cuda.synchronize(dev)
-            e_el = max_over_ranks((time.perf_counter() - t0) / reps, dist, dev)
-            h2d = host_x.numel() * 8 + host_w.numel() * 8
-            e2e = {"value": world * 3 * sx_e.tile_count() * S5 / e_el, "unit": "tile-slots/s",
-                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                   "ms_per_step": e_el * 1e3, "steps": reps, "host_buffers": "pinned" if pinned else "pageable",
-                   "x_slab_fraction": frac}
-    except Exception as exc:  # keep the bench line: report the failure instead
-        print(f"[bench] e2e failed: {exc!r}", file=sys.stderr)
-        e2e = {"error": repr(exc)}
+    if not args.skip_e2e:
+        e2e = bench_e2e(tt, args, sharding, plan, X, W, x_dense, w_dense, sx, sw, S, dist, dev,
+                        world, rank, sx_global)
+    del x_dense
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
-        threads = min(64, os.cpu_count() or 1)
-        kind, cores, secs, streamed = cpu_slab_pipeline(args.cpu_slab_tiles, threads)
-        cpu = {"value": streamed / secs["mul_sum"], "unit": "tile-slots/s", "cores": cores,
-               "kind": kind,
-               "sample": (f"reference tt_sum(tt_mul(X,W),k) k=1,2,3 on the config-5 slab "
-                          f"X[0:{16 * args.cpu_slab_tiles}] ({args.cpu_slab_tiles * 1024} tiles), "
-                          f"{secs['mul_sum']:.2f} s; pack {secs['pack']:.2f} s, "
-                          f"unpack {secs['unpack']:.2f} s")}
+        try:
+            cpu = cpu_baseline_block(args.cpu_slab_tiles, args.cpu_one_thread_slab_tiles)
+        except Exception as exc:
+            print(f"[bench] cpu baseline failed: {exc!r}", file=sys.stderr)
+            cpu = {"error": repr(exc)}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tile-slots/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_max / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded splitmix64 U[-1,1] generated on device; 16 GiB input > 126 MB L2 (no flush needed)",
-            "config": {"workload": "c5: tt_sum(tt_mul(X[2048/16,2048/32,512/32], W[*/16,2048/32,512/32]), k) for k=1,2,3",
-                       "slots": S5, "x_tiles_per_rank": X_TILES, "global_x": [2048 * world, 2048, 512],
-                       "parallelism": f"shard external dim 1 over {world} rank(s); NCCL all-reduce for the dim-1 sum",
-                       "l2": "inputs larger than L2"},
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": cfg,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "frac_of_8TBps": achieved / 8000.0,
                          "peak_source": peak_src, "traffic": tr,
+                         "traffic_source": traffic.get("source"),
                          "kernel": "group_tma_kernel / group_tma_win_kernel (fused fold + rotate-and-sum, TMA ring)",
-                         "alg_bytes_per_step": sum(alg.values())},
+                         "alg_bytes_per_step": sum(alg.values()), "x_tiles_per_rank": x_tiles},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "ops": ops,
         }
+        if world > 1:
+            line["backend"] = backend
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def dump_results(path, rank, world, plan, outs, chain_res):
+    """--dump DIR: slabs of this rank's results (first / middle / last output
+    rows) for the multi-rank parity test (tests/test_gpu_multirank.py)."""
+    import numpy as np
+    d = Path(path)
+    d.mkdir(parents=True, exist_ok=True)
+    r1, r2, r3 = (o.data() for o in outs)
+    blob = {"begin": np.array([plan.begin, plan.end])}
+    # dim 2 result: 16 tiles per external row of dim 1; dim 3: 64 per row
+    for name, r, per in (("dim2", r2, 16), ("dim3", r3, 64)):
+        e = r.shape[0] // per
+        for tag, row in (("first", 0), ("mid", e // 2), ("last", e - 1)):
+            blob[f"{name}_{tag}"] = r[row * per:(row + 1) * per].cpu().numpy()
+            blob[f"{name}_{tag}_row"] = np.array([plan.begin + row])
+    # dim 1 result (all-reduced, replicated): ext [1, 64, 16]; columns l2
+    for tag, l2 in (("first", 0), ("mid", 31), ("last", 63)):
+        blob[f"dim1_{tag}"] = r1[l2 * 16:(l2 + 1) * 16].cpu().numpy()
+        blob[f"dim1_{tag}_l2"] = np.array([l2])
+        if chain_res is not None:
+            blob[f"dim1chain_{tag}"] = chain_res.data()[l2 * 16:(l2 + 1) * 16].cpu().numpy()
+    np.savez(d / f"rank{rank}.npz", **blob)
+
+
+def bench_extra_ops(tt, X, W, x_dense, sx, S, stream, hbm_peak, args, out_tiles):
+    """The other config-5 tile passes (pack, unfused elementwise, sums,
+    rotate, clean, replicate) on this rank's data."""
+    ops = {}
+    x_tiles = sx.tile_count()
+    t = time_events(lambda: tt.pack(x_dense, sx, S), max(1, args.steps), stream)
+    pb = 2 * x_tiles * S5 * 8
+    ops["pack"] = {"ms": t * 1e3, "GB/s": pb / t / 1e9, "frac": pb / t / 1e9 / hbm_peak,
+                   "frac_of_8TBps": pb / t / 1e12 / 8.0, "tile_slots_per_s": x_tiles * S5 / t,
+                   "alg_bytes": pb}
+    # unfused elementwise (tt_mul with W broadcast along dim 1, tt_add)
+    for name, fn, nb in (("ew_mul_bcast", lambda: tt.tt_mul(X, W), (2 * x_tiles + W_TILES) * S5 * 8),
+                         ("ew_add", lambda: tt.tt_add(X, X), 2 * x_tiles * S5 * 8)):
+        t = time_events(fn, max(1, args.steps), stream)
+        ops[name] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak,
+                     "tile_slots_per_s": x_tiles * S5 / t, "alg_bytes": nb}
+    reps = max(1, min(3, args.steps))
+    for k in (1, 2, 3):
+        t = time_events(lambda: tt.tt_sum(X, k), reps, stream)
+        nb = (x_tiles + out_tiles[k]) * S5 * 8
+        ops[f"sum_dim{k}"] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak}
+    t = time_events(lambda: tt.tiles_rotate(S, X.data(), 5), reps, stream)
+    ops["rotate"] = {"ms": t * 1e3, "GB/s": 2 * x_tiles * S5 * 8 / t / 1e9,
+                     "frac": 2 * x_tiles * S5 * 8 / t / 1e9 / hbm_peak}
+    R3 = tt.tt_sum(X, 3)  # [rows/16,2048/32,1?/32]: boundary tiles
+    nb = 2 * out_tiles[3] * S5 * 8
+    t = time_events(lambda: tt.clean_unknowns(R3), 10, stream)
+    ops["clean_unknowns"] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak}
+    C3 = tt.clean_unknowns(R3)
+    t = time_events(lambda: tt.replicate_dim(C3, 3), 10, stream)
+    ops["replicate_dim"] = {"ms": t * 1e3, "GB/s": nb / t / 1e9, "frac": nb / t / 1e9 / hbm_peak}
+    return ops
+
+
+def host_slab_fraction(numel, world, dist, dev):
+    """Largest slab of X (1, 1/2, 1/4, 1/8 of its dim-1 rows) whose host
+    staging (x2.2 while pinning) fits the host's free memory for all local
+    ranks; 0 when not even 1/8 fits.  One decision for all ranks."""
+    frac = 1.0
+    try:
+        import psutil
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        avail = psutil.virtual_memory().available
+        if os.environ.get("TT_BENCH_HOST_GIB"):  # test hook: pretend a smaller host
+            avail = float(os.environ["TT_BENCH_HOST_GIB"]) * 2**30
+        while frac >= 0.125 and 2.2 * numel * 8 * frac * local_world > avail:
+            frac /= 2
+        if frac < 0.125:
+            frac = 0.0
+    except Exception as exc:
+        print(f"[bench] host memory probe failed ({exc!r}); staging 1/8 of X", file=sys.stderr)
+        frac = 0.125
+    return -max_over_ranks(-frac, dist, dev)
+
+
+def bench_e2e(tt, args, sharding, plan, X, W, x_dense, w_dense, sx, sw, S, dist, dev, world, rank,
+              sx_global):
+    """The same step through the public API from pinned HOST buffers: H2D
+    of the dense input + pack, the three fused products (+ the dim-1
+    all-reduce), unpack + D2H of every result."""
+    import torch
+    try:
+        frac = host_slab_fraction(x_dense.numel(), world, dist, dev)
+        if frac == 0.0:
+            return {"skipped": "host memory too small to stage even 1/8 of the input"}
+        rows = int(x_dense.shape[0] * frac)
+        sx_e = sx if frac == 1.0 else tt.TileTensorShape(
+            [tt.DimSpec(rows, 1, 16), tt.DimSpec(2048, 1, 32), tt.DimSpec(512, 1, 32)])
+        pinned = args.e2e_pinned
+        host_x = x_dense[:rows].to("cpu")
+        if pinned:
+            try:  # fall back to pageable memory if the host cannot pin it
+                host_x = host_x.pin_memory()
+            except RuntimeError as exc:
+                print(f"[bench] rank {rank}: pinning the host input failed ({exc}); pageable",
+                      file=sys.stderr)
+                pinned = False
+        host_w = w_dense.to("cpu").pin_memory() if pinned else w_dense.to("cpu")
+        torch.cuda.empty_cache()
+
+        def mul_sum(a, b, k):
+            return tt.tt_mul_sum(a, b, k)
+
+        def e2e_step():
+            Xh = tt.pack(host_x, sx_e, S)   # H2D of the dense input + pack kernel
+            Wh = tt.pack(host_w, sw, S)
+            d2h = 0
+            for k in (1, 2, 3):
+                r, _ = sharding.sharded_mul_sum(Xh, Wh, k, plan, mul_sum, lambda t: t.data())
+                res = tt.unpack(r)          # unpack kernel + D2H
+                d2h += res.nbytes
+            return d2h
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        reps = max(1, min(args.steps, args.e2e_steps))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            d2h = e2e_step()
+        torch.cuda.synchronize(dev)
+        e_el = max_over_ranks((time.perf_counter() - t0) / reps, dist, dev)
+        h2d = host_x.numel() * 8 + host_w.numel() * 8
+        units = 3 * sx_global.tile_count() * S5 * frac
+        return {"value": units / e_el, "unit": "tile-slots/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e_el * 1e3, "steps": reps,
+                "host_buffers": "pinned" if pinned else "pageable", "x_slab_fraction": frac,
+                "path": "tt.pack(host) -> tt_mul_sum x3 (+ dim-1 all-reduce) -> tt.unpack (D2H)"}
+    except Exception as exc:  # keep the bench line: report the failure instead
+        print(f"[bench] e2e failed: {exc!r}", file=sys.stderr)
+        return {"error": repr(exc)}
 
 
 def bench_small_configs(tt, configs, stream, hbm_peak, reps):
@@ -635,7 +850,8 @@ def bench_matmul(tt, configs, S, stream, hbm_peak, reps):
     t_graph = time_events(g.replay, reps, stream)
     tile = 8192 * 8
     # unique operand tiles + out tiles of both stages
-    alg = (1536 + 768 + 512 + 512 + 1024 + 512 + 512) * tile
+    # stage 1: Bt 96 MiB + C 48 MiB in, 32 MiB out; stage 2: A 64 + 32 MiB in, 32 MiB out
+    alg = (1536 + 768 + 512 + 1024 + 512 + 512) * tile  # 4864 tiles = 304 MiB
     prod_tiles = 24576 + 16384
     # the fold is FP64-issue bound, not HBM bound: one DMUL + one DADD per
     # product slot (no contraction -- bit parity), against the measured
@@ -683,9 +899,17 @@ def main():
     ap.add_argument("--skip-extra", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-pinned", type=int, default=1)
-    ap.add_argument("--cpu-slab-tiles", type=int, default=48)  # ~10 s of reference CPU work
-    ap.add_argument("--ref-slab-tiles", type=int, default=4)
+    ap.add_argument("--cpu-slab-tiles", type=int, default=48)  # ~5 s of reference CPU work
+    ap.add_argument("--cpu-one-thread-slab-tiles", type=int, default=4)
+    ap.add_argument("--ref-slab-tiles", type=int, default=8)
+    ap.add_argument("--scaling", default="auto", choices=["auto", "strong", "weak"])
+    ap.add_argument("--dump", default="", help="write result slabs per rank (parity test)")
+    ap.add_argument("--cpu-leg", default="", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_leg:  # internal: one reference CPU leg in a fresh process
+        slab, steps, warm = (int(v) for v in args.cpu_leg.split(","))
+        print(json.dumps(cpu_leg(slab, steps, warm)), flush=True)
+        return
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":

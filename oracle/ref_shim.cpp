@@ -470,6 +470,46 @@ int ref_bench_step(const double* dense_x, const tt_shape* sx, const int* dims, i
     secs[3] = sink;
   });
 }
+// Split form of ref_bench_step for the CPU baseline legs: pack X once
+// (timed), run tt_sum(tt_mul(X, W), dim) over `dims` as many times as the
+// caller asks (each call timed), unpack the last results once (timed).
+std::unique_ptr<TileTensor> g_bench_x;
+std::vector<TileTensor> g_bench_outs;
+
+int ref_bench_pack_x(const double* dense_x, const tt_shape* sx, double* secs) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    if (!g_bench_w) throw std::logic_error("ref_bench_prepare_w first");
+    g_bench_outs.clear();
+    g_bench_x.reset();
+    auto t0 = clk::now();
+    g_bench_x = std::make_unique<TileTensor>(pack(dense_of(dense_x, sx), to_ref(sx), *g_bench_session));
+    secs[0] = std::chrono::duration<double>(clk::now() - t0).count();
+  });
+}
+
+int ref_bench_mul_sum(const int* dims, int ndims, double* secs) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    if (!g_bench_x) throw std::logic_error("ref_bench_pack_x first");
+    g_bench_outs.clear();
+    auto t0 = clk::now();
+    for (int k = 0; k < ndims; ++k) g_bench_outs.push_back(tt_sum(tt_mul(*g_bench_x, *g_bench_w), dims[k]));
+    secs[0] = std::chrono::duration<double>(clk::now() - t0).count();
+  });
+}
+
+int ref_bench_unpack(double* secs) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    auto t0 = clk::now();
+    double sink = 0;
+    for (const auto& o : g_bench_outs) sink += unpack(o).values()[0];
+    secs[0] = std::chrono::duration<double>(clk::now() - t0).count();
+    secs[1] = sink;
+  });
+}
+
 // One call = pack a seeded dense tensor, then tt_sum(tt_mul(X, W), dim) for each
 // dim in `dims`, then unpack each result, exactly through the reference API.
 // Returns wall seconds of each phase in secs[0..2] (pack, mul+sum, unpack).

@@ -5,8 +5,9 @@
 * ``paper_2011_01805_b200/_lib/tt_host_tests`` -- C++ tests of the host mirror
   headers (run by ``tests/test_cpp_host.py`` on a GPU).
 * ``oracle/_build/libttoracle.so`` -- the CPU restatement (test checker only).
-* ``oracle/_ref/libttref.so`` -- the reference itself, only when
-  ``/root/reference`` is present (this container; never on the GPU box).
+* ``oracle/_ref/libttref.so`` -- the reference itself, compiled from its headers
+  where they lie (``/root/reference`` in this container) or from the git-ignored
+  copy ``baseline/_ref/include`` that travels to the GPU box.
 
 Sources are compiled only when newer than their outputs.
 """
@@ -27,7 +28,12 @@ HOST_TESTS = LIB_DIR / "tt_host_tests"
 ORACLE_DIR = ROOT / "oracle"
 ORACLE_LIB = ORACLE_DIR / "_build" / "libttoracle.so"
 REF_LIB = ORACLE_DIR / "_ref" / "libttref.so"
-REF_INC = Path(os.environ.get("TT_REFERENCE_INCLUDE", "/root/reference/proj/include"))
+REF_SRC = Path("/root/reference/proj/include")
+# the reference headers travel to the GPU box as a git-ignored copy,
+# so `make ref` also works where /root/reference does not exist
+REF_COPY = ROOT / "baseline" / "_ref" / "include"
+REF_INC = Path(os.environ.get("TT_REFERENCE_INCLUDE",
+                              str(REF_SRC if (REF_SRC / "tiletensor").is_dir() else REF_COPY)))
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -81,7 +87,23 @@ def build_host_tests(verbose: bool = False) -> Path:
     return HOST_TESTS
 
 
+def _copy_reference_headers() -> None:
+    """Mirror the reference's headers into baseline/_ref/include (git-ignored,
+    shipped with the gpurun snapshot); never written back to the reference."""
+    import shutil
+    src = REF_SRC / "tiletensor"
+    if not src.is_dir():
+        return
+    dst = REF_COPY / "tiletensor"
+    dst.mkdir(parents=True, exist_ok=True)
+    for f in src.glob("*.hpp"):
+        out = dst / f.name
+        if not out.exists() or out.read_bytes() != f.read_bytes():
+            shutil.copyfile(f, out)
+
+
 def build_oracle(verbose: bool = False) -> None:
+    _copy_reference_headers()
     targets = ["oracle"]
     if (REF_INC / "tiletensor").is_dir():
         targets.append("ref")

@@ -102,6 +102,28 @@ def broadcast_operand(data, src: int = 0, group=None) -> None:
         dist.broadcast(data, src=src, group=group)
 
 
+def _p2p_staged(dist, group) -> bool:
+    """gloo moves point-to-point messages through host memory only: device
+    tensors are staged through a host copy (the functional multi-rank check
+    on one GPU); NCCL sends device memory directly over NVLink."""
+    return dist.get_backend(group) == "gloo"
+
+
+def _send(dist, t, dst, group):
+    if _p2p_staged(dist, group) and getattr(t, "is_cuda", False):
+        t = t.cpu()
+    dist.send(t, dst=dst, group=group)
+
+
+def _recv_into(dist, t, src, group):
+    if _p2p_staged(dist, group) and getattr(t, "is_cuda", False):
+        h = t.new_empty(t.shape, device="cpu")
+        dist.recv(h, src=src, group=group)
+        t.copy_(h)
+    else:
+        dist.recv(t, src=src, group=group)
+
+
 def sharded_mul_sum(x_local, w_local, dim: int, x_plan: ShardPlan,
                     mul_sum: Callable[[Any, Any, int], Any],
                     data_of: Callable[[Any], Any], group=None):
@@ -144,10 +166,10 @@ def chain_mul_sum(x_local, w_local, dim: int, x_plan: ShardPlan, fold: Callable,
         init = None
         if rank > 0:
             init = new_acc(hi - lo)
-            dist.recv(init, src=rank - 1, group=group)
+            _recv_into(dist, init, rank - 1, group)
         acc = fold(x_local, w_local, dim, (lo, hi), init)
         if rank < world - 1:
-            dist.send(acc, dst=rank + 1, group=group)
+            _send(dist, acc, rank + 1, group)
         else:
             parts.append(acc)
     result = finish(parts) if rank == world - 1 else None

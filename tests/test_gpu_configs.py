@@ -236,3 +236,19 @@ def test_config5_full_size_slabs(gpu, oracle):
     got = tt.unpack(r1)[0, :32, :]
     dense = (xs2 * configs.c5_w(slice(0, 32))).sum(axis=0)
     assert oracle.max_rel_diff(got, dense) < 1e-12
+    # middle and last slabs: groups the persistent grids reach in later loop
+    # iterations (group index >= 148), the last external rows / columns and
+    # the sliding-window wrap on the final chunks
+    r2, r3 = tt.tt_mul_sum(X, W, 2), tt.tt_mul_sum(X, W, 3)
+    ss1 = tt.TileTensorShape([tt.DimSpec(16, 1, 16), tt.DimSpec(2048, 1, 32), tt.DimSpec(512, 1, 32)])
+    for row in (64, 97, 127):                      # external rows of dim 1
+        px = oracle.pack(configs.c5_x_slab(slice(16 * row, 16 * row + 16)), ss1, s)
+        assert bitwise_equal(X.data()[1024 * row:1024 * (row + 1)].cpu().numpy(), px), row
+        for dim, r, per in ((2, r2, 16), (3, r3, 64)):
+            _, want, _ = oracle.mul_sum(ss1, px, sw, pw, s, dim)
+            assert bitwise_equal(r.data()[per * row:per * (row + 1)].cpu().numpy(), want), (dim, row)
+    for l2 in (31, 63):                            # external columns of dim 2
+        cols = slice(32 * l2, 32 * l2 + 32)
+        px2 = oracle.pack(configs.c5_x_slab(slice(None), cols), ss2, s)
+        so, want, _ = oracle.mul_sum(ss2, px2, sw2, oracle.pack(configs.c5_w(cols), sw2, s), s, 1)
+        assert bitwise_equal(r1.data()[16 * l2:16 * (l2 + 1)].cpu().numpy(), want), l2
