@@ -539,6 +539,8 @@ def run_ours(args):
             ops.update(bench_extra_ops(tt, X, W, x_dense, sx, S, stream, hbm_peak, args, out_tiles))
             ops.update(bench_matmul(tt, configs, S, stream, hbm_peak, max(3, args.steps)))
             ops.update(bench_small_configs(tt, configs, stream, hbm_peak, max(20, args.steps)))
+            if rank == 0:
+                ops["cpp"] = bench_cpp_leg()
     except Exception as exc:  # keep the bench line: report the failure instead
         print(f"[bench] extra failed: {exc!r}", file=sys.stderr)
         ops["extra_error"] = repr(exc)
@@ -715,6 +717,24 @@ def bench_e2e(tt, args, sharding, plan, X, W, x_dense, w_dense, sx, sw, S, dist,
                 "path": "tt.pack(host) -> tt_mul_sum x3 (+ dim-1 all-reduce) -> tt.unpack (D2H)"}
     except Exception as exc:  # keep the bench line: report the failure instead
         print(f"[bench] e2e failed: {exc!r}", file=sys.stderr)
+        return {"error": repr(exc)}
+
+
+def bench_cpp_leg():
+    """Configs 1-4 per call through the C++ drop-in headers (tests_cpp/bench_cpp.cpp:
+    the reference's tiletensor:: API, results from the session's stream-ordered
+    pool), with each call's CUDA-graph replay beside it."""
+    from paper_2011_01805_b200 import build
+    try:
+        exe = build.build_cpp_bench()
+        proc = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+        if proc.returncode != 0:
+            return {"error": proc.stderr[-400:]}
+        out = json.loads(proc.stdout.strip().splitlines()[-1])
+        out["note"] = ("C++ per-call time through tiletensor_b200/*.hpp (host enqueue + device, "
+                       "drained once per loop); graph_replay_us: the same call as a CUDA graph")
+        return out
+    except Exception as exc:
         return {"error": repr(exc)}
 
 

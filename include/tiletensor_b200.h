@@ -138,6 +138,12 @@ uint64_t tt_session_launches(const tt_session* s);
 void tt_session_count_bootstraps(tt_session* s, int64_t count);
 
 /* ---- device memory helpers -------------------------------------------- */
+/* Stream-ordered: tt_device_alloc takes the block from the session's memory
+ * pool in order on the session stream (usable by work enqueued after it on
+ * that stream), tt_device_free returns it in order (after the work enqueued
+ * before it).  Neither synchronises the device; both are legal during stream
+ * capture.  Replaces the reference's per-tile std::vector storage
+ * (backend.hpp:65-80, tile_tensor.hpp:151). */
 int tt_device_alloc(tt_session* s, int64_t bytes, void** out);
 int tt_device_free(tt_session* s, void* p);
 int tt_copy_h2d(tt_session* s, void* dst, const void* host_src, int64_t bytes);

@@ -355,17 +355,6 @@ int ref_nn_params(const char* spec, uint64_t seed, double* out, int64_t cap, int
   });
 }
 
-// parse_plan + validate_plan (nn.hpp:586-700): the report's to_text() into buf.
-int ref_validate_plan(const char* plan, int64_t slots, int64_t depth, char* buf, int64_t cap) {
-  return guard([&] {
-    std::istringstream in(plan);
-    const auto steps = parse_plan(in);
-    const std::string text = validate_plan(steps, BackendConfig{slots, depth}).to_text();
-    if (static_cast<int64_t>(text.size()) + 1 > cap) throw std::invalid_argument("buffer too small");
-    std::memcpy(buf, text.c_str(), text.size() + 1);
-  });
-}
-
 int ref_clean_unknowns(const tt_shape* sh, const double* tin, int64_t slots, tt_shape* so,
                        double* out, tt_cost* c) {
   return guard([&] {

@@ -25,6 +25,7 @@ LIB_DIR = PKG / "_lib"
 OBJ_DIR = LIB_DIR / "obj"
 LIB = LIB_DIR / "libtiletensor_b200.so"
 HOST_TESTS = LIB_DIR / "tt_host_tests"
+CPP_BENCH = LIB_DIR / "tt_bench_cpp"
 ORACLE_DIR = ROOT / "oracle"
 ORACLE_LIB = ORACLE_DIR / "_build" / "libttoracle.so"
 REF_LIB = ORACLE_DIR / "_ref" / "libttref.so"
@@ -102,6 +103,20 @@ def _copy_reference_headers() -> None:
             shutil.copyfile(f, out)
 
 
+def build_cpp_bench(verbose: bool = False) -> Path:
+    """The C++ performance leg (tests_cpp/bench_cpp.cpp) over the drop-in headers."""
+    src = PKG / "tests_cpp" / "bench_cpp.cpp"
+    hdrs = sorted((PKG / "include" / "tiletensor_b200").glob("*.hpp"))
+    if src.exists() and _stale(CPP_BENCH, [src, LIB, *hdrs]):
+        if verbose:
+            print("[build] g++ bench_cpp.cpp")
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", str(ROOT / "include"),
+              "-I", str(PKG / "include"), "-I", "/usr/local/cuda/include", str(src), "-o",
+              str(CPP_BENCH), "-L", str(LIB_DIR), "-ltiletensor_b200", "-L", "/usr/local/cuda/lib64",
+              "-lcudart", "-Wl,-rpath,$ORIGIN", "-Wl,-rpath,/usr/local/cuda/lib64", "-pthread"])
+    return CPP_BENCH
+
+
 def build_oracle(verbose: bool = False) -> None:
     _copy_reference_headers()
     targets = ["oracle"]
@@ -114,6 +129,7 @@ def build_all(verbose: bool = False) -> None:
     build_product(verbose)
     build_oracle(verbose)
     build_host_tests(verbose)
+    build_cpp_bench(verbose)
 
 
 if __name__ == "__main__":

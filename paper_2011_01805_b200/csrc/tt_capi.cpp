@@ -44,6 +44,12 @@ struct tt_session {
   // session), and rebuilding it per call costs more host time than a small
   // op's kernels take on the GPU
   std::map<std::array<int64_t, 6>, std::shared_ptr<const ttb::Program>> programs;
+  // stream-ordered memory pool of tt_device_alloc / tt_device_free (operator
+  // results and staging buffers of the C++ drop-in): allocations and frees are
+  // ordered on the session stream, never synchronise the device, and are legal
+  // inside stream capture; freed blocks stay cached in the pool (no release
+  // threshold) so a steady-state op chain does no driver allocation at all
+  cudaMemPool_t pool = nullptr;
 };
 
 namespace {
@@ -343,6 +349,14 @@ int tt_session_create(int64_t slot_count, int64_t max_chain_index, int device, t
       check_cuda(cudaSetDevice(device), "cudaSetDevice");
       check_cuda(cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking), "stream");
       s->stream = s->own_stream;
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      check_cuda(cudaMemPoolCreate(&s->pool, &props), "memory pool");
+      uint64_t keep = ~uint64_t{0};
+      check_cuda(cudaMemPoolSetAttribute(s->pool, cudaMemPoolAttrReleaseThreshold, &keep), "pool threshold");
       cudaDeviceProp prop{};
       check_cuda(cudaGetDeviceProperties(&prop, device), "device properties");
       s->sm_count = prop.multiProcessorCount;
@@ -365,6 +379,8 @@ void tt_session_destroy(tt_session* s) {
   if (s->scratch) cudaFree(s->scratch);
   for (double* p : s->retired) cudaFree(p);
   if (s->sched) cudaFree(s->sched);
+  if (s->stream && s->stream != s->own_stream) cudaStreamSynchronize(s->stream);
+  if (s->pool) cudaMemPoolDestroy(s->pool);
   if (s->own_stream) cudaStreamDestroy(s->own_stream);
   delete s;
 }
@@ -431,16 +447,22 @@ void tt_session_count_bootstraps(tt_session* s, int64_t count) {
 int tt_device_alloc(tt_session* s, int64_t bytes, void** out) {
   return guarded([&] {
     need_session(s);
-    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
     *out = nullptr;
-    if (bytes > 0) check_cuda(cudaMalloc(out, static_cast<size_t>(bytes)), "cudaMalloc");
+    if (bytes <= 0) return;
+    std::lock_guard<std::mutex> lk(s->mu);
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    check_cuda(cudaMallocFromPoolAsync(out, static_cast<size_t>(bytes), s->pool, s->stream),
+               "cudaMallocFromPoolAsync");
   });
 }
 
 int tt_device_free(tt_session* s, void* p) {
   return guarded([&] {
     need_session(s);
-    if (p) check_cuda(cudaFree(p), "cudaFree");
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(s->mu);
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    check_cuda(cudaFreeAsync(p, s->stream), "cudaFreeAsync");
   });
 }
 

@@ -13,8 +13,10 @@ replicate_dim and the batch-packed affine fold -- runs on the GPU.
   nn_forward                  nn.hpp:202-257   (plaintext oracle, same left folds)
   infer_batch_packed          nn.hpp:270-346   (one tt_batch_affine pass per layer)
   cryptonets_infer            nn.hpp:350-507
-  bootstrap_lower_bound       nn.hpp:523-531
-  validate_plan / parse_plan  nn.hpp:534-700   (handcrafted shape / chain plan checker)
+
+The reference's bootstrap_lower_bound and handcrafted-plan checker
+(nn.hpp:511-700) are planning tools off the hot path (SURVEY.md section 2:
+out of scope) and are not mirrored.
 """
 from __future__ import annotations
 
@@ -679,158 +681,3 @@ class CompiledTiled:
         if int(batch.shape[0]) != self.net.input_size():
             raise ShapeError("batch feature size mismatch")
         return _infer_tiled(self.net, batch, self.tile, self.session, self._cache)
-
-
-# ---- bootstrap lower bound (nn.hpp:511-531) ------------------------------------------
-
-
-@dataclass
-class FilterGroup:
-    count: int = 1
-    filter_h: int = 1
-    filter_w: int = 1
-    out_rows: int = 1
-
-
-def bootstrap_lower_bound(groups: Sequence[FilterGroup], depth: int) -> int:
-    if depth < 1:
-        raise ValueError("depth must be >= 1")
-    num = sum(g.count * 3 * min(g.out_rows, g.filter_h * g.filter_w) for g in groups)
-    return (num + depth - 1) // depth
-
-
-# ---- handcrafted plan checker (nn.hpp:534-700) -----------------------------------------
-
-
-@dataclass
-class BackendConfig:  # backend.hpp BackendConfig{slot_count, max_chain_index}
-    slot_count: int = 1
-    max_chain_index: int = 1
-
-
-@dataclass
-class PlanStep:
-    name: str = ""
-    op: str = ""  # add sub mul square mask scale sum matmul rotate reshape concat bridge bootstrap
-    inputs: list = field(default_factory=list)  # tile tensor shape strings
-    output: str = ""
-    chain_before: int = 0
-    chain_after: int = 0
-
-
-@dataclass
-class PlanIssue:
-    step: int = 0  # 1-based
-    info: bool = False
-    message: str = ""
-
-
-@dataclass
-class PlanReport:
-    ok: bool = True
-    issues: list = field(default_factory=list)
-    bootstraps: int = 0
-
-    def to_text(self) -> str:
-        out = "".join(f"step {i.step}: {'note: ' if i.info else 'violation: '}{i.message}\n"
-                      for i in self.issues)
-        return out + f"bootstraps={self.bootstraps}\nok={'true' if self.ok else 'false'}\n"
-
-
-_MUL_LIKE = {"mul", "square", "mask", "scale", "matmul"}
-_ELEMENTWISE_LIKE = {"add", "sub", "mul", "matmul"}
-_DECLARED_EDGE = {"reshape", "concat", "bridge"}
-
-
-def validate_plan(steps: Sequence[PlanStep], config: BackendConfig) -> PlanReport:
-    """Every shape must parse; elementwise / matmul steps must pass the shape
-    compatibility rules; chain indices may not go negative or above the depth
-    and drop by one exactly on multiplication-like steps; bootstraps restore
-    the depth.  Reshape / concat / bridge and rank-bridging pairs are noted."""
-    rep = PlanReport()
-
-    def violation(i, msg):
-        rep.issues.append(PlanIssue(i + 1, False, msg))
-        rep.ok = False
-
-    def note(i, msg):
-        rep.issues.append(PlanIssue(i + 1, True, msg))
-
-    for i, st in enumerate(steps):
-        shapes = []
-        shapes_ok = True
-        for text in st.inputs:
-            try:
-                shapes.append(tt.parse_shape(text))
-            except ShapeError as e:
-                violation(i, f"input shape '{text}' does not parse: {e}")
-                shapes_ok = False
-        if st.output:
-            try:
-                tt.parse_shape(st.output)
-            except ShapeError as e:
-                violation(i, f"output shape '{st.output}' does not parse: {e}")
-                shapes_ok = False
-        if st.chain_before < 0 or st.chain_after < 0:
-            violation(i, "chain index drops below 0 (bootstrap needed before this step)")
-        if st.chain_before > config.max_chain_index or st.chain_after > config.max_chain_index:
-            violation(i, "chain index exceeds the configured depth")
-        if st.op == "bootstrap":
-            rep.bootstraps += 1
-            if st.chain_after != config.max_chain_index:
-                violation(i, f"bootstrap must restore the chain index to {config.max_chain_index}")
-        else:
-            expected = st.chain_before - (1 if st.op in _MUL_LIKE else 0)
-            if st.chain_after != expected:
-                violation(i, f"chain index after '{st.op}' should be {expected}, declared "
-                             f"{st.chain_after}")
-        if shapes_ok and st.op in _DECLARED_EDGE:
-            note(i, f"'{st.op}' step accepted as a declared edge (no shape derivation)")
-        elif shapes_ok and st.op in _ELEMENTWISE_LIKE and len(shapes) >= 2:
-            if any(sh.rank() != shapes[0].rank() for sh in shapes):
-                note(i, "inputs of different rank; rank-bridging accepted as declared")
-            else:
-                kind = tt.OpKind.mul if st.op in ("mul", "matmul") else tt.OpKind.add
-                try:
-                    acc = shapes[0]
-                    for sh in shapes[1:]:
-                        acc = tt.elementwise_result_shape(acc, sh, kind)
-                except ShapeError as e:
-                    violation(i, f"incompatible operand shapes: {e}")
-    return rep
-
-
-def parse_plan(text: str) -> list:
-    """`step <name> op=<kind> in=<shape> [in=<shape>...] out=<shape> chain=<before>:<after>`."""
-    steps = []
-    for line in text.splitlines():
-        tok = line.split()
-        if not tok or tok[0].startswith("#"):
-            continue
-        if tok[0] != "step" or len(tok) < 2:
-            raise RuntimeError("plan lines must start with 'step <name>': " + line)
-        st = PlanStep(name=tok[1])
-        for t in tok[2:]:
-            if "=" not in t:
-                raise RuntimeError("expected key=value token in: " + line)
-            key, value = t.split("=", 1)
-            if key == "op":
-                st.op = value
-            elif key == "in":
-                st.inputs.append(value)
-            elif key == "out":
-                st.output = value
-            elif key == "chain":
-                if ":" not in value:
-                    raise RuntimeError("chain must be <before>:<after> in: " + line)
-                a, b = value.split(":", 1)
-                try:
-                    st.chain_before, st.chain_after = int(a), int(b)
-                except ValueError:
-                    raise RuntimeError("chain must be <before>:<after> in: " + line) from None
-            else:
-                raise RuntimeError(f"unknown plan key '{key}' in: " + line)
-        if not st.op:
-            raise RuntimeError("plan step missing op=: " + line)
-        steps.append(st)
-    return steps

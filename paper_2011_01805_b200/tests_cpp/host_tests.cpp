@@ -176,13 +176,13 @@ static void backend() {
   for (int w = 0; w < 8; ++w)
     pool.emplace_back([&] {
       const Tile c = s5.constant_tile(1.0);
-      for (int i = 0; i < 200; ++i) {
+      for (int i = 0; i < 2000; ++i) {
         (void)s5.add(c, c);
         (void)s5.rotate(c, 1);
       }
     });
   for (auto& th : pool) th.join();
-  CHECK(s5.cost_report().additions == 1600 && s5.cost_report().rotations == 1600);
+  CHECK(s5.cost_report().additions == 16000 && s5.cost_report().rotations == 16000);
 }
 
 // ---- test_rotate_sum.cpp -----------------------------------------------------
@@ -642,7 +642,7 @@ static void nn_suite() {
     CHECK_THROWS_AS(cryptonets_infer(net, random_tensor({36, 9}, rng, -1, 1), {2, 4, 8}, session),
                     ShapeError);
   }
-  {  // im2col, text tensors, bootstrap bound
+  {  // im2col, text tensors
     const DenseTensor x = random_tensor({4, 4}, rng, -1, 1);
     const DenseTensor m1 = im2col(x, 2, 2, 2, 0);
     CHECK(m1.shape() == (std::vector<std::int64_t>{4, 4}) && m1(3, 0) == x(2, 2));
@@ -651,24 +651,6 @@ static void nn_suite() {
     std::stringstream io;
     write_tensor(io, x);
     CHECK(read_tensor(io) == x);
-    const std::vector<FilterGroup> groups{{32, 3, 50, 18}, {32, 5, 50, 16}};
-    CHECK(bootstrap_lower_bound(groups, 3) == 1088 && bootstrap_lower_bound(groups, 1) == 3264);
-    CHECK_THROWS_AS(bootstrap_lower_bound(groups, 0), std::invalid_argument);
-  }
-  {  // plan checker (tests/test_nn.cpp:304-385 behaviour)
-    std::vector<PlanStep> steps;
-    for (int i = 0; i < 4; ++i)
-      steps.push_back(PlanStep{"mul" + std::to_string(i + 1), "mul", {"[4/4]", "[4/4]"}, "[4/4]", 3 - i, 2 - i});
-    const auto rep = validate_plan(steps, BackendConfig{4, 3});
-    CHECK(!rep.ok && rep.issues.size() == 1 && rep.issues[0].step == 4 && !rep.issues[0].info);
-    const std::vector<PlanStep> bridge{PlanStep{"conv", "mul", {"[18,*/32,150/256,255]", "[1,32/32,150/256]"},
-                                                "[18,32/32,150/256,255]", 4, 3}};
-    const auto rb = validate_plan(bridge, BackendConfig{8192, 4});
-    CHECK(rb.ok && rb.issues.size() == 1 && rb.issues[0].info);
-    std::istringstream bad("step s1 op=add in=[4/4] out=[4/4] chain=11\n");
-    CHECK_THROWS_AS(parse_plan(bad), std::runtime_error);
-    std::istringstream fine("# c\nstep s1 op=add in=[4/4] in=[4/4] out=[4/4] chain=1:1\n");
-    CHECK(parse_plan(fine).size() == 1);
   }
 }
 

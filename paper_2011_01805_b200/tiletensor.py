@@ -681,6 +681,8 @@ def _product(which: int, a: TileTensor, b: TileTensor, variant) -> TileTensor:
                                    _ptr(out), ctypes.byref(chain)))
     shape = TileTensorShape.from_c(so)
     n = shape.tile_count()
+    if n > out.shape[0]:  # the host-side sizing and the C-ABI disagree: never hand out a short view
+        raise ShapeError(f"product result has {n} tiles, {out.shape[0]} allocated")
     return TileTensor._wrap(shape, out if n == out.shape[0] else out[:n], s, chain.value)
 
 

@@ -302,13 +302,6 @@ class Ref(_Base):
         r = rows.value
         return out[:r * batch.shape[1]].reshape(r, batch.shape[1]).copy(), _cost(c)
 
-    def validate_plan(self, plan_text, slots, depth):
-        """The reference's parse_plan + validate_plan report text (or CheckerError)."""
-        buf = ctypes.create_string_buffer(1 << 20)
-        self._rc(self.lib.ref_validate_plan(plan_text.encode(), ctypes.c_int64(slots),
-                                            ctypes.c_int64(depth), buf, ctypes.c_int64(len(buf))))
-        return buf.value.decode()
-
     def nn_params(self, spec, seed):
         """parse_network's seeded weights and biases, flattened in layer order."""
         cap = 1 << 20

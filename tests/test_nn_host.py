@@ -105,87 +105,3 @@ def test_tensor_text_round_trip():
         nn.read_tensor("1 2 3\n")
     with pytest.raises(RuntimeError):
         nn.read_tensor("shape: 2\n1 x\n")
-
-
-def test_bootstrap_lower_bound():
-    G = nn.FilterGroup
-    groups = [G(32, 3, 50, 18), G(32, 5, 50, 16)]
-    assert nn.bootstrap_lower_bound(groups, 3) == 1088
-    assert nn.bootstrap_lower_bound(groups, 4) == 816
-    assert nn.bootstrap_lower_bound([G(1, 3, 50, 18)], 3) == 18
-    assert nn.bootstrap_lower_bound([G(1, 2, 2, 100)], 1) == 12
-    with pytest.raises(ValueError):
-        nn.bootstrap_lower_bound(groups, 0)
-    prev = nn.bootstrap_lower_bound(groups, 1)
-    assert prev == 3264
-    for d in range(2, 65):
-        b = nn.bootstrap_lower_bound(groups, d)
-        assert b <= prev
-        if 3264 % d == 0:
-            assert b * d == 3264
-        prev = b
-
-
-# ---- plan checker (nn.hpp:534-700) ------------------------------------------------------
-
-REF_PLAN = "/root/reference/proj/tests/data/cnn_train_plan.txt"
-
-
-def _steps_text(steps):
-    out = []
-    for st in steps:
-        parts = [f"step {st.name}", f"op={st.op}"] + [f"in={x}" for x in st.inputs]
-        if st.output:
-            parts.append(f"out={st.output}")
-        parts.append(f"chain={st.chain_before}:{st.chain_after}")
-        out.append(" ".join(parts))
-    return "\n".join(out) + "\n"
-
-
-def test_plan_checker_kats():
-    P = nn.PlanStep
-    steps = [P(f"mul{i + 1}", "mul", ["[4/4]", "[4/4]"], "[4/4]", 3 - i, 2 - i) for i in range(4)]
-    rep = nn.validate_plan(steps, nn.BackendConfig(4, 3))
-    assert not rep.ok and len(rep.issues) == 1 and rep.issues[0].step == 4
-    assert not rep.issues[0].info
-    cfg = nn.BackendConfig(4, 3)
-    assert not nn.validate_plan([P("mul", "mul", ["[4/4]", "[4/4]"], "[4/4]", 3, 3)], cfg).ok
-    assert not nn.validate_plan([P("add", "add", ["[5/4]", "[6/4]"], "[6/4]", 3, 3)], cfg).ok
-    assert not nn.validate_plan([P("x", "add", ["[5/"], "[5/4]", 1, 1)], cfg).ok
-    assert not nn.validate_plan([P("boot", "bootstrap", ["[4/4]"], "[4/4]", 0, 2)], cfg).ok
-    assert nn.validate_plan([], cfg).ok
-    bridge = P("conv", "mul", ["[18,*/32,150/256,255]", "[1,32/32,150/256]"],
-               "[18,32/32,150/256,255]", 4, 3)
-    rep = nn.validate_plan([bridge], nn.BackendConfig(8192, 4))
-    assert rep.ok and len(rep.issues) == 1 and rep.issues[0].info
-    for bad in ("step s1 in=[4/4] out=[4/4] chain=1:1\n",
-                "step s1 op=add in=[4/4] out=[4/4] chain=11\n", "op=add\n", "step s1 op=add bogus\n"):
-        with pytest.raises(RuntimeError):
-            nn.parse_plan(bad)
-    assert len(nn.parse_plan("# c\nstep s1 op=add in=[4/4] in=[4/4] out=[4/4] chain=1:1\n")) == 1
-
-
-def test_plan_reports_match_reference(ref):
-    import os
-    import random
-    texts = []
-    if os.path.exists(REF_PLAN):
-        texts.append(open(REF_PLAN).read())
-    rng = random.Random(99)
-    shapes = ["[4/4]", "[5/4]", "[6/4]", "[*/4,8/2]", "[3/2,*/4]", "[5/", "[2,3/4]", "[8/8,1?/2]",
-              "[1,32/32,150/256]", "[18,*/32,150/256,255]"]
-    ops = ["add", "sub", "mul", "square", "mask", "scale", "sum", "matmul", "rotate", "reshape",
-           "concat", "bridge", "bootstrap"]
-    for _ in range(60):
-        steps = []
-        for k in range(rng.randint(0, 8)):
-            cb = rng.randint(-1, 5)
-            steps.append(nn.PlanStep(f"s{k}", rng.choice(ops),
-                                     [rng.choice(shapes) for _ in range(rng.randint(0, 3))],
-                                     rng.choice(shapes + [""]), cb, cb - rng.randint(-1, 2)))
-        texts.append(_steps_text(steps))
-    for text in texts:
-        for depth in (3, 4):
-            want = ref.validate_plan(text, 8192, depth)
-            got = nn.validate_plan(nn.parse_plan(text), nn.BackendConfig(8192, depth)).to_text()
-            assert got == want, text

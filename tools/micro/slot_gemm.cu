@@ -1,0 +1,292 @@
+// Microbenchmark: the tile-matmul fold (per-slot batched outer-product fold,
+// config 3 stage 1 shapes) fed by a TMA ring, to find where the FP64 pipe
+// loses issue cycles against the smem-only loop (tools/micro/gemm_loop.cu).
+//
+//   out[i][j][h] = fold_k ( A[k][i][h] * B[k][j][h] ),  k = 0..K-1 in order,
+//   each product and sum separately rounded (no FMA), starting from -0.0.
+//
+// A unit = PI x PJ groups x SL slots; a consumer thread owns RI x RJ groups of
+// one slot.  MODE 0: real ring; 1: consumers never wait for data (the ring
+// still streams); 2: the producer issues no TMA (barriers complete at once).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -std=c++17 -o slot_gemm slot_gemm.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) {                                                               \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__);      \
+      exit(1);                                                                             \
+    }                                                                                      \
+  } while (0)
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t par) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(
+          su32(b)),
+      "r"(par)
+      : "memory");
+}
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
+
+constexpr int NI = 32, NJ = 16, K = 48, S = 8192;
+
+template <int PI, int PJ, int SL, int RI, int RJ, int KS, int NS, int MODE, int MINB, int SCHED>
+__global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
+    sg_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, double* out,
+              int reps, unsigned* q) {
+  constexpr int kC = (PI / RI) * (PJ / RJ) * SL;  // consumer threads
+  constexpr int kCW = kC / 32;
+  constexpr int kA = KS * PI * SL, kB = KS * PJ * SL, kSt = kA + kB;
+  constexpr int nbi = NI / PI, nbj = NJ / PJ, nch = S / SL;
+  constexpr int units1 = nbi * nbj * nch;
+  constexpr int nst = K / KS;
+  extern __shared__ __align__(1024) double sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + NS * kSt);
+  uint64_t* empty = full + NS;
+  int* stu = reinterpret_cast<int*>(empty + NS);  // unit of each stage (-1: done)
+  const int units = units1 * reps;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kCW) {
+    if (lane != 0) return;
+    int st = 0;
+    uint32_t ph = 0;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int nsm = gridDim.x / MINB;
+    const int lo = (int)((long long)units * smid / nsm), hi = (int)((long long)units * (smid + 1) / nsm);
+    auto next = [&](int prev) -> int {
+      if (SCHED == 0) return prev < 0 ? blockIdx.x : prev + gridDim.x;
+      const int v = lo + (int)atomicAdd(&q[smid], 1u);
+      return v < hi ? v : units;
+    };
+    for (int u = next(-1); ; u = next(u)) {
+      if (u >= units) {
+        mbar_wait(&empty[st], ph ^ 1);
+        stu[st] = -1;
+        mbar_arrive(&full[st]);
+        break;
+      }
+      const int uu = u % units1;
+      const int ch = uu % nch, b = uu / nch, bi = b % nbi, bj = b / nbi;
+      for (int k = 0; k < nst; ++k) {
+        mbar_wait(&empty[st], ph ^ 1);
+        stu[st] = u;
+        if (MODE == 2) {
+          mbar_arrive(&full[st]);
+        } else {
+          mbar_expect(&full[st], kSt * 8);
+          tma3(sm + st * kSt, &mA, ch * SL, bi * PI, k * KS, &full[st]);
+          tma3(sm + st * kSt + kA, &mB, ch * SL, bj * PJ, k * KS, &full[st]);
+        }
+        if (++st == NS) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  const int sub = threadIdx.x / SL, slot = threadIdx.x % SL;
+  const int r0 = (sub / (PJ / RJ)) * RI, c0 = (sub % (PJ / RJ)) * RJ;
+  int st = 0;
+  uint32_t ph = 0;
+  for (;;) {
+    mbar_wait(&full[st], ph);
+    const int u = stu[st];
+    if (u < 0) break;
+    const int uu = u % units1;
+    const int ch = uu % nch, b = uu / nch, bi = b % nbi, bj = b / nbi;
+    double acc[RI][RJ];
+#pragma unroll
+    for (int i = 0; i < RI; ++i)
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) acc[i][j] = -0.0;
+    for (int k = 0; k < nst; ++k) {
+      if (k > 0) mbar_wait(&full[st], ph);
+      const double* sA = sm + st * kSt + r0 * SL + slot;
+      const double* sB = sm + st * kSt + kA + c0 * SL + slot;
+#pragma unroll
+      for (int h = 0; h < KS; ++h) {
+        double a[RI], bb[RJ];
+#pragma unroll
+        for (int i = 0; i < RI; ++i) a[i] = sA[h * PI * SL + i * SL];
+#pragma unroll
+        for (int j = 0; j < RJ; ++j) bb[j] = sB[h * PJ * SL + j * SL];
+#pragma unroll
+        for (int i = 0; i < RI; ++i)
+#pragma unroll
+          for (int j = 0; j < RJ; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], bb[j]));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == NS) {
+        st = 0;
+        ph ^= 1;
+      }
+    }
+    if (u < units1 || MODE != 0) {
+      double* o = out + ((size_t)(bi * PI + r0) * NJ + bj * PJ + c0) * S + ch * SL + slot;
+#pragma unroll
+      for (int i = 0; i < RI; ++i)
+#pragma unroll
+        for (int j = 0; j < RJ; ++j) o[((size_t)i * NJ + j) * S] = acc[i][j];
+    }
+  }
+}
+
+__global__ void ref_kernel(const double* A, const double* B, double* out) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)NI * NJ * S) return;
+  const int h = idx % S, g = idx / S, i = g / NJ, j = g % NJ;
+  double acc = -0.0;
+  for (int k = 0; k < K; ++k) acc = __dadd_rn(acc, __dmul_rn(A[((size_t)k * NI + i) * S + h], B[((size_t)k * NJ + j) * S + h]));
+  out[idx] = acc;
+}
+
+typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncFn enc() {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+  return (EncFn)p;
+}
+
+static void make_map(CUtensorMap* m, const double* base, int rows, int box_s, int box_r, int box_k) {
+  cuuint64_t dims[3] = {(cuuint64_t)S, (cuuint64_t)rows, (cuuint64_t)K};
+  cuuint64_t str[2] = {(cuuint64_t)S * 8, (cuuint64_t)rows * S * 8};
+  cuuint32_t box[3] = {(cuuint32_t)box_s, (cuuint32_t)box_r, (cuuint32_t)box_k};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    printf("encode failed %d\n", (int)r);
+    exit(1);
+  }
+}
+
+double *gA, *gB, *gO, *gR;
+unsigned* gQ;
+int g_sms;
+
+template <int PI, int PJ, int SL, int RI, int RJ, int KS, int NS, int MODE, int MINB, int SCHED = 1>
+void run(const char* name, int reps) {
+  CUtensorMap mA, mB;
+  make_map(&mA, gA, NI, SL, PI, KS);
+  make_map(&mB, gB, NJ, SL, PJ, KS);
+  constexpr int threads = (PI / RI) * (PJ / RJ) * SL + 32;
+  constexpr size_t smem = (size_t)NS * KS * (PI + PJ) * SL * 8 + 3 * NS * 8;
+  auto k = sg_kernel<PI, PJ, SL, RI, RJ, KS, NS, MODE, MINB, SCHED>;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, k));
+  const int units = (NI / PI) * (NJ / PJ) * (S / SL) * reps;
+  const int grid = occ * g_sms;
+  if (occ != MINB) { printf("%s: occupancy %d != %d, skipped\n", name, occ, MINB); return; }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  CK(cudaMemset(gO, 0xff, (size_t)NI * NJ * S * 8));
+  CK(cudaMemset(gQ, 0, 4096));
+  k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ);
+  CK(cudaDeviceSynchronize());
+  bool ok = true;
+  if (MODE == 0) {
+    std::vector<double> o((size_t)NI * NJ * S), r((size_t)NI * NJ * S);
+    CK(cudaMemcpy(o.data(), gO, o.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(r.data(), gR, r.size() * 8, cudaMemcpyDeviceToHost));
+    ok = memcmp(o.data(), r.data(), o.size() * 8) == 0;
+  }
+  float best = 1e30f;
+  for (int it = 0; it < 5; ++it) {
+    CK(cudaMemsetAsync(gQ, 0, 4096));
+    cudaEventRecord(e0);
+    k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  const double ops = 2.0 * NI * NJ * K * (double)S * reps;
+  printf("%-40s reps=%d thr=%3d occ=%d grid=%4d regs=%3d smem=%6zu  %8.2f us  %5.1f%% fp64 %s\n", name, reps, threads,
+         occ, grid, fa.numRegs, smem, best * 1e3, ops / (best * 1e-3) / 18.34e12 * 100, ok ? "bitwise-ok" : "MISMATCH");
+}
+
+int main() {
+  CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0));
+  const size_t na = (size_t)K * NI * S, nb = (size_t)K * NJ * S;
+  std::vector<double> h(na);
+  uint64_t x = 88172645463325252ull;
+  for (auto& v : h) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    v = ((x >> 11) * (1.0 / 9007199254740992.0)) * 2 - 1;
+  }
+  CK(cudaMalloc(&gA, na * 8));
+  CK(cudaMalloc(&gB, nb * 8));
+  CK(cudaMalloc(&gO, (size_t)NI * NJ * S * 8));
+  CK(cudaMalloc(&gR, (size_t)NI * NJ * S * 8));
+  CK(cudaMalloc(&gQ, 4096));
+  CK(cudaMemcpy(gA, h.data(), na * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(gB, h.data() + 7, nb * 8, cudaMemcpyHostToDevice));
+  ref_kernel<<<(NI * NJ * S + 255) / 256, 256>>>(gA, gB, gR);
+  CK(cudaDeviceSynchronize());
+  // the shipped shape: 16x16 groups x 16 slots, 8x4 per thread, 4x4 ring, 3 CTAs/SM
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 0>("16x16x16 8x4 ks4 ns4 static-rr", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 1>("16x16x16 8x4 ks4 ns4 per-SM", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 1>("16x16x16 8x4 ks4 ns4 per-SM", 8);
+  run<16, 16, 16, 8, 4, 4, 4, 2, 3, 1>("  ..no TMA", 8);
+  run<32, 16, 16, 8, 4, 4, 4, 0, 2>("32x16x16 8x4 ks4 ns4", 1);
+  run<32, 16, 16, 8, 4, 4, 4, 0, 2>("32x16x16 8x4 ks4 ns4", 8);
+  run<32, 16, 16, 8, 4, 4, 4, 2, 2>("  ..no TMA", 8);
+  run<32, 16, 8, 8, 4, 4, 6, 0, 3>("32x16x8 8x4 ks4 ns6", 1);
+  run<32, 16, 8, 8, 4, 4, 6, 0, 3>("32x16x8 8x4 ks4 ns6", 8);
+  run<32, 16, 8, 8, 4, 4, 6, 2, 3>("  ..no TMA", 8);
+  run<32, 16, 4, 8, 4, 4, 8, 0, 6>("32x16x4 8x4 ks4 ns8", 1);
+  run<32, 16, 4, 8, 4, 4, 8, 0, 6>("32x16x4 8x4 ks4 ns8", 8);
+  run<32, 16, 8, 8, 8, 4, 6, 0, 4>("32x16x8 8x8 ks4 ns6", 1);
+  run<32, 16, 8, 8, 8, 4, 6, 0, 4>("32x16x8 8x8 ks4 ns6", 8);
+  run<32, 16, 16, 8, 8, 4, 4, 0, 2>("32x16x16 8x8 ks4 ns4", 1);
+  run<16, 16, 16, 8, 4, 8, 3, 0, 3>("16x16x16 8x4 ks8 ns3", 1);
+  run<16, 16, 16, 8, 4, 2, 8, 0, 3>("16x16x16 8x4 ks2 ns8", 1);
+  run<16, 16, 8, 8, 4, 4, 6, 0, 4>("16x16x8 8x4 ks4 ns6", 1);
+  run<16, 16, 8, 8, 4, 4, 6, 0, 4>("16x16x8 8x4 ks4 ns6", 8);
+  return 0;
+}
