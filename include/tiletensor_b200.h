@@ -146,6 +146,15 @@ void tt_session_count_bootstraps(tt_session* s, int64_t count);
  * (backend.hpp:65-80, tile_tensor.hpp:151). */
 int tt_device_alloc(tt_session* s, int64_t bytes, void** out);
 int tt_device_free(tt_session* s, void* p);
+/* Result-tile cache on top of the pool (the Python mirror's operator results):
+ * tt_tiles_release keeps the block in a per-(stream, size) free list and
+ * tt_tiles_alloc hands it out again on the same stream with no driver call
+ * (stream order makes the reuse safe).  Freed blocks of a destroyed session
+ * are returned to the driver.  While the session stream is being captured
+ * tt_tiles_alloc returns TT_OK with *out == NULL: the caller allocates the
+ * result in the capturing framework's graph memory instead. */
+int tt_tiles_alloc(tt_session* s, int64_t bytes, void** out);
+int tt_tiles_release(tt_session* s, void* p);
 int tt_copy_h2d(tt_session* s, void* dst, const void* host_src, int64_t bytes);
 int tt_copy_d2h(tt_session* s, void* host_dst, const void* src, int64_t bytes);
 int tt_copy_d2d(tt_session* s, void* dst, const void* src, int64_t bytes);

@@ -70,6 +70,8 @@ SIGNATURES = {
     "tt_session_count_bootstraps": (None, [_P, _I64]),
     "tt_device_alloc": (_I, [_P, _I64, ctypes.POINTER(_P)]),
     "tt_device_free": (_I, [_P, _P]),
+    "tt_tiles_alloc": (_I, [_P, _I64, ctypes.POINTER(_P)]),
+    "tt_tiles_release": (_I, [_P, _P]),
     "tt_copy_h2d": (_I, [_P, _P, _P, _I64]),
     "tt_copy_d2h": (_I, [_P, _P, _P, _I64]),
     "tt_copy_d2d": (_I, [_P, _P, _P, _I64]),

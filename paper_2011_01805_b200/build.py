@@ -16,6 +16,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import sysconfig
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -26,6 +27,7 @@ OBJ_DIR = LIB_DIR / "obj"
 LIB = LIB_DIR / "libtiletensor_b200.so"
 HOST_TESTS = LIB_DIR / "tt_host_tests"
 CPP_BENCH = LIB_DIR / "tt_bench_cpp"
+PYFAST = PKG / ("_ttfast" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
 ORACLE_DIR = ROOT / "oracle"
 ORACLE_LIB = ORACLE_DIR / "_build" / "libttoracle.so"
 REF_LIB = ORACLE_DIR / "_ref" / "libttref.so"
@@ -73,7 +75,20 @@ def build_product(verbose: bool = False) -> Path:
                   "-o", str(o)])
     if _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"])
+    build_pyfast(verbose)
     return LIB
+
+
+def build_pyfast(verbose: bool = False) -> Path:
+    """The CPython fast-call module over the C-ABI (csrc/tt_pyfast.c)."""
+    src = CSRC / "tt_pyfast.c"
+    if _stale(PYFAST, [src, LIB, ROOT / "include" / "tiletensor_b200.h"]):
+        if verbose:
+            print("[build] gcc tt_pyfast.c")
+        _run(["gcc", "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"], "-I",
+              str(ROOT / "include"), str(src), "-o", str(PYFAST), "-L", str(LIB_DIR),
+              "-ltiletensor_b200", "-Wl,-rpath,$ORIGIN/_lib"])
+    return PYFAST
 
 
 def build_host_tests(verbose: bool = False) -> Path:

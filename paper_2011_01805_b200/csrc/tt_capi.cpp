@@ -16,6 +16,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "tt_internal.hpp"
@@ -50,6 +51,17 @@ struct tt_session {
   // inside stream capture; freed blocks stay cached in the pool (no release
   // threshold) so a steady-state op chain does no driver allocation at all
   cudaMemPool_t pool = nullptr;
+  // result-tile cache of tt_tiles_alloc / tt_tiles_release: blocks freed by
+  // their owner go to a free list keyed by (stream, bytes) and are handed out
+  // again only on that stream (stream order makes the reuse safe, as in
+  // torch's caching allocator), so a repeated op allocates with no driver call
+  struct CachedBlock {
+    size_t bytes;
+    cudaStream_t stream;
+  };
+  std::unordered_map<void*, CachedBlock> live;
+  std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free_blocks;
+  size_t cached_bytes = 0;
 };
 
 namespace {
@@ -380,6 +392,9 @@ void tt_session_destroy(tt_session* s) {
   for (double* p : s->retired) cudaFree(p);
   if (s->sched) cudaFree(s->sched);
   if (s->stream && s->stream != s->own_stream) cudaStreamSynchronize(s->stream);
+  for (auto& kv : s->free_blocks)
+    for (void* p : kv.second) cudaFree(p);
+  for (auto& kv : s->live) cudaFree(kv.first);
   if (s->pool) cudaMemPoolDestroy(s->pool);
   if (s->own_stream) cudaStreamDestroy(s->own_stream);
   delete s;
@@ -463,6 +478,54 @@ int tt_device_free(tt_session* s, void* p) {
     std::lock_guard<std::mutex> lk(s->mu);
     check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
     check_cuda(cudaFreeAsync(p, s->stream), "cudaFreeAsync");
+  });
+}
+
+// Cap on the bytes tt_tiles_release keeps cached per session; beyond it a
+// released block goes back to the pool (cudaFreeAsync).
+constexpr size_t kTileCacheBytes = size_t{8} << 30;
+
+int tt_tiles_alloc(tt_session* s, int64_t bytes, void** out) {
+  return guarded([&] {
+    need_session(s);
+    *out = nullptr;
+    if (bytes <= 0) bytes = 8;
+    const size_t nb = static_cast<size_t>(bytes);
+    std::lock_guard<std::mutex> lk(s->mu);
+    // under stream capture the result must live in the capturing framework's
+    // graph memory: hand out nothing, the caller allocates it itself
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    check_cuda(cudaStreamIsCapturing(s->stream, &cap), "capture status");
+    if (cap != cudaStreamCaptureStatusNone) return;
+    auto it = s->free_blocks.find({s->stream, nb});
+    if (it != s->free_blocks.end() && !it->second.empty()) {
+      *out = it->second.back();
+      it->second.pop_back();
+      s->cached_bytes -= nb;
+    } else {
+      check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+      check_cuda(cudaMallocFromPoolAsync(out, nb, s->pool, s->stream), "cudaMallocFromPoolAsync");
+    }
+    s->live[*out] = {nb, s->stream};
+  });
+}
+
+int tt_tiles_release(tt_session* s, void* p) {
+  return guarded([&] {
+    need_session(s);
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(s->mu);
+    auto it = s->live.find(p);
+    if (it == s->live.end()) invalid_argument("tt_tiles_release: not a tt_tiles_alloc block");
+    const tt_session::CachedBlock b = it->second;
+    s->live.erase(it);
+    if (s->cached_bytes + b.bytes <= kTileCacheBytes) {
+      s->free_blocks[{b.stream, b.bytes}].push_back(p);
+      s->cached_bytes += b.bytes;
+    } else {
+      check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+      check_cuda(cudaFreeAsync(p, b.stream), "cudaFreeAsync");
+    }
   });
 }
 

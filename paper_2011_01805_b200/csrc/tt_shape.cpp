@@ -57,6 +57,7 @@ Shape from_c(const tt_shape* c) {
 }
 
 void to_c(const Shape& s, tt_shape* out) {
+  if (out == nullptr) return;  // result shape not wanted (the caller already knows it)
   std::memset(out, 0, sizeof(*out));
   out->rank = s.rank();
   out->relaxed = s.relaxed ? 1 : 0;

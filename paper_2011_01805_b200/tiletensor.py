@@ -314,6 +314,9 @@ _COST_FIELDS = ("additions", "multiplications", "mask_multiplications", "rotatio
 # ---- session ------------------------------------------------------------------------
 
 
+_RAW_STREAM = None  # torch._C._cuda_getCurrentRawStream, bound on first Session
+
+
 def _current_raw_stream(device: int) -> int:
     """cudaStream_t of torch's current stream on `device` (the raw accessor
     when this torch has it: ~10x cheaper than building a Stream object)."""
@@ -344,6 +347,10 @@ class Session:
         self._depth = int(max_chain_index)
         self._device = int(device)
         self._stream = None  # stream last bound to the native session
+        self._tdev = _torch().device("cuda", self._device)
+        global _RAW_STREAM
+        if _RAW_STREAM is None:
+            _RAW_STREAM = getattr(_torch()._C, "_cuda_getCurrentRawStream", None)
 
     def __del__(self):
         p = getattr(self, "_ptr", None)
@@ -353,6 +360,14 @@ class Session:
             except Exception:
                 pass
             self._ptr = None
+
+    def _h(self) -> int:
+        """The session handle as an int (fast path), bound to torch's current stream."""
+        stream = _RAW_STREAM(self._device) if _RAW_STREAM is not None else _current_raw_stream(self._device)
+        if stream != self._stream:
+            _check(lib().tt_session_set_stream(self._ptr, ctypes.c_void_p(stream)))
+            self._stream = stream
+        return self._ptr.value
 
     @property
     def handle(self):
@@ -369,7 +384,7 @@ class Session:
         return self._depth
 
     def device(self):
-        return _torch().device("cuda", self._device)
+        return self._tdev
 
     def cost_report(self) -> CostReport:
         c = CCost()
@@ -391,7 +406,7 @@ class Session:
     # allocation helper
     def empty_tiles(self, count: int):
         torch = _torch()
-        return torch.empty((int(count), self._slots), dtype=torch.float64, device=self.device())
+        return torch.empty((int(count), self._slots), dtype=torch.float64, device=self._tdev)
 
 
 def _ptr(t) -> ctypes.c_void_p:
@@ -411,8 +426,43 @@ def _as_device(x, session: Session):
 # ---- tile tensors (tile_tensor.hpp:130-165) -------------------------------------------
 
 
+class _Block:
+    """A result block from the session's tile cache (tt_tiles_alloc): released
+    back to the cache (stream-ordered reuse, tt_tiles_release) when the last
+    reference -- the TileTensor, or a torch view made by data() -- goes away."""
+    __slots__ = ("ptr", "session", "__weakref__")
+
+    def __init__(self, ptr: int, session: "Session"):
+        self.ptr = ptr
+        self.session = session
+
+    def __del__(self):
+        try:
+            h = self.session._ptr
+            if h and h.value and _FASTMOD is not None:
+                _FASTMOD.release(h.value, self.ptr)
+        except Exception:
+            pass
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a _Block for torch.as_tensor (torch keeps
+    a reference to this object, hence to the block, for the tensor's life)."""
+
+    def __init__(self, block: _Block, shape):
+        self._block = block
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8",
+                                         "data": (block.ptr, False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
 class TileTensor:
-    """Shape + one device array [tile_count, s] + Session + chain index."""
+    """Shape + one device array [tile_count, s] + Session + chain index.
+
+    The array is a torch tensor, or (fast-path operator results) a block of
+    the session's tile cache that data() exposes as a torch tensor on demand."""
+
+    __slots__ = ("_shape", "_t", "_block", "_p", "_session", "_chain")
 
     def __init__(self, shape: TileTensorShape, tiles, session: Session, chain: Optional[int] = None):
         torch = _torch()
@@ -423,7 +473,9 @@ class TileTensor:
         if tiles.shape[0] != shape.tile_count():
             raise ShapeError("tile count does not match external shape")
         self._shape = shape
-        self._tiles = tiles.contiguous()
+        self._t = tiles.contiguous()
+        self._block = None
+        self._p = self._t.data_ptr()
         self._session = session
         self._chain = session.max_chain_index() if chain is None else int(chain)
 
@@ -433,9 +485,22 @@ class TileTensor:
         device array from Session.empty_tiles (no validation needed)."""
         obj = cls.__new__(cls)
         obj._shape = shape
-        obj._tiles = tiles
+        obj._t = tiles
+        obj._block = None
+        obj._p = tiles.data_ptr()
         obj._session = session
         obj._chain = int(chain)
+        return obj
+
+    @classmethod
+    def _wrap_block(cls, shape: TileTensorShape, ptr: int, session: Session, chain: int) -> "TileTensor":
+        obj = cls.__new__(cls)
+        obj._shape = shape
+        obj._t = None
+        obj._block = _Block(ptr, session)
+        obj._p = ptr
+        obj._session = session
+        obj._chain = chain
         return obj
 
     def shape(self) -> TileTensorShape:
@@ -449,17 +514,26 @@ class TileTensor:
 
     def data(self):
         """The device array [tile_count, s] (torch float64)."""
-        return self._tiles
+        if self._t is None:
+            n = self._shape.tile_count()
+            self._t = _torch().as_tensor(_CudaArray(self._block, (n, self._session._slots)),
+                                         device=self._session._tdev)
+        return self._t
 
     def tiles(self) -> np.ndarray:
         """Host copy of every tile, [tile_count, s] (TileTensor::tiles)."""
-        return self._tiles.detach().cpu().numpy()
+        return self.data().detach().cpu().numpy()
 
     def tile_at(self, flat: int) -> np.ndarray:
-        return self._tiles[flat].detach().cpu().numpy()
+        return self.data()[flat].detach().cpu().numpy()
 
     def chain_index(self) -> int:
         return self._chain
+
+
+def _dptr(t: TileTensor) -> ctypes.c_void_p:
+    """Device address of a tile tensor's array (no torch view needed)."""
+    return ctypes.c_void_p(t._p)
 
 
 def with_leading_unit_dim(t: TileTensor) -> TileTensor:  # tile_tensor.hpp:158-165
@@ -498,7 +572,7 @@ def unpack_device(t: TileTensor):
     s = t.session()
     ext = t.shape().tensor_extents()
     out = torch.empty(ext, dtype=torch.float64, device=s.device())
-    _check(lib().tt_unpack(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()), _ptr(out)))
+    _check(lib().tt_unpack(s.handle, ctypes.byref(t.shape().to_c()), _dptr(t), _ptr(out)))
     return out
 
 
@@ -531,10 +605,10 @@ def mul_fold(a: TileTensor, b: Optional[TileTensor], dim: int, out_range=None, i
     chain = ctypes.c_int64()
     if init is not None and tuple(init.shape) != (end - begin, s.slot_count()):
         raise ValueError("init must hold one tile per output tile of the range")
-    _check(lib().tt_mul_fold(s.handle, ctypes.byref(a.shape().to_c()), _ptr(a.data()),
+    _check(lib().tt_mul_fold(s.handle, ctypes.byref(a.shape().to_c()), _dptr(a),
                              a.chain_index(),
                              ctypes.byref(b.shape().to_c()) if b is not None else None,
-                             _ptr(b.data()) if b is not None else ctypes.c_void_p(0),
+                             _dptr(b) if b is not None else ctypes.c_void_p(0),
                              b.chain_index() if b is not None else 0, int(dim), begin, end,
                              _ptr(init), _ptr(acc), ctypes.byref(chain)))
     return acc, chain.value
@@ -553,15 +627,84 @@ def _result_tiles(key, compute) -> int:
     return n
 
 
+# ---- small-op fast path -------------------------------------------------------------
+# An operator's result shape, tile count and C structs depend only on its
+# operand shapes and arguments, so after the first call with a given key they
+# are reused: the repeat call is one torch allocation and ONE C-ABI call (which
+# still validates everything -- depth, slots -- before launching) with no
+# result-shape round trip.  The C side accepts a null out_shape / out_chain.
+
+class _Call:
+    __slots__ = ("nbytes", "shape", "ca", "cb", "v", "keep")
+
+    def __init__(self, nbytes, shape, ca, cb, v, keep):
+        self.nbytes, self.shape, self.ca, self.cb, self.v, self.keep = nbytes, shape, ca, cb, v, keep
+
+
+_FAST: dict = {}
+
+
+def _remember(key, shape: TileTensorShape, ca, cb, v, slots: int) -> None:
+    """ca / cb: the operands' cached tt_shape structs (immutable, owned by their
+    TileTensorShape, kept alive here); passed to the C-ABI by address."""
+    if len(_FAST) >= 4096:
+        _FAST.clear()
+    nbytes = max(1, shape.tile_count()) * slots * 8
+    _FAST[key] = _Call(nbytes, shape, ctypes.addressof(ca),
+                       ctypes.addressof(cb) if cb is not None else 0, -1 if v is None else v, (ca, cb))
+
+
+def _fastmod():
+    """The CPython fast-call module (csrc/tt_pyfast.c) over the same C-ABI."""
+    global _FASTMOD
+    if _FASTMOD is None:
+        lib()
+        from . import _ttfast
+        _FASTMOD = _ttfast
+    return _FASTMOD
+
+
+_FASTMOD = None
+
+
+_F64 = None
+
+
+def _empty(s: "Session", n: int):
+    global _F64
+    torch = _torch()
+    if _F64 is None:
+        _F64 = torch.float64
+    return torch.empty((n, s._slots), dtype=_F64, device=s._tdev)
+
+
 def tt_elementwise(a: TileTensor, b: TileTensor, op) -> TileTensor:
+    s = a._session
+    if b._session is s:
+        e = _FAST.get(("ew", op, a._shape, b._shape, s._slots))
+        if e is not None:
+            p = _fastmod().elementwise_new(s._h(), int(op), e.ca, a._p, a._chain, e.cb, b._p,
+                                           b._chain, e.nbytes)
+            if p < 0:
+                _check(-p)
+            if p:
+                chain = min(a._chain, b._chain) - (1 if int(op) == int(OpKind.mul) else 0)
+                return TileTensor._wrap_block(e.shape, p, s, chain)
+    r = _tt_elementwise(a, b, op)
+    _remember(("ew", op, a._shape, b._shape, s._slots), r._shape, a._shape.to_c(), b._shape.to_c(),
+              None, s._slots)
+    return r
+
+
+def _tt_elementwise(a: TileTensor, b: TileTensor, op) -> TileTensor:
     s = _same_session(a, b)
     so = CShape()
     chain = ctypes.c_int64()
     n_out = _result_tiles(("ew", int(op), a.shape(), b.shape()),
                           lambda: elementwise_result_shape(a.shape(), b.shape(), op).tile_count())
     out = s.empty_tiles(n_out)
-    _check(lib().tt_elementwise(s.handle, int(op), ctypes.byref(a.shape().to_c()), _ptr(a.data()),
-                                a.chain_index(), ctypes.byref(b.shape().to_c()), _ptr(b.data()),
+    _check(lib().tt_elementwise(s.handle, int(op), ctypes.byref(a.shape().to_c()), _dptr(a),
+                                a.chain_index(), ctypes.byref(b.shape().to_c()), _dptr(b),
                                 b.chain_index(), ctypes.byref(so), _ptr(out), ctypes.byref(chain)))
     return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
 
@@ -580,12 +723,27 @@ def _variant(v) -> int:
 
 def tt_sum(t: TileTensor, dim: int, variant: Optional[SumVariant] = None) -> TileTensor:
     """tt_sum tile_tensor.hpp:286-347."""
+    key = ("sum", t._shape, dim, variant, t._session._slots)
+    e = _FAST.get(key)
+    if e is not None:
+        s = t._session
+        p = _fastmod().sum_new(s._h(), e.ca, t._p, dim, e.v, e.nbytes)
+        if p < 0:
+            _check(-p)
+        if p:
+            return TileTensor._wrap_block(e.shape, p, s, t._chain)
+    r = _tt_sum(t, dim, variant)
+    _remember(key, r._shape, t._shape.to_c(), None, _variant(variant), t._session._slots)
+    return r
+
+
+def _tt_sum(t: TileTensor, dim: int, variant: Optional[SumVariant] = None) -> TileTensor:
     s = t.session()
     n_out = _result_tiles(("sum", t.shape(), int(dim)),
                           lambda: sum_result_shape(t.shape(), dim).tile_count())
     out = s.empty_tiles(n_out)
     so = CShape()
-    _check(lib().tt_sum(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()), int(dim),
+    _check(lib().tt_sum(s.handle, ctypes.byref(t.shape().to_c()), _dptr(t), int(dim),
                         _variant(variant), ctypes.byref(so), _ptr(out)))
     return TileTensor._wrap(TileTensorShape.from_c(so), out, s, t.chain_index())
 
@@ -593,14 +751,32 @@ def tt_sum(t: TileTensor, dim: int, variant: Optional[SumVariant] = None) -> Til
 def tt_mul_sum(a: TileTensor, b: TileTensor, dim: int,
                variant: Optional[SumVariant] = None) -> TileTensor:
     """tt_sum(tt_mul(a, b), dim) fused: one pass, product never stored."""
+    s = a._session
+    if b._session is s:
+        e = _FAST.get(("mulsum", a._shape, b._shape, dim, variant, s._slots))
+        if e is not None:
+            p = _fastmod().mul_sum_new(s._h(), e.ca, a._p, a._chain, e.cb, b._p, b._chain, dim, e.v,
+                                       e.nbytes)
+            if p < 0:
+                _check(-p)
+            if p:
+                return TileTensor._wrap_block(e.shape, p, s, min(a._chain, b._chain) - 1)
+    r = _tt_mul_sum(a, b, dim, variant)
+    _remember(("mulsum", a._shape, b._shape, dim, variant, s._slots), r._shape, a._shape.to_c(),
+              b._shape.to_c(), _variant(variant), s._slots)
+    return r
+
+
+def _tt_mul_sum(a: TileTensor, b: TileTensor, dim: int,
+                variant: Optional[SumVariant] = None) -> TileTensor:
     s = _same_session(a, b)
     n_out = _result_tiles(("mulsum", a.shape(), b.shape(), int(dim)), lambda: sum_result_shape(
         elementwise_result_shape(a.shape(), b.shape(), OpKind.mul), dim).tile_count())
     out = s.empty_tiles(n_out)
     so = CShape()
     chain = ctypes.c_int64()
-    _check(lib().tt_mul_sum(s.handle, ctypes.byref(a.shape().to_c()), _ptr(a.data()),
-                            a.chain_index(), ctypes.byref(b.shape().to_c()), _ptr(b.data()),
+    _check(lib().tt_mul_sum(s.handle, ctypes.byref(a.shape().to_c()), _dptr(a),
+                            a.chain_index(), ctypes.byref(b.shape().to_c()), _dptr(b),
                             b.chain_index(), int(dim), _variant(variant), ctypes.byref(so),
                             _ptr(out), ctypes.byref(chain)))
     return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
@@ -617,8 +793,8 @@ def tt_mul_sum_clean(a: TileTensor, b: TileTensor, dim: int,
     out = s.empty_tiles(n_out)
     so = CShape()
     chain = ctypes.c_int64()
-    _check(lib().tt_mul_sum_clean(s.handle, ctypes.byref(a.shape().to_c()), _ptr(a.data()),
-                                  a.chain_index(), ctypes.byref(b.shape().to_c()), _ptr(b.data()),
+    _check(lib().tt_mul_sum_clean(s.handle, ctypes.byref(a.shape().to_c()), _dptr(a),
+                                  a.chain_index(), ctypes.byref(b.shape().to_c()), _dptr(b),
                                   b.chain_index(), int(dim), _variant(variant), ctypes.byref(so),
                                   _ptr(out), ctypes.byref(chain)))
     return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
@@ -645,9 +821,9 @@ def tt_mul_sum_affine(a: TileTensor, b: TileTensor, dim: int, c: Optional[TileTe
     so = CShape()
     chain = ctypes.c_int64()
     _check(lib().tt_mul_sum_affine(
-        s.handle, ctypes.byref(a.shape().to_c()), _ptr(a.data()), a.chain_index(),
-        ctypes.byref(b.shape().to_c()), _ptr(b.data()), b.chain_index(), int(dim), _variant(variant),
-        None if c is None else ctypes.byref(c.shape().to_c()), None if c is None else _ptr(c.data()),
+        s.handle, ctypes.byref(a.shape().to_c()), _dptr(a), a.chain_index(),
+        ctypes.byref(b.shape().to_c()), _dptr(b), b.chain_index(), int(dim), _variant(variant),
+        None if c is None else ctypes.byref(c.shape().to_c()), None if c is None else _dptr(c),
         0 if c is None else c.chain_index(), 1 if square else 0, ctypes.byref(so), _ptr(out),
         ctypes.byref(chain)))
     return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
@@ -657,6 +833,23 @@ _PRODUCT_TILES: dict = {}
 
 
 def _product(which: int, a: TileTensor, b: TileTensor, variant) -> TileTensor:
+    s = a._session
+    if b._session is s:
+        e = _FAST.get(("prod", which, a._shape, b._shape, variant, s._slots))
+        if e is not None:
+            p = _fastmod().product_new(s._h(), which, e.ca, a._p, a._chain, e.cb, b._p, b._chain,
+                                       e.v, e.nbytes)
+            if p < 0:
+                _check(-p)
+            if p:
+                return TileTensor._wrap_block(e.shape, p, s, min(a._chain, b._chain) - 1)
+    r = _product_slow(which, a, b, variant)
+    _remember(("prod", which, a._shape, b._shape, variant, s._slots), r._shape, a._shape.to_c(),
+              b._shape.to_c(), _variant(variant), s._slots)
+    return r
+
+
+def _product_slow(which: int, a: TileTensor, b: TileTensor, variant) -> TileTensor:
     s = _same_session(a, b)
     so = CShape()
     chain = ctypes.c_int64()
@@ -675,8 +868,8 @@ def _product(which: int, a: TileTensor, b: TileTensor, variant) -> TileTensor:
         _PRODUCT_TILES[key] = n_out
     out = s.empty_tiles(max(n_out, 1))
     _check(lib().tt_linalg_product(s.handle, which, ctypes.byref(a.shape().to_c()),
-                                   _ptr(a.data()), a.chain_index(),
-                                   ctypes.byref(b.shape().to_c()), _ptr(b.data()),
+                                   _dptr(a), a.chain_index(),
+                                   ctypes.byref(b.shape().to_c()), _dptr(b),
                                    b.chain_index(), _variant(variant), ctypes.byref(so),
                                    _ptr(out), ctypes.byref(chain)))
     shape = TileTensorShape.from_c(so)
@@ -707,7 +900,7 @@ def clean_unknowns(t: TileTensor) -> TileTensor:  # tile_tensor.hpp:352-386
     out = s.empty_tiles(t.tile_count())
     so = CShape()
     chain = ctypes.c_int64()
-    _check(lib().tt_clean_unknowns(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()),
+    _check(lib().tt_clean_unknowns(s.handle, ctypes.byref(t.shape().to_c()), _dptr(t),
                                    t.chain_index(), ctypes.byref(so), _ptr(out),
                                    ctypes.byref(chain)))
     return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
@@ -717,7 +910,7 @@ def replicate_dim(t: TileTensor, dim: int) -> TileTensor:  # tile_tensor.hpp:391
     s = t.session()
     out = s.empty_tiles(t.tile_count())
     so = CShape()
-    _check(lib().tt_replicate_dim(s.handle, ctypes.byref(t.shape().to_c()), _ptr(t.data()),
+    _check(lib().tt_replicate_dim(s.handle, ctypes.byref(t.shape().to_c()), _dptr(t),
                                   int(dim), ctypes.byref(so), _ptr(out)))
     return TileTensor._wrap(TileTensorShape.from_c(so), out, s, t.chain_index())
 

@@ -27,6 +27,20 @@ t1 = time.perf_counter()
 torch.cuda.synchronize()
 t2 = time.perf_counter()
 print(f"enqueue {1e6 * (t1 - t0) / n:.1f} us/op, with drain {1e6 * (t2 - t0) / n:.1f} us/op")
+c2 = configs.config2()
+S2 = tt.Session(8192, 8)
+M = tt.pack(c2.tensors["M"], tt.parse_shape(c2.shapes["M"]), S2)
+V = tt.pack(c2.tensors["V"], tt.parse_shape(c2.shapes["V"]), S2)
+for _ in range(20):
+    tt.matvec_a(M, V)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(500):
+    tt.matvec_a(M, V)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+t2 = time.perf_counter()
+print(f"c2 matvec_a enqueue {1e6 * (t1 - t0) / 500:.1f} us/op, with drain {1e6 * (t2 - t0) / 500:.1f} us/op")
 lib = tt.tiletensor.lib()
 import ctypes  # noqa: E402
 t0 = time.perf_counter()
