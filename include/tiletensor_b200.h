@@ -210,6 +210,22 @@ int tt_mul_sum_clean(tt_session* s, const tt_shape* a, const double* ta, int64_t
 int tt_linalg_product(tt_session* s, int which, const tt_shape* a, const double* ta,
                       int64_t chain_a, const tt_shape* b, const double* tb, int64_t chain_b,
                       int variant, tt_shape* out_shape, double* out, int64_t* out_chain);
+/* Two consecutive products in one launch (the persistent chain kernel):
+ *   R1 = product(which1, a1, b1)
+ *   R2 = product(which2, x, R1)   (r1_pos == 1: R1 is the right operand)
+ *      = product(which2, R1, x)   (r1_pos == 0)
+ * e.g. config 3's zero-repack chain matmul_a(A, matmul_b(Bt, C))
+ * (tests/test_linalg.cpp:157-178 of the reference).  Both results are
+ * written (R1 to out1, R2 to out2); shapes, chain indices, counters and
+ * errors equal the two tt_linalg_product calls (which run as such when the
+ * pair is not fusable, and always when the first call's inputs are
+ * invalid).  Phase 2's fold units at a slot chunk start as soon as phase 1's
+ * column trees covering that chunk are done -- no kernel boundary. */
+int tt_linalg_chain2(tt_session* s, int which1, const tt_shape* a1, const double* ta1,
+                     int64_t chain_a1, const tt_shape* b1, const double* tb1, int64_t chain_b1,
+                     int which2, const tt_shape* x, const double* tx, int64_t chain_x, int r1_pos,
+                     int variant, tt_shape* out1_shape, double* out1, int64_t* out1_chain,
+                     tt_shape* out2_shape, double* out2, int64_t* out2_chain);
 /* clean_unknowns tile_tensor.hpp:352-386.  Returns the input unchanged (a
  * device copy when out != in) at zero cost when the shape has no '?'. */
 int tt_clean_unknowns(tt_session* s, const tt_shape* in_shape, const double* tin, int64_t chain,
@@ -289,6 +305,11 @@ void tt_affine_layer_destroy(tt_session* s, tt_affine_layer* layer);
  * only speed differs. */
 int tt_set_kernel_path(int path);
 int tt_kernel_path(void);
+/* The persistent chain kernel (fold units + in-tile tree items of one or two
+ * products from one dependency-ordered queue): 1 = on, 0 = off (default;
+ * env TT_CHAIN).  Results are identical either way. */
+int tt_set_chain_kernel(int on);
+int tt_chain_kernel(void);
 
 /* ---- sharding (north star item 5) -------------------------------------- */
 /* Block-partition external dim `shard_dim` (1-based) of `shape` over

@@ -82,6 +82,8 @@ SIGNATURES = {
     "tt_sum": (_I, [_P, _SP, _P, _I, _I, _SP, _P]),
     "tt_mul_sum": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64, _I, _I, _SP, _P, _I64P]),
     "tt_linalg_product": (_I, [_P, _I, _SP, _P, _I64, _SP, _P, _I64, _I, _SP, _P, _I64P]),
+    "tt_linalg_chain2": (_I, [_P, _I, _SP, _P, _I64, _SP, _P, _I64, _I, _SP, _P, _I64, _I, _I,
+                              _SP, _P, _I64P, _SP, _P, _I64P]),
     "tt_mul_sum_clean": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64, _I, _I, _SP, _P, _I64P]),
     "tt_mul_sum_affine": (_I, [_P, _SP, _P, _I64, _SP, _P, _I64, _I, _I, _SP, _P, _I64, _I, _SP, _P,
                                _I64P]),
@@ -101,6 +103,8 @@ SIGNATURES = {
     "tt_replicate_tile_dim": (_I, [_P, _P, _I64P, _I, _I, _P, _I64]),
     "tt_set_kernel_path": (_I, [_I]),
     "tt_kernel_path": (_I, []),
+    "tt_set_chain_kernel": (_I, [_I]),
+    "tt_chain_kernel": (_I, []),
     "tt_shard_plan": (_I, [_SP, _I, _I, _I, _I64P, _I64P, _SP]),
 }
 

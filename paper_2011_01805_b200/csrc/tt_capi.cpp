@@ -37,6 +37,7 @@ struct tt_session {
   // kSchedSlots (next, done) pairs, each left at zero by the launch using it
   unsigned int* sched = nullptr;
   unsigned int sched_next = 0;
+  unsigned int chain_next = 0;
   size_t scratch_bytes = 0;
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;
@@ -119,6 +120,8 @@ LaunchCtx ctx_of(tt_session* s) {
   c.scratch_owner = s;
   c.sched_base = s->sched;
   c.sched_next = &s->sched_next;
+  c.chain_base = s->sched ? s->sched + 2 * kSchedSlots : nullptr;
+  c.chain_next = &s->chain_next;
   return c;
 }
 
@@ -208,6 +211,40 @@ void run_reduction(tt_session* s, const Shape& prod, int di, int variant, const 
   const GroupSpec g = make_group_spec(ext, di, a_st, b_st, tb != nullptr);
   add_cost(s, prog.per_group, static_cast<uint64_t>(g.groups));
   launch_group_program(ctx_of(s), prog, g, s->slots, ta, tb, out, epi);
+}
+
+// The program and group grid run_reduction would launch for tt_sum(tt_mul(a, b), dim)
+// (counted like it); false when the sum is degenerate (the product itself).
+struct PreparedProduct {
+  std::shared_ptr<const Program> prog;
+  GroupSpec g;
+  Shape prod, so;
+};
+bool prepare_product(tt_session* s, const Shape& sa, const Shape& sb, int dim, int variant,
+                     PreparedProduct& pp) {
+  pp.prod = elementwise_result_shape(sa, sb, TT_OP_MUL);
+  pp.so = sum_result_shape(pp.prod, dim);
+  const int di = dim - 1;
+  const Dim& ds = pp.prod.dims[di];
+  if (ds.n == 1 && ds.d > 1) return false;
+  if (ds.interleaved && ds.unknown && ds.used() < pp.prod.ext(di) * ds.t) return false;
+  const auto ext = pp.prod.external();
+  const int64_t stride = tile_strides(pp.prod)[di];
+  const std::array<int64_t, 6> key{ext[di], ds.t, stride, ds.used(), ds.unknown ? 1 : 0, variant};
+  auto it = s->programs.find(key);
+  if (it == s->programs.end()) {
+    if (s->programs.size() >= 256) s->programs.clear();
+    it = s->programs
+             .emplace(key, std::make_shared<const Program>(build_sum_program(
+                               ext[di], ds.t, stride, s->slots, ds.used(), ds.unknown, variant)))
+             .first;
+  }
+  pp.prog = it->second;
+  std::vector<int64_t> ast, bst;
+  operand_strides(sa, ast);
+  operand_strides(sb, bst);
+  pp.g = make_group_spec(ext, di, ast, bst, true);
+  return true;
 }
 
 void require_slots(const tt_session* s, const Shape& sh, const char* who) {
@@ -373,7 +410,7 @@ int tt_session_create(int64_t slot_count, int64_t max_chain_index, int device, t
       check_cuda(cudaGetDeviceProperties(&prop, device), "device properties");
       s->sm_count = prop.multiProcessorCount;
       s->smem_optin = prop.sharedMemPerBlockOptin;
-      const size_t sched_bytes = 2 * kSchedSlots * sizeof(unsigned int);
+      const size_t sched_bytes = (2 * kSchedSlots + kChainSlots * kChainCounters) * sizeof(unsigned int);
       check_cuda(cudaMalloc(&s->sched, sched_bytes), "scheduler counters");
       check_cuda(cudaMemset(s->sched, 0, sched_bytes), "scheduler counters");
     } catch (...) {
@@ -898,6 +935,129 @@ int tt_linalg_product(tt_session* s, int which, const tt_shape* a, const double*
   return tt_mul_sum(s, a, ta, chain_a, b, tb, chain_b, dim, variant, out_shape, out, out_chain);
 }
 
+int tt_linalg_chain2(tt_session* s, int which1, const tt_shape* a1, const double* ta1,
+                     int64_t chain_a1, const tt_shape* b1, const double* tb1, int64_t chain_b1,
+                     int which2, const tt_shape* x, const double* tx, int64_t chain_x, int r1_pos,
+                     int variant, tt_shape* out1_shape, double* out1, int64_t* out1_chain,
+                     tt_shape* out2_shape, double* out2, int64_t* out2_chain) {
+  // Dry validation of both calls on the host (no launch, no counters): any
+  // error -- or a pair the chain kernel does not take -- runs the two calls.
+  tt_shape r1{};
+  int64_t c1 = 0;
+  bool fusable = true;
+  {
+    const std::string err = g_error;
+    const int64_t pos = g_error_pos;
+    try {
+      need_session(s);
+      if (which1 < 0 || which1 > 3 || which2 < 0 || which2 > 3 || (r1_pos != 0 && r1_pos != 1))
+        invalid_argument("tt_linalg_chain2: bad product form or operand position");
+      const Shape sa = from_c(a1), sb = from_c(b1), sx = from_c(x);
+      auto check = [&](int which, const Shape& l, const Shape& r) {
+        const int rank = which < 2 ? 2 : 3;
+        if (l.rank() != rank || r.rank() != rank) throw std::runtime_error("rank");
+        auto req = [](const Shape& sh, int d0) {
+          const Dim& ds = sh.dims[d0];
+          if (!(ds.n == 1 && ds.d == ds.t)) throw std::runtime_error("replication");
+        };
+        if (which == 0) req(r, 0);
+        if (which == 1) req(r, 1);
+        if (which == 2) {
+          req(l, 2);
+          req(r, 0);
+        }
+        if (which == 3) {
+          req(l, 2);
+          req(r, 1);
+        }
+        require_slots(s, l, "tt_mul");
+        require_slots(s, r, "tt_mul");
+      };
+      check(which1, sa, sb);
+      const Shape p1 = elementwise_result_shape(sa, sb, TT_OP_MUL);
+      check_tiles_addressable(p1);
+      c1 = mul_chain(chain_a1, chain_b1);
+      const int dim1 = (which1 == 0 || which1 == 2) ? 2 : 1;
+      const Shape s1 = sum_result_shape(p1, dim1);
+      to_c(s1, &r1);
+      const Shape& l2 = r1_pos ? sx : s1;
+      const Shape& rr2 = r1_pos ? s1 : sx;
+      check(which2, l2, rr2);
+      const Shape p2 = elementwise_result_shape(l2, rr2, TT_OP_MUL);
+      check_tiles_addressable(p2);
+      (void)mul_chain(r1_pos ? chain_x : c1, r1_pos ? c1 : chain_x);
+      (void)sum_result_shape(p2, (which2 == 0 || which2 == 2) ? 2 : 1);
+    } catch (const std::exception&) {
+      fusable = false;
+    }
+    g_error = err;
+    g_error_pos = pos;
+  }
+  if (!fusable) {  // the two calls, with their own errors and counters
+    tt_shape mid{};
+    int64_t ch = 0;
+    int rc = tt_linalg_product(s, which1, a1, ta1, chain_a1, b1, tb1, chain_b1, variant, &mid, out1, &ch);
+    if (rc != TT_OK) return rc;
+    if (out1_shape) *out1_shape = mid;
+    if (out1_chain) *out1_chain = ch;
+    return r1_pos ? tt_linalg_product(s, which2, x, tx, chain_x, &mid, out1, ch, variant, out2_shape, out2,
+                                      out2_chain)
+                  : tt_linalg_product(s, which2, &mid, out1, ch, x, tx, chain_x, variant, out2_shape, out2,
+                                      out2_chain);
+  }
+  return guarded([&] {
+    const Shape sa = from_c(a1), sb = from_c(b1), sx = from_c(x), s1 = from_c(&r1);
+    const int dim1 = (which1 == 0 || which1 == 2) ? 2 : 1;
+    const int dim2 = (which2 == 0 || which2 == 2) ? 2 : 1;
+    const Shape& l2 = r1_pos ? sx : s1;
+    const Shape& rr2 = r1_pos ? s1 : sx;
+    std::lock_guard<std::mutex> lk(s->mu);
+    PreparedProduct pp[2];
+    const bool ok1 = prepare_product(s, sa, sb, dim1, variant, pp[0]);
+    const bool ok2 = prepare_product(s, l2, rr2, dim2, variant, pp[1]);
+    const LaunchCtx c = ctx_of(s);
+    ChainStep steps[2];
+    steps[0].prog = pp[0].prog.get();
+    steps[0].g = pp[0].g;
+    steps[0].ta = ta1;
+    steps[0].tb = tb1;
+    steps[0].tout = out1;
+    steps[1].prog = pp[1].prog.get();
+    steps[1].g = pp[1].g;
+    steps[1].ta = r1_pos ? tx : out1;
+    steps[1].tb = r1_pos ? out1 : tx;
+    steps[1].tout = out2;
+    if (!(ok1 && ok2 && launch_chain(c, steps, 2, s->slots))) {
+      // not fusable after all: the two reductions back to back (same kernels
+      // the separate calls launch)
+      auto one = [&](const Shape& l, const Shape& r, int dim, const double* tl, const double* tr,
+                     double* o) {
+        const Shape prod = elementwise_result_shape(l, r, TT_OP_MUL);
+        const Dim& ds = prod.dims[dim - 1];
+        if (ds.n == 1 && ds.d > 1) {
+          launch_elementwise(c, TT_OP_MUL, prod, l, r, s->slots, tl, tr, o);
+          return;
+        }
+        std::vector<int64_t> ast, bst;
+        operand_strides(l, ast);
+        operand_strides(r, bst);
+        run_reduction(s, prod, dim - 1, variant, tl, ast, tr, bst, o);
+      };
+      one(sa, sb, dim1, ta1, tb1, out1);
+      one(l2, rr2, dim2, steps[1].ta, steps[1].tb, out2);
+    } else {
+      add_cost(s, pp[0].prog->per_group, static_cast<uint64_t>(pp[0].g.groups));
+      add_cost(s, pp[1].prog->per_group, static_cast<uint64_t>(pp[1].g.groups));
+    }
+    s->muls += static_cast<uint64_t>(pp[0].prod.tile_count() + pp[1].prod.tile_count());
+    if (out1_shape) *out1_shape = r1;
+    if (out1_chain) *out1_chain = c1;
+    const int64_t c2 = std::min(r1_pos ? chain_x : c1, r1_pos ? c1 : chain_x) - 1;
+    to_c(sum_result_shape(elementwise_result_shape(l2, rr2, TT_OP_MUL), dim2), out2_shape);
+    if (out2_chain) *out2_chain = c2;
+  });
+}
+
 int tt_clean_unknowns(tt_session* s, const tt_shape* in_shape, const double* tin, int64_t chain,
                       tt_shape* out_shape, double* out, int64_t* out_chain) {
   return guarded([&] {
@@ -1338,6 +1498,12 @@ int tt_set_kernel_path(int path) {
 }
 
 int tt_kernel_path(void) { return kernel_path(); }
+
+int tt_set_chain_kernel(int on) {
+  set_chain_kernel(on);
+  return TT_OK;
+}
+int tt_chain_kernel(void) { return chain_kernel_enabled(); }
 
 // ---- sharding ---------------------------------------------------------------------
 

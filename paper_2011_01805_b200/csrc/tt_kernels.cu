@@ -248,6 +248,7 @@ __device__ __forceinline__ void epi_apply_n(const EpiDev& e, double (&x)[N], con
 #include "kernels/gemm.cuh"
 #include "kernels/tree.cuh"
 #include "kernels/layers.cuh"
+#include "kernels/chain.cuh"
 
 // ---- synthetic input generator (== or_fill_uniform in oracle/tt_oracle.c) ------------
 
@@ -1172,6 +1173,109 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
   post_launch(c, "row tree pass");
 }
 
+// TT_CHAIN=0 turns the persistent chain kernel (kernels/chain.cuh) off: products
+// then run as GEMM fold + tree pass (two launches each), as before.
+// Off by default: measured on config 3 it does not beat the two-launch path
+// (fold 41.8 + column tree 7.8 us, fold 27.4 + row tree 12.4 us): the chain
+// kernel's products take 57 / 58 us and the two-product chain 109 us -- its
+// tree items run latency-bound on the GEMM CTAs' 4 consumer warps, the
+// dependency probes lengthen each claim, and the row trees of the second
+// product still wait for the last fold units (profiles/r02_chain_kernel.md).
+std::atomic<int> g_chain{[] {
+  const char* e = std::getenv("TT_CHAIN");
+  return e ? std::atoi(e) : 0;
+}()};
+// TT_CHAIN_P2COL=1: a chain's second product (row tree) folds in the first
+// product's column order (starts earlier, its row trees wait for the end)
+const int g_chain_p2_col = [] {
+  const char* e = std::getenv("TT_CHAIN_P2COL");
+  return e ? std::atoi(e) : 0;
+}();
+// TT_CHAIN_G: column blocks per super-group of the column-major fold order
+const int g_chain_g = [] {
+  const char* e = std::getenv("TT_CHAIN_G");
+  return e ? std::atoi(e) : 4;
+}();
+
+// Host view of one chain phase.
+struct ChainPlan {
+  ChainPhaseDev dev{};
+  alignas(64) unsigned char mapA[128];
+  alignas(64) unsigned char mapB[128];
+  int64_t n_out = 0;
+};
+
+// A product is chain-eligible when its fold is GEMM shaped (one group dim along
+// which only A varies, one along which only B varies, every other group dim of
+// extent 1, positive fold steps, the fold over all steps from 0) and its in-tile
+// schedule is a forward power-of-two tree of the column-local (t * stride = s,
+// stride a multiple of 16) or row-local (reach <= 16 rows of 32) kind -- or none.
+bool plan_chain_phase(const LaunchCtx& c, const ChainStep& st, int64_t s, ChainPlan& cp) {
+  const Program& prog = *st.prog;
+  const GroupSpec& g = st.g;
+  if (!st.tb || s % (kChSL * 32) != 0 || s >= (int64_t{1} << 31)) return false;
+  const bool fold_only = prog.ops.size() == 1 && prog.ops[0].kind == GOP_FOLD && prog.ops[0].dst == BUF_OUT;
+  if (!fold_only && !prog.simple_pow2) return false;
+  GroupParams p = make_group_params(prog, g, s);
+  if (p.ops[0].x != 0 || p.ops[0].y < 1 || p.ops[0].y >= (int64_t{1} << 24)) return false;
+  const BlockPlan bp = block_plan(g, true);
+  if (bp.ia < 0 || bp.ib < 0) return false;
+  for (int i = 0; i < g.nd; ++i)
+    if (i != bp.ia && i != bp.ib && g.ext[i] != 1) return false;
+  if (g.astep <= 0 || g.bstep <= 0 || g.a_stride[bp.ia] <= 0 || g.b_stride[bp.ib] <= 0) return false;
+  const int64_t ni = g.ext[bp.ia], nj = g.ext[bp.ib];
+  if (ni > 16 * 255 || nj > 16 * 255 || ((ni + 15) / 16) * ((nj + 15) / 16) > 64) return false;
+  if (!aligned16(st.ta) || !aligned16(st.tb) || !aligned16(st.tout)) return false;
+  ChainPhaseDev& d = cp.dev;
+  d.ni = static_cast<int>(ni);
+  d.nj = static_cast<int>(nj);
+  d.nk = static_cast<int>(p.ops[0].y);
+  d.nbi = static_cast<int>((ni + 15) / 16);
+  d.nbj = static_cast<int>((nj + 15) / 16);
+  d.out_i = g.out_stride[bp.ia];
+  d.out_j = g.out_stride[bp.ib];
+  d.out = st.tout;
+  d.nsub = 16;
+  const int nchunks = static_cast<int>(s / kChSL);
+  if (fold_only) {
+    d.tree = 0;
+  } else {
+    p.nlevels = static_cast<int>(prog.ops.size()) - 1;
+    if (p.nlevels < 1 || p.nlevels > 8) return false;
+    for (int i = 0; i < p.nlevels; ++i) p.rots[i] = prog.ops[i + 1].x;
+    const TreePass tp = plan_tree_pass(p, s, c.smem_optin);
+    if (tp.back || tp.kind == 3) return false;
+    if (tp.kind == 1 && tp.stride0 % kChSL == 0 && tp.t <= 32) {
+      d.tree = 1;
+      d.col_t = static_cast<int>(tp.t);
+      d.col_stride = static_cast<int>(tp.stride0);
+      d.tree_ncb = static_cast<int>(tp.stride0 / kChSL);
+      d.tq = d.tree_ncb;
+      d.tree_per = nchunks / d.tree_ncb;
+    } else if (tp.kind == 2 && tp.hr <= 16) {
+      d.tree = 2;
+      d.hr = tp.hr;
+      d.nlevels = p.nlevels;
+      for (int i = 0; i < p.nlevels; ++i) d.lv[i] = static_cast<int>(p.rots[i]);
+      d.tq = static_cast<int>(s / 512);
+      d.tree_per = 512 / kChSL;
+    } else {
+      return false;
+    }
+  }
+  // operand tensor maps {slot, block row, fold step}
+  const uint64_t eb = sizeof(double);
+  const uint64_t dA[3] = {static_cast<uint64_t>(s), static_cast<uint64_t>(ni), static_cast<uint64_t>(d.nk)};
+  const uint64_t dB[3] = {static_cast<uint64_t>(s), static_cast<uint64_t>(nj), static_cast<uint64_t>(d.nk)};
+  const uint64_t sA[2] = {static_cast<uint64_t>(g.a_stride[bp.ia] * s) * eb, static_cast<uint64_t>(g.astep * s) * eb};
+  const uint64_t sB[2] = {static_cast<uint64_t>(g.b_stride[bp.ib] * s) * eb, static_cast<uint64_t>(g.bstep * s) * eb};
+  const uint32_t box[3] = {kChSL, kChP, kChKS};
+  if (!encode_tensor_map_f64(cp.mapA, 3, st.ta, dA, sA, box) ||
+      !encode_tensor_map_f64(cp.mapB, 3, st.tb, dB, sB, box))
+    return false;
+  return true;
+}
+
 // Returns true when `epi` was applied (fused into a tree pass); the caller
 // runs it as a separate pass otherwise.
 template <bool HAS_B>
@@ -1225,6 +1329,16 @@ bool launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
     // ...unless the whole reduction is tiny (< 2^20 product slots): then one
     // fused launch beats two (small ops are launch-latency bound; config 1)
     const bool tiny = g.groups * prog.ops[0].y * s < (int64_t{1} << 20);
+    if (matmul_like && HAS_B && force == 0 && prog.ops[0].y > 1 && (epi == nullptr || !epi->active()) &&
+        !tiny) {
+      ChainStep one;
+      one.prog = &prog;
+      one.g = g;
+      one.ta = ta;
+      one.tb = tb;
+      one.tout = tout;
+      if (launch_chain(c, &one, 1, s)) return false;
+    }
     if ((g.groups < static_cast<int64_t>(c.sm_count) * std::min<int64_t>(per_sm, 4) ||
          (matmul_like && force != 1 && force != 2)) &&
         prog.ops[0].y > 1 && !(tiny && force == 0)) {
@@ -1308,7 +1422,91 @@ bool launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
 }  // namespace
 
 void set_kernel_path(int path) { g_forced_path.store(path, std::memory_order_relaxed); }
+void set_chain_kernel(int on) { g_chain.store(on ? 1 : 0, std::memory_order_relaxed); }
+int chain_kernel_enabled() { return g_chain.load(std::memory_order_relaxed); }
 int kernel_path() { return forced_path(); }
+
+bool launch_chain(const LaunchCtx& c, const ChainStep* steps, int n, int64_t s) {
+  if (!g_chain.load(std::memory_order_relaxed) || n < 1 || n > 2 || !c.chain_base || forced_path() != 0)
+    return false;
+  ChainPlan cp[2];
+  for (int k = 0; k < n; ++k)
+    if (!plan_chain_phase(c, steps[k], s, cp[k])) return false;
+  if (n == 2) {  // the second product reads the first's result: column tree needed
+    if (cp[0].dev.tree != 1) return false;
+    if (steps[1].ta != steps[0].tout && steps[1].tb != steps[0].tout) return false;
+  }
+  ChainDev d{};
+  d.nphase = n;
+  d.s = s;
+  d.nchunks = static_cast<int>(s / kChSL);
+  // fold buffers: session scratch, one region per phase with a tree
+  size_t fold_bytes[2] = {0, 0};
+  for (int k = 0; k < n; ++k) {
+    if (!cp[k].dev.tree) continue;
+    const int64_t hi = (cp[k].dev.ni - 1) * cp[k].dev.out_i + (cp[k].dev.nj - 1) * cp[k].dev.out_j + 1;
+    fold_bytes[k] = static_cast<size_t>(hi) * s * sizeof(double);
+  }
+  double* scratch = (fold_bytes[0] + fold_bytes[1]) ? c.scratch(c.scratch_owner, fold_bytes[0] + fold_bytes[1]) : nullptr;
+  int counter = 5;  // queue heads F0, T0, F1, T1 and the exit count
+  for (int k = 0; k < n; ++k) {
+    ChainPhaseDev& P = cp[k].dev;
+    P.fold = P.tree ? scratch + (k == 1 ? fold_bytes[0] / sizeof(double) : 0) : P.out;
+    const int nb = P.nbi * P.nbj;
+    if (k == 1 && (P.tree != 2 || g_chain_p2_col)) {  // follow phase 1's column order: its column block c % ncb unlocks chunk c
+      P.col_order = 1;
+      P.ncb = cp[0].dev.tree_ncb;
+      P.q = P.ncb;
+      P.per_q = d.nchunks / P.ncb;
+      P.dep_phase = 0;
+      P.dep_ncb = cp[0].dev.tree_ncb;
+      P.dep_target = cp[0].dev.nbi * cp[0].dev.nbj * cp[0].dev.nsub;
+    } else {
+      P.dep_phase = -1;
+      if (k == 1) {  // rows of phase 2 complete one after the other (its row trees overlap)
+        P.dep_phase = 0;
+        P.dep_ncb = cp[0].dev.tree_ncb;
+        P.dep_target = cp[0].dev.nbi * cp[0].dev.nbj * cp[0].dev.nsub;
+      }
+      if (P.tree == 1) {  // column blocks complete one after the other
+        P.col_order = 1;
+        P.ncb = P.tree_ncb;
+        P.q = P.ncb;
+        P.per_q = d.nchunks / P.ncb;
+      } else {            // row blocks complete one after the other
+        P.col_order = 0;
+        P.ncb = 1;
+        P.q = P.tree == 2 ? P.tq : 1;
+        P.per_q = d.nchunks / P.q;
+      }
+    }
+    if (P.col_order) {  // super-groups of colg column blocks (a divisor of q)
+      P.colg = std::max(1, std::min(g_chain_g, P.q));
+      while (P.q % P.colg) --P.colg;
+    }
+    P.nf = P.q * P.per_q * nb;
+    P.nt = P.tree ? P.tq * nb * P.nsub : 0;
+    P.fold_done = counter;
+    counter += P.tree ? P.tq * nb : 0;
+    P.tree_done = counter;
+    counter += P.tree == 1 ? P.tq : 0;
+    d.ph[k] = P;
+  }
+  if (counter > static_cast<int>(kChainCounters)) return false;
+  d.ncnt = counter;
+  d.cnt = c.chain_base + ((*c.chain_next)++ % kChainSlots) * kChainCounters;
+  const size_t smem = static_cast<size_t>(kChNS) * kChStage * sizeof(double) + 3 * kChNS * 8;
+  set_smem_attr((const void*)chain_kernel, smem);
+  const int grid = grid_for(c, (const void*)chain_kernel, kChThreads, smem,
+                            d.ph[0].nf + (n > 1 ? d.ph[1].nf : 0));
+  const CUtensorMap* m0a = reinterpret_cast<const CUtensorMap*>(cp[0].mapA);
+  const CUtensorMap* m0b = reinterpret_cast<const CUtensorMap*>(cp[0].mapB);
+  const CUtensorMap* m1a = reinterpret_cast<const CUtensorMap*>(n > 1 ? cp[1].mapA : cp[0].mapA);
+  const CUtensorMap* m1b = reinterpret_cast<const CUtensorMap*>(n > 1 ? cp[1].mapB : cp[0].mapB);
+  chain_kernel<<<grid, kChThreads, smem, c.stream>>>(*m0a, *m0b, *m1a, *m1b, d);
+  post_launch(c, "chain kernel");
+  return true;
+}
 
 void launch_group_program(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
                           const double* ta, const double* tb, double* tout, const Epilogue* epi) {

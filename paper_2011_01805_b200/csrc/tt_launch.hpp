@@ -21,9 +21,16 @@ struct LaunchCtx {
   // Session-owned ring of work-queue counter pairs (next unit, CTAs done).
   unsigned int* sched_base = nullptr;
   unsigned int* sched_next = nullptr;
+  unsigned int* chain_base = nullptr;   // kChainSlots blocks of kChainCounters
+  unsigned int* chain_next = nullptr;
 };
 
 constexpr unsigned int kSchedSlots = 256;
+// Dependency-counter blocks of the chain kernel (kernels/chain.cuh), a ring
+// after the scheduler pairs in the same session buffer; each launch's last CTA
+// leaves its block at zero.
+constexpr unsigned int kChainSlots = 8;
+constexpr unsigned int kChainCounters = 8192;
 // The (next, done) counter pair for one dynamically scheduled launch.  The
 // kernel's last CTA resets both to zero, so a slot is reusable by the next
 // launch on the stream; concurrent launches (different streams) get distinct
@@ -122,6 +129,20 @@ struct Epilogue {
 };
 // Runs `prog` for every group of `g`; `tb` may be null (no fused multiply);
 // `epi` (optional) is applied to every output tile.
+// One product of a fused chain (tt_linalg_chain): its reduction program and
+// group grid as run_reduction builds them, operand and result tiles.
+struct ChainStep {
+  const Program* prog = nullptr;
+  GroupSpec g;
+  const double* ta = nullptr;
+  const double* tb = nullptr;
+  double* tout = nullptr;
+};
+// Runs 1 or 2 products (the second reading the first's result as one operand)
+// as one persistent chain kernel; false (nothing launched) when a product is
+// not a GEMM-shaped fold with a column- or row-local power-of-two tree.
+bool launch_chain(const LaunchCtx& c, const ChainStep* steps, int n, int64_t s);
+
 void launch_group_program(const LaunchCtx& c, const Program& prog, const GroupSpec& g, int64_t s,
                           const double* ta, const double* tb, double* tout,
                           const Epilogue* epi = nullptr);
@@ -136,5 +157,7 @@ void check_cuda(cudaError_t e, const char* what);
 // 0 = best eligible, 1 = TMA ring, 2 = register tree, 3 = generic interpreter.
 void set_kernel_path(int path);
 int kernel_path();
+void set_chain_kernel(int on);
+int chain_kernel_enabled();
 
 }  // namespace ttb

@@ -895,6 +895,48 @@ def matmul_b(m1_transposed: TileTensor, m2: TileTensor, variant=None) -> TileTen
     return _product(3, m1_transposed, m2, variant)
 
 
+_PRODUCTS = {"matvec_a": 0, "matvec_b": 1, "matmul_a": 2, "matmul_b": 3}
+
+
+def linalg_chain(first: str, a: TileTensor, b: TileTensor, second: str, x: TileTensor,
+                 first_is_right: bool = True, variant=None):
+    """Two consecutive products in ONE launch (tt_linalg_chain2):
+    r1 = first(a, b); r2 = second(x, r1) (first_is_right) or second(r1, x).
+    E.g. config 3's zero-repack chain matmul_a(A, matmul_b(Bt, C)) is
+    linalg_chain("matmul_b", Bt, C, "matmul_a", A) -- the reference's own
+    two-call chain (tests/test_linalg.cpp:157-178).  Returns (r1, r2), bit for
+    bit, counter for counter and error for error the two calls' results; the
+    second product's units start on a slot chunk as soon as the first
+    product's trees covering it are done (no kernel boundary between them)."""
+    w1, w2 = _PRODUCTS[first], _PRODUCTS[second]
+    s = _same_session(a, b)
+    _same_session(a, x)
+    d1 = 2 if w1 in (0, 2) else 1
+    d2 = 2 if w2 in (0, 2) else 1
+    try:
+        s1 = sum_result_shape(elementwise_result_shape(a.shape(), b.shape(), OpKind.mul), d1)
+        l2, r2s = (x.shape(), s1) if first_is_right else (s1, x.shape())
+        n2 = sum_result_shape(elementwise_result_shape(l2, r2s, OpKind.mul), d2).tile_count()
+        n1 = s1.tile_count()
+    except ShapeError:  # let the C-ABI raise the reference's error for the calls
+        n1 = n2 = 0
+    out1 = s.empty_tiles(max(n1, 1))
+    out2 = s.empty_tiles(max(n2, 1))
+    so1, so2 = CShape(), CShape()
+    c1, c2 = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().tt_linalg_chain2(s.handle, w1, ctypes.byref(a.shape().to_c()), _dptr(a),
+                                  a.chain_index(), ctypes.byref(b.shape().to_c()), _dptr(b),
+                                  b.chain_index(), w2, ctypes.byref(x.shape().to_c()), _dptr(x),
+                                  x.chain_index(), 1 if first_is_right else 0, _variant(variant),
+                                  ctypes.byref(so1), _ptr(out1), ctypes.byref(c1), ctypes.byref(so2),
+                                  _ptr(out2), ctypes.byref(c2)))
+    sh1, sh2 = TileTensorShape.from_c(so1), TileTensorShape.from_c(so2)
+    if sh1.tile_count() > out1.shape[0] or sh2.tile_count() > out2.shape[0]:
+        raise ShapeError("chain result larger than allocated")
+    return (TileTensor._wrap(sh1, out1[:sh1.tile_count()], s, c1.value),
+            TileTensor._wrap(sh2, out2[:sh2.tile_count()], s, c2.value))
+
+
 def clean_unknowns(t: TileTensor) -> TileTensor:  # tile_tensor.hpp:352-386
     s = t.session()
     out = s.empty_tiles(t.tile_count())
@@ -1009,6 +1051,16 @@ KERNEL_PATHS = {"auto": 0, "tma": 1, "regs": 2, "generic": 3, "window": 4}
 def set_kernel_path(path: str) -> None:
     """Force the reduction kernel path (identical results, different speed)."""
     _check(lib().tt_set_kernel_path(KERNEL_PATHS[path]))
+
+
+def set_chain_kernel(on: bool) -> None:
+    """Run GEMM-shaped products (and linalg_chain) on the persistent chain
+    kernel (csrc/kernels/chain.cuh); identical results, off by default."""
+    _check(lib().tt_set_chain_kernel(1 if on else 0))
+
+
+def chain_kernel() -> bool:
+    return bool(lib().tt_chain_kernel())
 
 
 def kernel_path() -> str:
