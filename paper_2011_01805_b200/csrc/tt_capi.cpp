@@ -59,10 +59,12 @@ struct tt_session {
   struct CachedBlock {
     size_t bytes;
     cudaStream_t stream;
+    bool cacheable;
   };
   std::unordered_map<void*, CachedBlock> live;
   std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free_blocks;
   size_t cached_bytes = 0;
+  size_t cache_cap = size_t{8} << 30;  // a quarter of the device memory (set at creation)
 };
 
 namespace {
@@ -406,6 +408,8 @@ int tt_session_create(int64_t slot_count, int64_t max_chain_index, int device, t
       check_cuda(cudaMemPoolCreate(&s->pool, &props), "memory pool");
       uint64_t keep = ~uint64_t{0};
       check_cuda(cudaMemPoolSetAttribute(s->pool, cudaMemPoolAttrReleaseThreshold, &keep), "pool threshold");
+      size_t free_mem = 0, total_mem = 0;
+      if (cudaMemGetInfo(&free_mem, &total_mem) == cudaSuccess) s->cache_cap = total_mem / 4;
       cudaDeviceProp prop{};
       check_cuda(cudaGetDeviceProperties(&prop, device), "device properties");
       s->sm_count = prop.multiProcessorCount;
@@ -496,15 +500,62 @@ void tt_session_count_bootstraps(tt_session* s, int64_t count) {
 
 // ---- memory -----------------------------------------------------------------------
 
+namespace {
+// Blocks handed out by tt_device_alloc / tt_tiles_alloc come from the session's
+// stream-ordered pool and, once released, from a free list keyed by (stream,
+// bytes): a repeated op of the same shape allocates with no driver call.  (The
+// pool alone is not enough: reusing a released 16 GiB block through
+// cudaMallocFromPoolAsync measured 27 ms per call on config 5 -- the pool
+// re-maps large blocks -- against 5.7 ms for the op itself.)  The cache keeps at
+// most a quarter of the device memory; beyond it blocks go back to the pool.
+void* cache_take(tt_session* s, size_t nb) {
+  auto it = s->free_blocks.find({s->stream, nb});
+  if (it == s->free_blocks.end() || it->second.empty()) return nullptr;
+  void* p = it->second.back();
+  it->second.pop_back();
+  s->cached_bytes -= nb;
+  return p;
+}
+
+void* block_alloc(tt_session* s, size_t nb, bool cacheable) {
+  void* p = cacheable ? cache_take(s, nb) : nullptr;
+  if (!p) {
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    check_cuda(cudaMallocFromPoolAsync(&p, nb, s->pool, s->stream), "cudaMallocFromPoolAsync");
+  }
+  s->live[p] = {nb, s->stream, cacheable};
+  return p;
+}
+
+void block_release(tt_session* s, void* p) {
+  auto it = s->live.find(p);
+  if (it == s->live.end()) invalid_argument("release of a block this session did not allocate");
+  const tt_session::CachedBlock b = it->second;
+  s->live.erase(it);
+  if (b.cacheable && s->cached_bytes + b.bytes <= s->cache_cap) {
+    s->free_blocks[{b.stream, b.bytes}].push_back(p);
+    s->cached_bytes += b.bytes;
+  } else {
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    check_cuda(cudaFreeAsync(p, s->stream), "cudaFreeAsync");
+  }
+}
+
+bool capturing(const tt_session* s) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  check_cuda(cudaStreamIsCapturing(s->stream, &cap), "capture status");
+  return cap != cudaStreamCaptureStatusNone;
+}
+}  // namespace
+
 int tt_device_alloc(tt_session* s, int64_t bytes, void** out) {
   return guarded([&] {
     need_session(s);
     *out = nullptr;
     if (bytes <= 0) return;
     std::lock_guard<std::mutex> lk(s->mu);
-    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
-    check_cuda(cudaMallocFromPoolAsync(out, static_cast<size_t>(bytes), s->pool, s->stream),
-               "cudaMallocFromPoolAsync");
+    // a block allocated under stream capture is graph memory: never cached
+    *out = block_alloc(s, static_cast<size_t>(bytes), !capturing(s));
   });
 }
 
@@ -513,37 +564,20 @@ int tt_device_free(tt_session* s, void* p) {
     need_session(s);
     if (!p) return;
     std::lock_guard<std::mutex> lk(s->mu);
-    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
-    check_cuda(cudaFreeAsync(p, s->stream), "cudaFreeAsync");
+    block_release(s, p);
   });
 }
-
-// Cap on the bytes tt_tiles_release keeps cached per session; beyond it a
-// released block goes back to the pool (cudaFreeAsync).
-constexpr size_t kTileCacheBytes = size_t{8} << 30;
 
 int tt_tiles_alloc(tt_session* s, int64_t bytes, void** out) {
   return guarded([&] {
     need_session(s);
     *out = nullptr;
     if (bytes <= 0) bytes = 8;
-    const size_t nb = static_cast<size_t>(bytes);
     std::lock_guard<std::mutex> lk(s->mu);
     // under stream capture the result must live in the capturing framework's
     // graph memory: hand out nothing, the caller allocates it itself
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    check_cuda(cudaStreamIsCapturing(s->stream, &cap), "capture status");
-    if (cap != cudaStreamCaptureStatusNone) return;
-    auto it = s->free_blocks.find({s->stream, nb});
-    if (it != s->free_blocks.end() && !it->second.empty()) {
-      *out = it->second.back();
-      it->second.pop_back();
-      s->cached_bytes -= nb;
-    } else {
-      check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
-      check_cuda(cudaMallocFromPoolAsync(out, nb, s->pool, s->stream), "cudaMallocFromPoolAsync");
-    }
-    s->live[*out] = {nb, s->stream};
+    if (capturing(s)) return;
+    *out = block_alloc(s, static_cast<size_t>(bytes), true);
   });
 }
 
@@ -552,17 +586,7 @@ int tt_tiles_release(tt_session* s, void* p) {
     need_session(s);
     if (!p) return;
     std::lock_guard<std::mutex> lk(s->mu);
-    auto it = s->live.find(p);
-    if (it == s->live.end()) invalid_argument("tt_tiles_release: not a tt_tiles_alloc block");
-    const tt_session::CachedBlock b = it->second;
-    s->live.erase(it);
-    if (s->cached_bytes + b.bytes <= kTileCacheBytes) {
-      s->free_blocks[{b.stream, b.bytes}].push_back(p);
-      s->cached_bytes += b.bytes;
-    } else {
-      check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
-      check_cuda(cudaFreeAsync(p, b.stream), "cudaFreeAsync");
-    }
+    block_release(s, p);
   });
 }
 

@@ -327,6 +327,11 @@ const int g_ew_chunk = [] {
   const char* e = std::getenv("TT_EW_CHUNK");
   return e ? std::atoi(e) : 1;
 }();
+// TT_EW_HINT=0: no L2 eviction hints in the broadcast elementwise kernel
+const int g_ew_hint = [] {
+  const char* e = std::getenv("TT_EW_HINT");
+  return e ? std::atoi(e) : 1;
+}();
 
 void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const double* in,
                   double* out) {
@@ -396,12 +401,23 @@ void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shap
     const uint64_t chunks = static_cast<uint64_t>((s + kEwChunk - 1) / kEwChunk);
     const FastDiv64 cd = make_div64(chunks);
     const int64_t items = p.n_tiles * static_cast<int64_t>(chunks);
+    for (int i = 0; i < p.rank; ++i) {
+      if (eo[i] > 1 && p.a_stride[i] == 0) q.keep_a = 1;
+      if (eo[i] > 1 && p.b_stride[i] == 0) q.keep_b = 1;
+    }
+    // the L2 hints pay when the broadcast operand's re-reads outgrow the L2
+    const bool hint = g_ew_hint && (q.keep_a || q.keep_b) &&
+                      p.n_tiles * s * 8 > (int64_t{64} << 20);
+    auto run = [&](auto k) {
+      const int grid = grid_for(c, (const void*)k, 256, 0, items);
+      k<<<grid, 256, 0, c.stream>>>(q, ta, tb, tout, cd);
+    };
     if (op == TT_OP_ADD) {
-      const int grid = grid_for(c, (const void*)elementwise_chunk_kernel<TT_OP_ADD>, 256, 0, items);
-      elementwise_chunk_kernel<TT_OP_ADD><<<grid, 256, 0, c.stream>>>(q, ta, tb, tout, cd);
+      if (hint) run(elementwise_chunk_kernel<TT_OP_ADD, true>);
+      else run(elementwise_chunk_kernel<TT_OP_ADD, false>);
     } else {
-      const int grid = grid_for(c, (const void*)elementwise_chunk_kernel<TT_OP_MUL>, 256, 0, items);
-      elementwise_chunk_kernel<TT_OP_MUL><<<grid, 256, 0, c.stream>>>(q, ta, tb, tout, cd);
+      if (hint) run(elementwise_chunk_kernel<TT_OP_MUL, true>);
+      else run(elementwise_chunk_kernel<TT_OP_MUL, false>);
     }
     post_launch(c, "elementwise chunk kernel");
     return;

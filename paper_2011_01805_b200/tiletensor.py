@@ -439,8 +439,8 @@ class _Block:
     def __del__(self):
         try:
             h = self.session._ptr
-            if h and h.value and _FASTMOD is not None:
-                _FASTMOD.release(h.value, self.ptr)
+            if h and h.value:
+                _fastmod().release(h.value, self.ptr)
         except Exception:
             pass
 
@@ -534,6 +534,43 @@ class TileTensor:
 def _dptr(t: TileTensor) -> ctypes.c_void_p:
     """Device address of a tile tensor's array (no torch view needed)."""
     return ctypes.c_void_p(t._p)
+
+
+class _Out:
+    """An operator's result storage: a block of the session's tile cache
+    (tt_tiles_alloc: the same block the next call of that shape reuses), or a
+    torch tensor while the stream is being captured into a CUDA graph.  A block
+    not handed to a TileTensor (the call raised) is released on collection."""
+    __slots__ = ("s", "n", "ptr", "t", "owned")
+
+    def __init__(self, s: Session, n: int):
+        self.s, self.n = s, max(int(n), 1)
+        p = ctypes.c_void_p()
+        _check(lib().tt_tiles_alloc(s.handle, self.n * s._slots * 8, ctypes.byref(p)))
+        if p.value:
+            self.ptr, self.t, self.owned = p.value, None, True
+        else:
+            self.t = s.empty_tiles(self.n)
+            self.ptr, self.owned = self.t.data_ptr(), False
+
+    def c(self) -> ctypes.c_void_p:
+        return ctypes.c_void_p(self.ptr)
+
+    def wrap(self, shape: TileTensorShape, chain: int) -> TileTensor:
+        n = shape.tile_count()
+        if n > self.n:  # host-side sizing and the C-ABI disagree: never hand out a short array
+            raise ShapeError(f"result has {n} tiles, {self.n} allocated")
+        if self.t is not None:
+            return TileTensor._wrap(shape, self.t if n == self.t.shape[0] else self.t[:n], self.s, chain)
+        self.owned = False
+        return TileTensor._wrap_block(shape, self.ptr, self.s, int(chain))
+
+    def __del__(self):
+        if getattr(self, "owned", False):
+            try:
+                _fastmod().release(self.s._ptr.value, self.ptr)
+            except Exception:
+                pass
 
 
 def with_leading_unit_dim(t: TileTensor) -> TileTensor:  # tile_tensor.hpp:158-165
@@ -702,11 +739,11 @@ def _tt_elementwise(a: TileTensor, b: TileTensor, op) -> TileTensor:
     chain = ctypes.c_int64()
     n_out = _result_tiles(("ew", int(op), a.shape(), b.shape()),
                           lambda: elementwise_result_shape(a.shape(), b.shape(), op).tile_count())
-    out = s.empty_tiles(n_out)
+    out = _Out(s, n_out)
     _check(lib().tt_elementwise(s.handle, int(op), ctypes.byref(a.shape().to_c()), _dptr(a),
                                 a.chain_index(), ctypes.byref(b.shape().to_c()), _dptr(b),
-                                b.chain_index(), ctypes.byref(so), _ptr(out), ctypes.byref(chain)))
-    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
+                                b.chain_index(), ctypes.byref(so), out.c(), ctypes.byref(chain)))
+    return out.wrap(TileTensorShape.from_c(so), chain.value)
 
 
 def tt_add(a: TileTensor, b: TileTensor) -> TileTensor:
@@ -741,11 +778,11 @@ def _tt_sum(t: TileTensor, dim: int, variant: Optional[SumVariant] = None) -> Ti
     s = t.session()
     n_out = _result_tiles(("sum", t.shape(), int(dim)),
                           lambda: sum_result_shape(t.shape(), dim).tile_count())
-    out = s.empty_tiles(n_out)
+    out = _Out(s, n_out)
     so = CShape()
     _check(lib().tt_sum(s.handle, ctypes.byref(t.shape().to_c()), _dptr(t), int(dim),
-                        _variant(variant), ctypes.byref(so), _ptr(out)))
-    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, t.chain_index())
+                        _variant(variant), ctypes.byref(so), out.c()))
+    return out.wrap(TileTensorShape.from_c(so), t.chain_index())
 
 
 def tt_mul_sum(a: TileTensor, b: TileTensor, dim: int,
@@ -772,14 +809,14 @@ def _tt_mul_sum(a: TileTensor, b: TileTensor, dim: int,
     s = _same_session(a, b)
     n_out = _result_tiles(("mulsum", a.shape(), b.shape(), int(dim)), lambda: sum_result_shape(
         elementwise_result_shape(a.shape(), b.shape(), OpKind.mul), dim).tile_count())
-    out = s.empty_tiles(n_out)
+    out = _Out(s, n_out)
     so = CShape()
     chain = ctypes.c_int64()
     _check(lib().tt_mul_sum(s.handle, ctypes.byref(a.shape().to_c()), _dptr(a),
                             a.chain_index(), ctypes.byref(b.shape().to_c()), _dptr(b),
                             b.chain_index(), int(dim), _variant(variant), ctypes.byref(so),
-                            _ptr(out), ctypes.byref(chain)))
-    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
+                            out.c(), ctypes.byref(chain)))
+    return out.wrap(TileTensorShape.from_c(so), chain.value)
 
 
 def tt_mul_sum_clean(a: TileTensor, b: TileTensor, dim: int,
@@ -790,14 +827,14 @@ def tt_mul_sum_clean(a: TileTensor, b: TileTensor, dim: int,
     s = _same_session(a, b)
     n_out = _result_tiles(("mulsum", a.shape(), b.shape(), int(dim)), lambda: sum_result_shape(
         elementwise_result_shape(a.shape(), b.shape(), OpKind.mul), dim).tile_count())
-    out = s.empty_tiles(n_out)
+    out = _Out(s, n_out)
     so = CShape()
     chain = ctypes.c_int64()
     _check(lib().tt_mul_sum_clean(s.handle, ctypes.byref(a.shape().to_c()), _dptr(a),
                                   a.chain_index(), ctypes.byref(b.shape().to_c()), _dptr(b),
                                   b.chain_index(), int(dim), _variant(variant), ctypes.byref(so),
-                                  _ptr(out), ctypes.byref(chain)))
-    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
+                                  out.c(), ctypes.byref(chain)))
+    return out.wrap(TileTensorShape.from_c(so), chain.value)
 
 
 def tt_mul_sum_affine(a: TileTensor, b: TileTensor, dim: int, c: Optional[TileTensor] = None,
@@ -817,16 +854,16 @@ def tt_mul_sum_affine(a: TileTensor, b: TileTensor, dim: int, c: Optional[TileTe
         return r.tile_count()
     n_out = _result_tiles(("mulsum_affine", a.shape(), b.shape(), int(dim),
                            None if c is None else c.shape()), count)
-    out = s.empty_tiles(n_out)
+    out = _Out(s, n_out)
     so = CShape()
     chain = ctypes.c_int64()
     _check(lib().tt_mul_sum_affine(
         s.handle, ctypes.byref(a.shape().to_c()), _dptr(a), a.chain_index(),
         ctypes.byref(b.shape().to_c()), _dptr(b), b.chain_index(), int(dim), _variant(variant),
         None if c is None else ctypes.byref(c.shape().to_c()), None if c is None else _dptr(c),
-        0 if c is None else c.chain_index(), 1 if square else 0, ctypes.byref(so), _ptr(out),
+        0 if c is None else c.chain_index(), 1 if square else 0, ctypes.byref(so), out.c(),
         ctypes.byref(chain)))
-    return TileTensor._wrap(TileTensorShape.from_c(so), out, s, chain.value)
+    return out.wrap(TileTensorShape.from_c(so), chain.value)
 
 
 _PRODUCT_TILES: dict = {}
@@ -866,17 +903,13 @@ def _product_slow(which: int, a: TileTensor, b: TileTensor, variant) -> TileTens
         if len(_PRODUCT_TILES) >= 4096:
             _PRODUCT_TILES.clear()
         _PRODUCT_TILES[key] = n_out
-    out = s.empty_tiles(max(n_out, 1))
+    out = _Out(s, max(n_out, 1))
     _check(lib().tt_linalg_product(s.handle, which, ctypes.byref(a.shape().to_c()),
                                    _dptr(a), a.chain_index(),
                                    ctypes.byref(b.shape().to_c()), _dptr(b),
                                    b.chain_index(), _variant(variant), ctypes.byref(so),
-                                   _ptr(out), ctypes.byref(chain)))
-    shape = TileTensorShape.from_c(so)
-    n = shape.tile_count()
-    if n > out.shape[0]:  # the host-side sizing and the C-ABI disagree: never hand out a short view
-        raise ShapeError(f"product result has {n} tiles, {out.shape[0]} allocated")
-    return TileTensor._wrap(shape, out if n == out.shape[0] else out[:n], s, chain.value)
+                                   out.c(), ctypes.byref(chain)))
+    return out.wrap(TileTensorShape.from_c(so), chain.value)
 
 
 def matvec_a(m: TileTensor, v: TileTensor, variant=None) -> TileTensor:  # linalg.hpp:41
@@ -920,21 +953,17 @@ def linalg_chain(first: str, a: TileTensor, b: TileTensor, second: str, x: TileT
         n1 = s1.tile_count()
     except ShapeError:  # let the C-ABI raise the reference's error for the calls
         n1 = n2 = 0
-    out1 = s.empty_tiles(max(n1, 1))
-    out2 = s.empty_tiles(max(n2, 1))
+    out1, out2 = _Out(s, n1), _Out(s, n2)
     so1, so2 = CShape(), CShape()
     c1, c2 = ctypes.c_int64(), ctypes.c_int64()
     _check(lib().tt_linalg_chain2(s.handle, w1, ctypes.byref(a.shape().to_c()), _dptr(a),
                                   a.chain_index(), ctypes.byref(b.shape().to_c()), _dptr(b),
                                   b.chain_index(), w2, ctypes.byref(x.shape().to_c()), _dptr(x),
                                   x.chain_index(), 1 if first_is_right else 0, _variant(variant),
-                                  ctypes.byref(so1), _ptr(out1), ctypes.byref(c1), ctypes.byref(so2),
-                                  _ptr(out2), ctypes.byref(c2)))
-    sh1, sh2 = TileTensorShape.from_c(so1), TileTensorShape.from_c(so2)
-    if sh1.tile_count() > out1.shape[0] or sh2.tile_count() > out2.shape[0]:
-        raise ShapeError("chain result larger than allocated")
-    return (TileTensor._wrap(sh1, out1[:sh1.tile_count()], s, c1.value),
-            TileTensor._wrap(sh2, out2[:sh2.tile_count()], s, c2.value))
+                                  ctypes.byref(so1), out1.c(), ctypes.byref(c1), ctypes.byref(so2),
+                                  out2.c(), ctypes.byref(c2)))
+    return (out1.wrap(TileTensorShape.from_c(so1), c1.value),
+            out2.wrap(TileTensorShape.from_c(so2), c2.value))
 
 
 def clean_unknowns(t: TileTensor) -> TileTensor:  # tile_tensor.hpp:352-386
