@@ -303,7 +303,25 @@ __global__ void __launch_bounds__(256) clean_chunk_kernel(const __grid_constant_
           const int64_t k = u * 256 + threadIdx.x;
           if (2 * k < n) x[u] = __ldg(s2 + k);
         }
-        if (n == kCleanChunk && g.tile_slots == g.s) {
+        // a cut dim whose whole period t * 2^sh fits in 512 slots has the same
+        // coordinate at o and at base + 512 u + o: the mask is per thread
+        bool local = true;
+#pragma unroll
+        for (int i = 0; i < RK; ++i) local = local && (!cut[i] || (g.t[i] << sh[i]) <= 512);
+        if (local && n == kCleanChunk && g.tile_slots == g.s) {
+          bool ok[2] = {true, true};
+#pragma unroll
+          for (int i = 0; i < RK; ++i)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (cut[i]) ok[e] = ok[e] && (((2 * static_cast<int>(threadIdx.x) + e) >> sh[i]) & (g.t[i] - 1)) < v[i];
+          const double m0 = ok[0] ? 1.0 : 0.0, m1 = ok[1] ? 1.0 : 0.0;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t k = u * 256 + threadIdx.x;
+            d2[k] = make_double2(dmul(x[u].x, m0), dmul(x[u].y, m1));
+          }
+        } else if (n == kCleanChunk && g.tile_slots == g.s) {
           // h = base + 512 u + o with o = 2 tid + e < 512 and base + 512 u a
           // multiple of 512, so the coordinate of a cut dim with stride 2^sh
           // splits into an item/u part and a per-thread part:

@@ -64,45 +64,75 @@ __device__ __forceinline__ void row_shift(double (&v)[NR], int D) {
 // block first, and carries each block's raw (pre-tree) rows over as the halo of
 // the block before it -- rows are read (C + HR/R) / C times instead of twice.
 template <int HR, int R = 16, bool BACK = false, bool EPI = false, int C = 1>
-__global__ void __launch_bounds__(256, (HR <= 8 ? 3 : 2)) row_tree_kernel(const double* __restrict__ in,
+__global__ void __launch_bounds__(256, (C == 1 && R + HR <= 20 ? 2 : HR <= 8 ? 3 : 2)) row_tree_kernel(const double* __restrict__ in,
                                                        double* __restrict__ out, int64_t n_tiles,
                                                        int64_t s, int nlevels, int4 lv0, int4 lv1,
                                                        const __grid_constant__ EpiDev epi) {
   constexpr int NR = R + HR;
+  // PF: the next block's rows are loaded before this block's levels run, so a
+  // warp keeps its loads in flight while it computes (small halos only: the
+  // second row set doubles the registers)
+  constexpr bool PF = C == 1 && NR <= 20;
   static_assert(C == 1 || HR <= R, "the carried halo comes from one block");
   const int lane = threadIdx.x & 31;
   const int rows = static_cast<int>(s / 32);
   const int chains_per_tile = rows / R / C;
   const uint64_t total = static_cast<uint64_t>(n_tiles) * chains_per_tile;
   const int lvl[8] = {lv0.x, lv0.y, lv0.z, lv0.w, lv1.x, lv1.y, lv1.z, lv1.w};
-  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
-       u < total; u += static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5)) {
+  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  // rows [block, block + NR) of unit u (cyclic over its tile), mirrored when BACK
+  auto load_rows = [&](uint64_t u, double (&dst)[NR]) {
+    const uint64_t tile = u / chains_per_tile;
+    const int rb = static_cast<int>(u - tile * chains_per_tile) * R;
+    const double* t = in + tile * s;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      int row = rb + i;
+      if (row >= rows) row -= rows;
+      const int64_t p = row * 32 + lane;
+      dst[i] = __ldg(t + (BACK ? s - 1 - p : p));
+    }
+  };
+  double pre[PF ? NR : 1];
+  uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if constexpr (PF) {
+    if (u < total) load_rows(u, pre);
+  }
+  for (; u < total; u += gstride) {
     const uint64_t tile = u / chains_per_tile;
     const int b0 = static_cast<int>(u - tile * chains_per_tile) * C;
     const double* t = in + tile * s;
     double* o = out + tile * s;
     double halo[HR];  // raw rows following the current block (cyclic over the tile)
+    if constexpr (!PF) {
 #pragma unroll
-    for (int i = 0; i < HR; ++i) {
-      int row = (b0 + C) * R + i;
-      if (row >= rows) row -= rows;
-      const int64_t p = row * 32 + lane;
-      halo[i] = __ldg(t + (BACK ? s - 1 - p : p));
+      for (int i = 0; i < HR; ++i) {
+        int row = (b0 + C) * R + i;
+        if (row >= rows) row -= rows;
+        const int64_t p = row * 32 + lane;
+        halo[i] = __ldg(t + (BACK ? s - 1 - p : p));
+      }
     }
 #pragma unroll 1
     for (int kk = C - 1; kk >= 0; --kk) {
     const int rb = (b0 + kk) * R;
     double v[NR];
+    if constexpr (PF) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int64_t p = (rb + i) * 32 + lane;
-      v[i] = __ldg(t + (BACK ? s - 1 - p : p));
-    }
+      for (int i = 0; i < NR; ++i) v[i] = pre[i];
+      if (u + gstride < total) load_rows(u + gstride, pre);
+    } else {
 #pragma unroll
-    for (int i = 0; i < HR; ++i) v[R + i] = halo[i];
-    if (C > 1) {
+      for (int i = 0; i < R; ++i) {
+        const int64_t p = (rb + i) * 32 + lane;
+        v[i] = __ldg(t + (BACK ? s - 1 - p : p));
+      }
 #pragma unroll
-      for (int i = 0; i < HR; ++i) halo[i] = v[i < R ? i : 0];
+      for (int i = 0; i < HR; ++i) v[R + i] = halo[i];
+      if (C > 1) {
+#pragma unroll
+        for (int i = 0; i < HR; ++i) halo[i] = v[i < R ? i : 0];
+      }
     }
     for (int k = 0; k < nlevels; ++k) {
       const int d = lvl[k];

@@ -45,6 +45,8 @@ def timeit(fn, reps):
 T = 131072 * 16384 * 8
 for name, fn, nb, reps in (("ew_mul_bcast", lambda: tt.tt_mul(X, W), 2 * T + 1024 * 16384 * 8, 5),
                            ("clean_unknowns", lambda: tt.clean_unknowns(R3), 2 * 8192 * 16384 * 8, 20),
-                           ("replicate_dim", lambda: tt.replicate_dim(C3, 3), 2 * 8192 * 16384 * 8, 20)):
+                           ("replicate_dim", lambda: tt.replicate_dim(C3, 3), 2 * 8192 * 16384 * 8, 20),
+                           ("ew_add_1GiB", lambda: tt.tt_add(C3, C3), 2 * 8192 * 16384 * 8, 20),
+                           ("copy_1GiB", lambda: C3.data().clone(), 2 * 8192 * 16384 * 8, 20)):
     t = timeit(fn, reps)
     print(f"{name:16s} {t * 1e3:8.3f} ms  {nb / t / 1e9:8.1f} GB/s  {nb / t / 1e9 / peak:.3f} of peak")
