@@ -434,6 +434,10 @@ int or_sum(const tt_shape* sh, const double* tin, int64_t s, int dim, int varian
   const tt_dim* ds = &sh->dims[di];
   const size_t bytes = (size_t)s * sizeof(double);
   const int64_t n_in = or_tile_count(sh);
+  /* builder's `~` rule I9: the '?' boundary split assumes
+   * a used prefix per tile; an unknown interleaved dim must be cleaned first */
+  if (ds->interleaved && ds->unknown && ds->n * ds->d < ((ds->n * ds->d + ds->t - 1) / ds->t) * ds->t)
+    return OR_SHAPE;
   if (ds->n == 1 && ds->d > 1) { /* degenerate: tiles unchanged :295 */
     memmove(out, tin, (size_t)n_in * bytes);
     return OR_OK;
@@ -556,6 +560,7 @@ int or_replicate_dim(const tt_shape* sh, const double* tin, int64_t s, int dim, 
   for (int64_t flat = 0; flat < n; ++flat)
     or_replicate_tile_dim(tin + flat * s, s, te, sh->rank, dim, out + flat * s, c);
   so->dims[dim - 1].d = ds->t;
+  so->dims[dim - 1].interleaved = 0; /* I13: a replicated dim is not interleaved */
   return OR_OK;
 }
 
