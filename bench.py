@@ -324,7 +324,7 @@ def run_reference(args):
     value, sample = _leg_summary(leg)
     one = None
     try:
-        o = cpu_leg_subprocess(1, args.ref_slab_tiles, 1, 0)
+        o = cpu_leg_subprocess(1, args.cpu_one_thread_slab_tiles, 1, 0)
         v1, s1 = _leg_summary(o)
         one = {"value": v1, "unit": "tile-slots/s", "cores": 1, "sample": s1}
     except Exception as exc:
@@ -538,7 +538,7 @@ def run_ours(args):
         if not args.skip_extra:
             ops.update(bench_extra_ops(tt, X, W, x_dense, sx, S, stream, hbm_peak, args, out_tiles))
             ops.update(bench_matmul(tt, configs, S, stream, hbm_peak, max(3, args.steps)))
-            ops.update(bench_small_configs(tt, configs, stream, hbm_peak, max(20, args.steps)))
+            ops.update(bench_small_configs(tt, configs, stream, hbm_peak, max(200, args.steps)))
             if rank == 0:
                 ops["cpp"] = bench_cpp_leg()
     except Exception as exc:  # keep the bench line: report the failure instead
@@ -919,9 +919,11 @@ def main():
     ap.add_argument("--skip-extra", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-pinned", type=int, default=1)
-    ap.add_argument("--cpu-slab-tiles", type=int, default=48)  # ~5 s of reference CPU work
+    # the reference arm and the cpu_baseline leg time the same slab (32 external rows of
+    # dim 1 = 32768 of 131072 X tiles, ~3.5 s per step on 16 host threads)
+    ap.add_argument("--cpu-slab-tiles", type=int, default=32)
     ap.add_argument("--cpu-one-thread-slab-tiles", type=int, default=4)
-    ap.add_argument("--ref-slab-tiles", type=int, default=8)
+    ap.add_argument("--ref-slab-tiles", type=int, default=32)
     ap.add_argument("--scaling", default="auto", choices=["auto", "strong", "weak"])
     ap.add_argument("--dump", default="", help="write result slabs per rank (parity test)")
     ap.add_argument("--cpu-leg", default="", help=argparse.SUPPRESS)
