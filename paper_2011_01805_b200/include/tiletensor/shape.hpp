@@ -1,0 +1,4 @@
+#pragma once
+// Drop-in include path: the reference's "tiletensor/shape.hpp" (proj/include/tiletensor/shape.hpp)
+// resolves to the B200 build's header of the same API, so callers keep their #include lines.
+#include "tiletensor_b200/shape.hpp"

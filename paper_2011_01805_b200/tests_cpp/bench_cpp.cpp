@@ -19,8 +19,10 @@
 #include <string>
 #include <vector>
 
-#include "tiletensor_b200/linalg.hpp"
-#include "tiletensor_b200/tile_tensor.hpp"
+// the reference's own include names (proj/include/tiletensor/*.hpp), resolved to
+// the drop-in headers by paper_2011_01805_b200/include/tiletensor/
+#include "tiletensor/linalg.hpp"
+#include "tiletensor/tile_tensor.hpp"
 
 using namespace tiletensor;
 using clk = std::chrono::steady_clock;
