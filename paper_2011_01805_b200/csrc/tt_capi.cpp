@@ -41,6 +41,7 @@ struct tt_session {
   size_t scratch_bytes = 0;
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;
+  size_t l2_bytes = size_t{126} << 20;
   // compiled rotate-and-sum schedules, keyed by (ext, t, stride, used,
   // unknown, variant): a schedule depends only on these (slots are fixed per
   // session), and rebuilding it per call costs more host time than a small
@@ -117,6 +118,7 @@ LaunchCtx ctx_of(tt_session* s) {
   c.device = s->device;
   c.sm_count = s->sm_count;
   c.smem_optin = s->smem_optin;
+  c.l2_bytes = s->l2_bytes;
   c.launches = &s->launches;
   c.scratch = scratch_fn;
   c.scratch_owner = s;
@@ -414,6 +416,7 @@ int tt_session_create(int64_t slot_count, int64_t max_chain_index, int device, t
       check_cuda(cudaGetDeviceProperties(&prop, device), "device properties");
       s->sm_count = prop.multiProcessorCount;
       s->smem_optin = prop.sharedMemPerBlockOptin;
+      s->l2_bytes = static_cast<size_t>(prop.l2CacheSize);
       const size_t sched_bytes = (2 * kSchedSlots + kChainSlots * kChainCounters) * sizeof(unsigned int);
       check_cuda(cudaMalloc(&s->sched, sched_bytes), "scheduler counters");
       check_cuda(cudaMemset(s->sched, 0, sched_bytes), "scheduler counters");

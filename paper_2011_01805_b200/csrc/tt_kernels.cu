@@ -595,9 +595,13 @@ int forced_path() {
 }
 
 // Few-group folds stream their operands through a cp.async ring
-// (fold_ring_kernel) when the streamed operand is larger than ~half the L2:
-// config 4's layer-2 fold 36 -> 22 us; an L2-resident one (config 2, 32 MiB)
-// is ~0.5 us faster without.  TT_FOLD_RING=0 / 1 forces it off / on.
+// (fold_ring_kernel) when the streamed operand's bytes (groups x fold steps x
+// tile: the per-group operand; a broadcast second operand is re-read from L2 and
+// not counted) exceed half the device L2: config 4's layer-2 fold (100 MiB) 36 ->
+// 22 us; an L2-resident one (config 2, 32 MiB) is ~0.5 us faster without.
+// TT_FOLD_RING=0 / 1 forces it off / on; "on" still needs the ring's layout:
+// s % 256 == 0, more than one fold step, 16-byte aligned operands (otherwise
+// the plain fold runs).
 const int g_fold_ring = [] {
   const char* e = std::getenv("TT_FOLD_RING");
   return e ? std::atoi(e) : -1;
@@ -618,7 +622,7 @@ void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, con
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, true>, 256, 0, work);
     fold_kernel<HAS_B, true><<<grid, 256, 0, c.stream>>>(to_fold(p), ta, tb, tout, make_div64(units));
   } else if ((g_fold_ring == 1 ||
-              (g_fold_ring < 0 && p.g.groups * p.ops[0].y * s * 8 > (int64_t{48} << 20))) &&
+              (g_fold_ring < 0 && p.g.groups * p.ops[0].y * s * 8 > static_cast<int64_t>(c.l2_bytes / 2))) &&
              s % 256 == 0 && p.ops[0].y > 1 && aligned16(ta) && (!HAS_B || aligned16(tb)) &&
              aligned16(tout)) {
     const int64_t runs = s / 256;

@@ -14,6 +14,7 @@ struct LaunchCtx {
   int device = 0;
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;  // max dynamic smem per block
+  size_t l2_bytes = size_t{126} << 20;  // device L2 size (cudaDeviceProp::l2CacheSize)
   uint64_t* launches = nullptr;    // incremented per kernel launch
   // Session-owned device scratch; (re)sized by the caller via `need`.
   double* (*scratch)(void* owner, size_t bytes) = nullptr;
