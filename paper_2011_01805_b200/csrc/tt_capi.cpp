@@ -17,6 +17,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "tt_internal.hpp"
@@ -63,6 +64,7 @@ struct tt_session {
     bool cacheable;
   };
   std::unordered_map<void*, CachedBlock> live;
+  std::unordered_set<void*> direct;  // blocks from cudaMalloc (large), not the pool
   std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free_blocks;
   size_t cached_bytes = 0;
   size_t cache_cap = size_t{8} << 30;  // a quarter of the device memory (set at creation)
@@ -520,12 +522,27 @@ void* cache_take(tt_session* s, size_t nb) {
   return p;
 }
 
+// Large blocks outside stream capture come from cudaMalloc: growing the
+// stream-ordered pool maps physical memory at ~20 GB/s (a first 16 GiB result
+// took 0.8 s), cudaMalloc does it in a few ms.  They are cached like the rest and
+// returned with cudaFree only beyond the cache cap or at session end.
+constexpr size_t kDirectAllocBytes = size_t{64} << 20;
+
 void* block_alloc(tt_session* s, size_t nb, bool cacheable) {
   void* p = cacheable ? cache_take(s, nb) : nullptr;
+  bool direct = false;
   if (!p) {
     check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
-    check_cuda(cudaMallocFromPoolAsync(&p, nb, s->pool, s->stream), "cudaMallocFromPoolAsync");
+    if (cacheable && nb >= kDirectAllocBytes) {
+      check_cuda(cudaMalloc(&p, nb), "cudaMalloc");
+      direct = true;
+    } else {
+      check_cuda(cudaMallocFromPoolAsync(&p, nb, s->pool, s->stream), "cudaMallocFromPoolAsync");
+    }
+  } else {
+    direct = s->direct.count(p) != 0;
   }
+  if (direct) s->direct.insert(p);
   s->live[p] = {nb, s->stream, cacheable};
   return p;
 }
@@ -538,6 +555,10 @@ void block_release(tt_session* s, void* p) {
   if (b.cacheable && s->cached_bytes + b.bytes <= s->cache_cap) {
     s->free_blocks[{b.stream, b.bytes}].push_back(p);
     s->cached_bytes += b.bytes;
+  } else if (s->direct.erase(p)) {
+    check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
+    check_cuda(cudaStreamSynchronize(b.stream), "stream synchronize");  // its last users
+    check_cuda(cudaFree(p), "cudaFree");
   } else {
     check_cuda(cudaSetDevice(s->device), "cudaSetDevice");
     check_cuda(cudaFreeAsync(p, s->stream), "cudaFreeAsync");
