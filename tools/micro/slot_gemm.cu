@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstring>
 #include <vector>
+#include <algorithm>
+#include <cstdlib>
 
 #define CK(x)                                                                              \
   do {                                                                                     \
@@ -58,7 +60,7 @@ constexpr int NI = 32, NJ = 16, K = 48, S = 8192;
 template <int PI, int PJ, int SL, int RI, int RJ, int KS, int NS, int MODE, int MINB, int SCHED>
 __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
     sg_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, double* out,
-              int reps, unsigned* q) {
+              int reps, unsigned* q, unsigned long long* rec) {
   constexpr int kC = (PI / RI) * (PJ / RJ) * SL;  // consumer threads
   constexpr int kCW = kC / 32;
   constexpr int kA = KS * PI * SL, kB = KS * PJ * SL, kSt = kA + kB;
@@ -129,6 +131,8 @@ __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
     if (u < 0) break;
     const int uu = u % units1;
     const int ch = uu % nch, b = uu / nch, bi = b % nbi, bj = b / nbi;
+    unsigned long long t_begin = 0;
+    if (rec && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
     double acc[RI][RJ];
 #pragma unroll
     for (int i = 0; i < RI; ++i)
@@ -156,6 +160,15 @@ __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
         st = 0;
         ph ^= 1;
       }
+    }
+    if (rec && threadIdx.x == 0) {
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      rec[3 * u] = t_begin;
+      rec[3 * u + 1] = t_end;
+      rec[3 * u + 2] = smid * 65536ull + blockIdx.x;
     }
     if (u < units1 || MODE != 0) {
       double* o = out + ((size_t)(bi * PI + r0) * NJ + bj * PJ + c0) * S + ch * SL + slot;
@@ -225,7 +238,7 @@ void run(const char* name, int reps) {
   cudaEventCreate(&e1);
   CK(cudaMemset(gO, 0xff, (size_t)NI * NJ * S * 8));
   CK(cudaMemset(gQ, 0, 4096));
-  k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ);
+  k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ, nullptr);
   CK(cudaDeviceSynchronize());
   bool ok = true;
   if (MODE == 0) {
@@ -238,12 +251,48 @@ void run(const char* name, int reps) {
   for (int it = 0; it < 5; ++it) {
     CK(cudaMemsetAsync(gQ, 0, 4096));
     cudaEventRecord(e0);
-    k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ);
+    k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ, nullptr);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     best = std::min(best, ms);
+  }
+  if (getenv("SG_TIMELINE")) {
+    const int units = (NI / PI) * (NJ / PJ) * (S / SL) * reps;
+    unsigned long long* rec;
+    CK(cudaMalloc(&rec, units * 24));
+    CK(cudaMemsetAsync(gQ, 0, 4096));
+    k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ, rec);
+    CK(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(units * 3);
+    CK(cudaMemcpy(h.data(), rec, units * 24, cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int u = 0; u < units; ++u) { t0 = std::min(t0, h[3 * u]); t1 = std::max(t1, h[3 * u + 1]); }
+    std::vector<double> sm_end(g_sms, 0), sm_busy(g_sms, 0);
+    std::vector<int> sm_units(g_sms, 0);
+    double dsum = 0, dmin = 1e30, dmax = 0;
+    for (int u = 0; u < units; ++u) {
+      const int sm = (int)(h[3 * u + 2] >> 16);
+      const double b = (h[3 * u] - t0) * 1e-3, e = (h[3 * u + 1] - t0) * 1e-3;
+      sm_end[sm] = std::max(sm_end[sm], e);
+      sm_units[sm]++;
+      dsum += e - b; dmin = std::min(dmin, e - b); dmax = std::max(dmax, e - b);
+    }
+    std::vector<double> ends = sm_end;
+    std::sort(ends.begin(), ends.end());
+    int hist[12] = {0};
+    for (int i = 0; i < g_sms; ++i) hist[std::min(11, sm_units[i])]++;
+    printf("   timeline: span %.1f us; unit duration min/avg/max %.1f/%.1f/%.1f us; SM finish p0/p10/p50/p90/p100 %.1f/%.1f/%.1f/%.1f/%.1f us\n",
+           (t1 - t0) * 1e-3, dmin, dsum / units, dmax, ends[0], ends[g_sms / 10], ends[g_sms / 2], ends[g_sms * 9 / 10], ends[g_sms - 1]);
+    printf("   units per SM histogram:");
+    for (int i = 0; i < 12; ++i) if (hist[i]) printf(" %d:%d", i, hist[i]);
+    printf("\n");
+    // first unit start per SM and per-round timing
+    double first_end = 1e30;
+    for (int u = 0; u < units; ++u) first_end = std::min(first_end, (h[3 * u + 1] - t0) * 1e-3);
+    printf("   earliest unit end %.1f us\n", first_end);
+    cudaFree(rec);
   }
   const double ops = 2.0 * NI * NJ * K * (double)S * reps;
   printf("%-40s reps=%d thr=%3d occ=%d grid=%4d regs=%3d smem=%6zu  %8.2f us  %5.1f%% fp64 %s\n", name, reps, threads,
@@ -268,25 +317,8 @@ int main() {
   CK(cudaMemcpy(gB, h.data() + 7, nb * 8, cudaMemcpyHostToDevice));
   ref_kernel<<<(NI * NJ * S + 255) / 256, 256>>>(gA, gB, gR);
   CK(cudaDeviceSynchronize());
-  // the shipped shape: 16x16 groups x 16 slots, 8x4 per thread, 4x4 ring, 3 CTAs/SM
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 0>("16x16x16 8x4 ks4 ns4 static-rr", 1);
   run<16, 16, 16, 8, 4, 4, 4, 0, 3, 1>("16x16x16 8x4 ks4 ns4 per-SM", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 1>("16x16x16 8x4 ks4 ns4 per-SM", 8);
-  run<16, 16, 16, 8, 4, 4, 4, 2, 3, 1>("  ..no TMA", 8);
-  run<32, 16, 16, 8, 4, 4, 4, 0, 2>("32x16x16 8x4 ks4 ns4", 1);
-  run<32, 16, 16, 8, 4, 4, 4, 0, 2>("32x16x16 8x4 ks4 ns4", 8);
-  run<32, 16, 16, 8, 4, 4, 4, 2, 2>("  ..no TMA", 8);
-  run<32, 16, 8, 8, 4, 4, 6, 0, 3>("32x16x8 8x4 ks4 ns6", 1);
-  run<32, 16, 8, 8, 4, 4, 6, 0, 3>("32x16x8 8x4 ks4 ns6", 8);
-  run<32, 16, 8, 8, 4, 4, 6, 2, 3>("  ..no TMA", 8);
-  run<32, 16, 4, 8, 4, 4, 8, 0, 6>("32x16x4 8x4 ks4 ns8", 1);
-  run<32, 16, 4, 8, 4, 4, 8, 0, 6>("32x16x4 8x4 ks4 ns8", 8);
-  run<32, 16, 8, 8, 8, 4, 6, 0, 4>("32x16x8 8x8 ks4 ns6", 1);
-  run<32, 16, 8, 8, 8, 4, 6, 0, 4>("32x16x8 8x8 ks4 ns6", 8);
-  run<32, 16, 16, 8, 8, 4, 4, 0, 2>("32x16x16 8x8 ks4 ns4", 1);
-  run<16, 16, 16, 8, 4, 8, 3, 0, 3>("16x16x16 8x4 ks8 ns3", 1);
-  run<16, 16, 16, 8, 4, 2, 8, 0, 3>("16x16x16 8x4 ks2 ns8", 1);
-  run<16, 16, 8, 8, 4, 4, 6, 0, 4>("16x16x8 8x4 ks4 ns6", 1);
-  run<16, 16, 8, 8, 4, 4, 6, 0, 4>("16x16x8 8x4 ks4 ns6", 8);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 0>("16x16x16 8x4 ks4 ns4 static", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 1>("16x16x16 8x4 ks4 ns4 per-SM", 4);
   return 0;
 }
