@@ -43,7 +43,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
            "-ffp-contract=off", "--fmad=false", "-I", str(ROOT / "include"), "-I", str(CSRC)]
 SOURCES = ["tt_shape.cpp", "tt_schedule.cpp", "tt_capi.cpp", "tt_kernels.cu", "tt_tma_pack.cu"]
-HEADERS = [CSRC / "tt_internal.hpp", CSRC / "tt_launch.hpp", ROOT / "include" / "tiletensor_b200.h",
+HEADERS = [CSRC / "tt_internal.hpp", CSRC / "tt_launch.hpp", CSRC / "tt_pdl.cuh", ROOT / "include" / "tiletensor_b200.h",
            *sorted((CSRC / "kernels").glob("*.cuh"))]
 
 

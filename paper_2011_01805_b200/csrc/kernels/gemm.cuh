@@ -31,6 +31,7 @@ template <bool HAS_B, int P, int Q>
 __global__ void __launch_bounds__(kBlockThreads) fold_blocked_kernel(
     const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
     const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ OUT) {
+  pdl_enter();
   const int64_t s = p.s;
   const int64_t first = p.first;
   const int64_t count = p.count;
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(128) fold_ring_kernel(const __grid_constant__ 
                                                         const double* __restrict__ A,
                                                         const double* __restrict__ B,
                                                         double* __restrict__ OUT, FastDiv64 runs_div) {
+  pdl_enter();
   __shared__ __align__(16) double2 ring[kFoldRing][HAS_B ? 2 : 1][128];
   const int64_t s = p.s;
   const int64_t count = p.count;
@@ -186,6 +188,7 @@ __global__ void __launch_bounds__((SLOTS / 32) * (kGemmBlk / kGemmSubR) * (BC / 
     fold_gemm_kernel(const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
                      const double* __restrict__ A, const double* __restrict__ B,
                      double* __restrict__ OUT) {
+  pdl_enter();
   constexpr int kHalves = SLOTS / 32;
   constexpr int kThreads = kHalves * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32;
   constexpr int kSubCols = BC / kGemmSubC;
@@ -466,6 +469,7 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
                          const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
                          const __grid_constant__ TgSpec ts, double* __restrict__ OUT,
                          unsigned int* __restrict__ sched) {
+  pdl_enter();
   constexpr int kW = tg_warps<BC, SL, SC, PB>();
   constexpr int kTgRows = 8 / SC;  // rows of products batched before their adds
   constexpr int kA = kTgSteps * PB * SL;  // doubles per stage
@@ -663,6 +667,7 @@ __global__ void __launch_bounds__((tg_warps<BC, SL, SC, PB>() + 1) * 32, 3)
                         const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
                         const __grid_constant__ TgSpec ts, double* __restrict__ OUT,
                         unsigned int* __restrict__ sched, int wait_mode) {
+  pdl_enter();
   // wait_mode (TT_GEMM_WAIT): 0 = every mbarrier waiter spins on try_wait,
   // 1 = the producer sleeps on try_wait's suspend hint, 2 = every waiter does
   constexpr int kW = tg_warps<BC, SL, SC, PB>();  // consumer warps

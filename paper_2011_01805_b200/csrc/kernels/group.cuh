@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(512, 1) group_pow2_kernel(const __grid_constan
                                                             const double* __restrict__ A,
                                                             const double* __restrict__ B,
                                                             double* __restrict__ OUT) {
+  pdl_enter();
   extern __shared__ __align__(16) double sbuf[];
   const int T = blockDim.x;
   const int tid = threadIdx.x;
@@ -350,6 +351,7 @@ template <int VMAX, bool HAS_B>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     group_tma_kernel(const __grid_constant__ GroupParams p, const double* __restrict__ A,
                      const double* __restrict__ B, double* __restrict__ OUT, int nstages) {
+  pdl_enter();
   extern __shared__ __align__(128) double smem[];
   const int s = static_cast<int>(p.s);
   const bool b_stream = HAS_B && p.g.bstep != 0;
@@ -500,6 +502,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     group_tma_win_kernel(const __grid_constant__ GroupParams p, const double* __restrict__ A,
                          const double* __restrict__ B, double* __restrict__ OUT, int nstages,
                          int halo) {
+  pdl_enter();
   extern __shared__ __align__(128) double smem[];
   const int s = static_cast<int>(p.s);
   const bool b_stream = HAS_B && p.g.bstep != 0;
@@ -698,6 +701,7 @@ __global__ void __launch_bounds__(512) group_generic_kernel(const __grid_constan
                                                             const double* __restrict__ B,
                                                             double* __restrict__ OUT,
                                                             double* __restrict__ scratch) {
+  pdl_enter();
   extern __shared__ __align__(16) double sbuf[];
   const int T = blockDim.x;
   const int tid = threadIdx.x;
@@ -761,6 +765,7 @@ __global__ void __launch_bounds__(256) fold_kernel(const __grid_constant__ FoldP
                                                     const double* __restrict__ B,
                                                     double* __restrict__ OUT,
                                                     FastDiv64 units_div) {
+  pdl_enter();
   const int64_t first = p.first;
   const int64_t count = p.count;
   const int64_t s = p.s;

@@ -15,6 +15,7 @@ __global__ void __launch_bounds__(256) batch_affine_kernel(const double* __restr
                                                            const double* __restrict__ w,
                                                            const double* __restrict__ bias,
                                                            double* __restrict__ out, FastDiv64 sdiv) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t o = fdiv(i, sdiv);
@@ -41,6 +42,7 @@ __global__ void __launch_bounds__(256) fold_range_kernel(const __grid_constant__
                                                           const double* __restrict__ init,
                                                           double* __restrict__ acc_out, uint64_t total,
                                                           FastDiv64 pairs_div) {
+  pdl_enter();
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t k = fdiv(w, pairs_div);  // output tile within the range
@@ -100,6 +102,7 @@ __global__ void __launch_bounds__(256) batch_affine_blocked_kernel(
     const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ src,
     const double* __restrict__ w, const double* __restrict__ bias, double* __restrict__ out,
     FastDiv64 pairs_div) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t blk = fdiv(i, pairs_div);
@@ -149,6 +152,7 @@ __global__ void __launch_bounds__(256) batch_affine_smem_kernel(
     const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ src,
     const double* __restrict__ w, const double* __restrict__ bias, double* __restrict__ out,
     FastDiv64 chunks_div) {
+  pdl_enter();
   __shared__ __align__(16) double ws[kBaTaps][8];
   __shared__ int64_t ss[kBaTaps];
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {

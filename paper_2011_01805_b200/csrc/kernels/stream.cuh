@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ Geo g
                                                     const double* __restrict__ dense,
                                                     double* __restrict__ tiles,
                                                     FastDiv64 units_div) {
+  pdl_enter();
   const uint64_t total = static_cast<uint64_t>(g.n_tiles) * units_div.d;
   const int lane = threadIdx.x & 31;
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -160,6 +161,7 @@ __global__ void __launch_bounds__(256) unpack_kernel(const __grid_constant__ Geo
                                                       const double* __restrict__ tiles,
                                                       double* __restrict__ dense,
                                                       uint64_t total) {
+  pdl_enter();
   const uint64_t quads = (total + 3) / 4;
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < quads;
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -216,6 +218,7 @@ __global__ void __launch_bounds__(256) clean_kernel(const __grid_constant__ Geo 
                                                      const double* __restrict__ in,
                                                      double* __restrict__ out,
                                                      FastDiv64 quads_div) {
+  pdl_enter();
   const uint64_t total = static_cast<uint64_t>(g.n_tiles) * quads_div.d;
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -246,6 +249,7 @@ __global__ void __launch_bounds__(256) clean_chunk_kernel(const __grid_constant_
                                                            const double* __restrict__ in,
                                                            double* __restrict__ out,
                                                            FastDiv64 chunks_div) {
+  pdl_enter();
   const uint64_t items = static_cast<uint64_t>(g.n_tiles) * chunks_div.d;
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint64_t flat = fdiv(item, chunks_div);
@@ -396,6 +400,7 @@ __global__ void __launch_bounds__(256) elementwise_kernel(const __grid_constant_
                                                            const double* __restrict__ b,
                                                            double* __restrict__ out,
                                                            FastDiv64 quads_div) {
+  pdl_enter();
   const uint64_t total = static_cast<uint64_t>(p.n_tiles) * quads_div.d;
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -479,6 +484,7 @@ __global__ void __launch_bounds__(256) elementwise_chunk_kernel(const __grid_con
                                                                  const double* __restrict__ b,
                                                                  double* __restrict__ out,
                                                                  FastDiv64 chunks_div) {
+  pdl_enter();
   const uint64_t items = static_cast<uint64_t>(p.n_tiles) * chunks_div.d;
   const int tid = threadIdx.x;
   const uint64_t pol_a = l2_policy(HINT && p.keep_a), pol_b = l2_policy(HINT && p.keep_b);
@@ -537,6 +543,7 @@ __global__ void __launch_bounds__(256) binary_flat_kernel(const double* __restri
                                                            const double* __restrict__ b,
                                                            double* __restrict__ out,
                                                            uint64_t count) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     out[i] = OP == TT_OP_ADD ? dadd(a[i], b[i]) : dmul(a[i], b[i]);
@@ -546,6 +553,7 @@ __global__ void __launch_bounds__(256) rotate_kernel(const double* __restrict__ 
                                                       double* __restrict__ out, uint64_t s,
                                                       uint64_t r, uint64_t total,
                                                       FastDiv64 sdiv) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t tile = fdiv(i, sdiv);
@@ -563,6 +571,7 @@ __global__ void __launch_bounds__(256) rotate_chunk_kernel(const double* __restr
                                                             double* __restrict__ out, int64_t s,
                                                             int64_t r, uint64_t items,
                                                             FastDiv64 chunks_div) {
+  pdl_enter();
   constexpr int U = kRotChunk / 256;
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint64_t tile = fdiv(item, chunks_div);
@@ -596,6 +605,7 @@ __global__ void __launch_bounds__(256) rotate_aligned_kernel(const double* __res
                                                               double* __restrict__ out, int64_t s,
                                                               int64_t r, uint64_t units,
                                                               FastDiv64 units_div) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int rho = static_cast<int>(r & 31);
   const int64_t r0 = r - rho;  // aligned part of the rotation

@@ -18,6 +18,7 @@ template <int T, bool BACK = false, bool EPI = false>
 __global__ void __launch_bounds__(256) col_tree_kernel(const double* in, double* out, int64_t n_tiles,
                                                        int64_t stride, int64_t s, FastDiv64 cdiv,
                                                        const __grid_constant__ EpiDev epi) {
+  pdl_enter();
   const uint64_t total = static_cast<uint64_t>(n_tiles) * stride;
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(256, (C == 1 && R + HR <= 20 ? 2 : HR <= 8 ? 3
                                                        double* __restrict__ out, int64_t n_tiles,
                                                        int64_t s, int nlevels, int4 lv0, int4 lv1,
                                                        const __grid_constant__ EpiDev epi) {
+  pdl_enter();
   constexpr int NR = R + HR;
   // PF: the next block's rows are loaded before this block's levels run, so a
   // warp keeps its loads in flight while it computes (small halos only: the
@@ -198,6 +200,7 @@ template <int PER>
 __global__ void __launch_bounds__(kTreeThreads, 2) smem_tree_kernel(double* __restrict__ tiles,
                                                                     int64_t n_tiles, int nlevels,
                                                                     int4 lv0, int4 lv1) {
+  pdl_enter();
   extern __shared__ double tsh[];
   constexpr int T = kTreeThreads, s = T * PER;
   const int tid = threadIdx.x;
@@ -230,6 +233,7 @@ template <bool VEC>
 __global__ void __launch_bounds__(256) epilogue_kernel(double* __restrict__ tiles, int64_t n_tiles,
                                                        int64_t s, FastDiv64 per_tile,
                                                        const __grid_constant__ EpiDev epi) {
+  pdl_enter();
   const uint64_t total = static_cast<uint64_t>(n_tiles) * per_tile.d;
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {

@@ -27,8 +27,25 @@
 #include <type_traits>
 
 #include "tt_launch.hpp"
+#include "tt_pdl.cuh"
 
 namespace ttb {
+
+// TT_PDL=0: launch without programmatic stream serialization (tt_pdl.cuh)
+int pdl_enabled() {
+  static const int on = [] {
+    const char* e = std::getenv("TT_PDL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return on;
+}
+int pdl_oversub() {
+  static const int k = [] {
+    const char* e = std::getenv("TT_PDL_OVERSUB");
+    return e ? std::max(1, std::atoi(e)) : 8;
+  }();
+  return k;
+}
 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -105,6 +122,7 @@ struct OccKey {
 std::mutex g_launch_cache_mu;
 std::map<OccKey, int> g_occupancy;
 std::map<std::pair<int, const void*>, size_t> g_smem_attr;
+std::map<const void*, size_t> g_static_smem;
 
 void set_smem_attr(const void* kernel, size_t smem) {
   int dev = 0;
@@ -118,7 +136,10 @@ void set_smem_attr(const void* kernel, size_t smem) {
   cur = smem;
 }
 
-int grid_for(const LaunchCtx& c, const void* kernel, int threads, size_t smem, int64_t work) {
+// one_wave: the grid must stay co-resident (dependency waits) or schedules its
+// own work dynamically -- never oversubscribed
+int grid_for(const LaunchCtx& c, const void* kernel, int threads, size_t smem, int64_t work,
+             bool one_wave = false) {
   int per_sm = 0;
   {
     std::lock_guard<std::mutex> lk(g_launch_cache_mu);
@@ -133,9 +154,72 @@ int grid_for(const LaunchCtx& c, const void* kernel, int threads, size_t smem, i
     }
   }
   if (per_sm < 1) per_sm = 1;
-  const int64_t cap = static_cast<int64_t>(c.sm_count) * per_sm;
+  // Under PDL a grid is dispatched while its predecessor still holds most SMs:
+  // the SMs that free up first would take all of a one-wave persistent grid's
+  // CTAs.  Several waves' worth of CTAs keep the grid-stride loops balanced.
+  const int64_t waves = per_sm > 1 && !one_wave && pdl_would_allow(c, kernel, smem) ? pdl_oversub() : 1;
+  const int64_t cap = static_cast<int64_t>(c.sm_count) * per_sm * waves;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cap, work)));
 }
+
+}  // namespace
+
+// A kernel that keeps no shared memory of its own runs on L1 cache; dispatched
+// early onto an SM whose shared-memory carve-out a predecessor still holds
+// (GEMM fold, TMA group kernels: ~200 KiB per SM), it is left with a few KiB
+// of L1 and measured slower (config 3 row tree 12.2 -> 15.2 us).  Such a
+// launch after a shared-memory-heavy one is made without the PDL attribute:
+// it then starts on drained SMs, which reconfigure their carve-out.
+namespace {
+std::mutex g_pdl_mu;
+std::map<cudaStream_t, size_t> g_pdl_last;  // per-SM smem of each stream's last launch
+
+// per-CTA shared memory (dynamic + static) and resident CTAs per SM
+std::pair<size_t, size_t> smem_footprint(const LaunchCtx& c, const void* kernel, size_t dyn_smem) {
+  size_t cta = dyn_smem, per_sm = 1;
+  std::lock_guard<std::mutex> lk(g_launch_cache_mu);
+  auto it = g_static_smem.find(kernel);
+  if (it == g_static_smem.end()) {
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) fa.sharedSizeBytes = 0;
+    it = g_static_smem.emplace(kernel, fa.sharedSizeBytes).first;
+  }
+  cta += it->second;
+  for (const auto& [key, occ] : g_occupancy)
+    if (key.kernel == kernel && key.device == c.device && key.smem == dyn_smem)
+      per_sm = std::max(per_sm, static_cast<size_t>(occ));
+  return {cta, per_sm};
+}
+
+bool pdl_rule(size_t prev_per_sm, size_t cta) {
+  return !(prev_per_sm >= (size_t{96} << 10) && cta <= (size_t{16} << 10));
+}
+}  // namespace
+
+// peek: would a launch of `kernel` on c.stream get the PDL attribute now?
+bool pdl_would_allow(const LaunchCtx& c, const void* kernel, size_t dyn_smem) {
+  if (!pdl_enabled()) return false;
+  const size_t cta = smem_footprint(c, kernel, dyn_smem).first;
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  auto it = g_pdl_last.find(c.stream);
+  return pdl_rule(it == g_pdl_last.end() ? 0 : it->second, cta);
+}
+
+// A grid smaller than one full wave is launched without the attribute too:
+// dispatched early it would be packed onto the first SMs to free up (config 4's
+// 512-CTA layer-2 fold on ~70 SMs: 22 -> 28 us) instead of spread over all.
+bool pdl_allow(const LaunchCtx& c, const void* kernel, size_t dyn_smem, int64_t grid) {
+  if (!pdl_enabled()) return false;
+  const auto [cta, per_sm] = smem_footprint(c, kernel, dyn_smem);
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  if (g_pdl_last.size() > 4096) g_pdl_last.clear();  // streams come and go; a forgotten one costs one overlap
+  size_t& prev = g_pdl_last[c.stream];
+  const bool allow = pdl_rule(prev, cta) && grid >= static_cast<int64_t>(c.sm_count) * static_cast<int64_t>(per_sm);
+  prev = cta * per_sm;
+  return allow;
+}
+
+namespace {
 
 void count_launch(const LaunchCtx& c) {
   if (c.launches) ++*c.launches;
@@ -261,6 +345,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 
 __global__ void fill_uniform_kernel(double* out, uint64_t count, uint64_t key, uint64_t offset,
                                     double lo, double span) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t u = splitmix64(key ^ (offset + i));
@@ -302,9 +387,9 @@ void launch_pack(const LaunchCtx& c, const Shape& shape, int64_t s, const double
     const void* k = vec ? (const void*)pack_kernel<RK, true> : (const void*)pack_kernel<RK, false>;
     const int grid = grid_for(c, k, 256, 0, work);
     if (vec)
-      pack_kernel<RK, true><<<grid, 256, 0, c.stream>>>(g, dense, tiles, ud);
+      launch_k(c, pack_kernel<RK, true>, grid, 256, 0, g, dense, tiles, ud);
     else
-      pack_kernel<RK, false><<<grid, 256, 0, c.stream>>>(g, dense, tiles, ud);
+      launch_k(c, pack_kernel<RK, false>, grid, 256, 0, g, dense, tiles, ud);
   });
   post_launch(c, "pack kernel");
 }
@@ -317,7 +402,7 @@ void launch_unpack(const LaunchCtx& c, const Shape& shape, int64_t s, const doub
   const int64_t work = static_cast<int64_t>((total + 1023) / 1024);
   TT_RANK_SWITCH(g.rank, RK, {
     const int grid = grid_for(c, (const void*)unpack_kernel<RK>, 256, 0, work);
-    unpack_kernel<RK><<<grid, 256, 0, c.stream>>>(g, tiles, dense, total);
+    launch_k(c, unpack_kernel<RK>, grid, 256, 0, g, tiles, dense, total);
   });
   post_launch(c, "unpack kernel");
 }
@@ -342,7 +427,7 @@ void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const doubl
     const int64_t items = g.n_tiles * static_cast<int64_t>(chunks);
     TT_RANK_SWITCH(g.rank, RK, {
       const int grid = grid_for(c, (const void*)clean_chunk_kernel<RK>, 256, 0, items);
-      clean_chunk_kernel<RK><<<grid, 256, 0, c.stream>>>(g, in, out, cd);
+      launch_k(c, clean_chunk_kernel<RK>, grid, 256, 0, g, in, out, cd);
     });
     post_launch(c, "clean_unknowns chunk kernel");
     return;
@@ -352,7 +437,7 @@ void launch_clean(const LaunchCtx& c, const Shape& shape, int64_t s, const doubl
   const int64_t work = (g.n_tiles * static_cast<int64_t>(quads) + 255) / 256;
   TT_RANK_SWITCH(g.rank, RK, {
     const int grid = grid_for(c, (const void*)clean_kernel<RK>, 256, 0, work);
-    clean_kernel<RK><<<grid, 256, 0, c.stream>>>(g, in, out, qd);
+    launch_k(c, clean_kernel<RK>, grid, 256, 0, g, in, out, qd);
   });
   post_launch(c, "clean_unknowns kernel");
 }
@@ -410,7 +495,7 @@ void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shap
                       p.n_tiles * s * 8 > (int64_t{64} << 20);
     auto run = [&](auto k) {
       const int grid = grid_for(c, (const void*)k, 256, 0, items);
-      k<<<grid, 256, 0, c.stream>>>(q, ta, tb, tout, cd);
+      launch_k(c, k, grid, 256, 0, q, ta, tb, tout, cd);
     };
     if (op == TT_OP_ADD) {
       if (hint) run(elementwise_chunk_kernel<TT_OP_ADD, true>);
@@ -428,7 +513,7 @@ void launch_elementwise(const LaunchCtx& c, int op, const Shape& out, const Shap
 #define TT_EW(OPV, VECV)                                                                  \
   {                                                                                       \
     const int grid = grid_for(c, (const void*)elementwise_kernel<OPV, VECV>, 256, 0, work); \
-    elementwise_kernel<OPV, VECV><<<grid, 256, 0, c.stream>>>(p, ta, tb, tout, qd);       \
+    launch_k(c, elementwise_kernel<OPV, VECV>, grid, 256, 0, p, ta, tb, tout, qd);       \
   }
   if (op == TT_OP_ADD) {
     if (vec) TT_EW(TT_OP_ADD, true) else TT_EW(TT_OP_ADD, false)
@@ -466,7 +551,7 @@ void launch_fold_range(const LaunchCtx& c, const FoldRange& fr, int64_t s, int64
 #define TT_FR(HB, IN)                                                                        \
   {                                                                                         \
     const int grid = grid_for(c, (const void*)fold_range_kernel<HB, IN>, 256, 0, work);      \
-    fold_range_kernel<HB, IN><<<grid, 256, 0, c.stream>>>(p, ta, tb, init, acc, total, pd);  \
+    launch_k(c, fold_range_kernel<HB, IN>, grid, 256, 0, p, ta, tb, init, acc, total, pd);  \
   }
   if (tb) {
     if (init) TT_FR(true, true) else TT_FR(true, false)
@@ -488,7 +573,7 @@ void launch_batch_affine(const LaunchCtx& c, const double* in, int64_t s, int64_
     const uint64_t blocks = static_cast<uint64_t>((n_out + block - 1) / block);
     const uint64_t items = blocks * static_cast<uint64_t>(s / 512);
     const int grid = grid_for(c, (const void*)batch_affine_smem_kernel, 256, 0, static_cast<int64_t>(items));
-    batch_affine_smem_kernel<<<grid, 256, 0, c.stream>>>(in, s, n_out, block, items, row_ptr, src, w,
+    launch_k(c, batch_affine_smem_kernel, grid, 256, 0, in, s, n_out, block, items, row_ptr, src, w,
                                                          bias, out, make_div64(static_cast<uint64_t>(s / 512)));
     post_launch(c, "batch affine smem kernel");
     return;
@@ -501,18 +586,18 @@ void launch_batch_affine(const LaunchCtx& c, const double* in, int64_t s, int64_
     const int64_t nb = static_cast<int64_t>((work + 255) / 256);
     if (pair) {
       const int grid = grid_for(c, (const void*)batch_affine_blocked_kernel<8, 2>, 256, 0, nb);
-      batch_affine_blocked_kernel<8, 2><<<grid, 256, 0, c.stream>>>(in, s, n_out, block, work, row_ptr,
+      launch_k(c, batch_affine_blocked_kernel<8, 2>, grid, 256, 0, in, s, n_out, block, work, row_ptr,
                                                                     src, w, bias, out, make_div64(per));
     } else {
       const int grid = grid_for(c, (const void*)batch_affine_blocked_kernel<8, 1>, 256, 0, nb);
-      batch_affine_blocked_kernel<8, 1><<<grid, 256, 0, c.stream>>>(in, s, n_out, block, work, row_ptr,
+      launch_k(c, batch_affine_blocked_kernel<8, 1>, grid, 256, 0, in, s, n_out, block, work, row_ptr,
                                                                     src, w, bias, out, make_div64(per));
     }
     post_launch(c, "batch affine blocked kernel");
     return;
   }
   const int grid = grid_for(c, (const void*)batch_affine_kernel, 256, 0, (total + 255) / 256);
-  batch_affine_kernel<<<grid, 256, 0, c.stream>>>(in, s, total, row_ptr, src, w, bias, out,
+  launch_k(c, batch_affine_kernel, grid, 256, 0, in, s, total, row_ptr, src, w, bias, out,
                                                    make_div64(static_cast<uint64_t>(s)));
   post_launch(c, "batch affine kernel");
 }
@@ -523,10 +608,10 @@ void launch_binary_flat(const LaunchCtx& c, int op, const double* a, const doubl
   const int64_t work = (count + 255) / 256;
   if (op == TT_OP_ADD) {
     const int grid = grid_for(c, (const void*)binary_flat_kernel<TT_OP_ADD>, 256, 0, work);
-    binary_flat_kernel<TT_OP_ADD><<<grid, 256, 0, c.stream>>>(a, b, out, count);
+    launch_k(c, binary_flat_kernel<TT_OP_ADD>, grid, 256, 0, a, b, out, count);
   } else {
     const int grid = grid_for(c, (const void*)binary_flat_kernel<TT_OP_MUL>, 256, 0, work);
-    binary_flat_kernel<TT_OP_MUL><<<grid, 256, 0, c.stream>>>(a, b, out, count);
+    launch_k(c, binary_flat_kernel<TT_OP_MUL>, grid, 256, 0, a, b, out, count);
   }
   post_launch(c, "binary kernel");
 }
@@ -540,7 +625,7 @@ void launch_rotate(const LaunchCtx& c, const double* in, double* out, int64_t s,
     const uint64_t units = per_tile * static_cast<uint64_t>(n_tiles);
     const int64_t work = static_cast<int64_t>((units + 7) / 8);
     const int grid = grid_for(c, (const void*)rotate_aligned_kernel<16>, 256, 0, work);
-    rotate_aligned_kernel<16><<<grid, 256, 0, c.stream>>>(in, out, s, r, units, make_div64(per_tile));
+    launch_k(c, rotate_aligned_kernel<16>, grid, 256, 0, in, out, s, r, units, make_div64(per_tile));
     post_launch(c, "rotate aligned kernel");
     return;
   }
@@ -548,12 +633,12 @@ void launch_rotate(const LaunchCtx& c, const double* in, double* out, int64_t s,
   const uint64_t items = chunks * static_cast<uint64_t>(n_tiles);
   if (s >= 1024) {  // chunked: whole 4096-slot items (small tiles keep one slot per thread)
     const int grid = grid_for(c, (const void*)rotate_chunk_kernel, 256, 0, static_cast<int64_t>(items));
-    rotate_chunk_kernel<<<grid, 256, 0, c.stream>>>(in, out, s, r, items, make_div64(chunks));
+    launch_k(c, rotate_chunk_kernel, grid, 256, 0, in, out, s, r, items, make_div64(chunks));
     post_launch(c, "rotate chunk kernel");
     return;
   }
   const int grid = grid_for(c, (const void*)rotate_kernel, 256, 0, (total + 255) / 256);
-  rotate_kernel<<<grid, 256, 0, c.stream>>>(in, out, s, r, total, make_div64(s));
+  launch_k(c, rotate_kernel, grid, 256, 0, in, out, s, r, total, make_div64(s));
   post_launch(c, "rotate kernel");
 }
 
@@ -561,7 +646,7 @@ void launch_fill_uniform(const LaunchCtx& c, double* out, int64_t count, uint64_
                          int64_t offset, double lo, double hi) {
   if (count <= 0) return;
   const int grid = grid_for(c, (const void*)fill_uniform_kernel, 256, 0, (count + 255) / 256);
-  fill_uniform_kernel<<<grid, 256, 0, c.stream>>>(out, count, host_splitmix64(seed), offset, lo,
+  launch_k(c, fill_uniform_kernel, grid, 256, 0, out, count, host_splitmix64(seed), offset, lo,
                                                   hi - lo);
   post_launch(c, "fill kernel");
 }
@@ -620,19 +705,19 @@ void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, con
     const uint64_t units = static_cast<uint64_t>((s / 2 + 127) / 128);
     const int64_t work = (p.g.groups * static_cast<int64_t>(units) + 7) / 8;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, true>, 256, 0, work);
-    fold_kernel<HAS_B, true><<<grid, 256, 0, c.stream>>>(to_fold(p), ta, tb, tout, make_div64(units));
+    launch_k(c, fold_kernel<HAS_B, true>, grid, 256, 0, to_fold(p), ta, tb, tout, make_div64(units));
   } else if ((g_fold_ring == 1 ||
               (g_fold_ring < 0 && p.g.groups * p.ops[0].y * s * 8 > static_cast<int64_t>(c.l2_bytes / 2))) &&
              s % 256 == 0 && p.ops[0].y > 1 && aligned16(ta) && (!HAS_B || aligned16(tb)) &&
              aligned16(tout)) {
     const int64_t runs = s / 256;
     const int grid = grid_for(c, (const void*)fold_ring_kernel<HAS_B>, 128, 0, p.g.groups * runs);
-    fold_ring_kernel<HAS_B><<<grid, 128, 0, c.stream>>>(to_fold(p), ta, tb, tout,
+    launch_k(c, fold_ring_kernel<HAS_B>, grid, 128, 0, to_fold(p), ta, tb, tout,
                                                         make_div64(static_cast<uint64_t>(runs)));
   } else {
     const int64_t work = (p.g.groups * s + 255) / 256;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, false>, 256, 0, work);
-    fold_kernel<HAS_B, false><<<grid, 256, 0, c.stream>>>(to_fold(p), ta, tb, tout,
+    launch_k(c, fold_kernel<HAS_B, false>, grid, 256, 0, to_fold(p), ta, tb, tout,
                                                            make_div64(static_cast<uint64_t>(s)));
   }
   post_launch(c, "fold kernel");
@@ -764,15 +849,15 @@ bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupPar
   constexpr size_t smem = tg_smem_bytes<BC, SL, kTgSteps, kTgStages, PB>();
   constexpr int threads = (tg_warps<BC, SL, SC, PB>() + (WS ? 1 : 0)) * 32;
   set_smem_attr((const void*)k, smem);
-  int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
-  if (g_gemm_grid > 0) grid = std::min(grid, g_gemm_grid);  // measurement knob
   unsigned int* sched = g_gemm_dynamic ? take_sched_slot(c) : nullptr;
+  int grid = grid_for(c, (const void*)k, threads, smem, bs.units, sched != nullptr);
+  if (g_gemm_grid > 0) grid = std::min(grid, g_gemm_grid);  // measurement knob
   if constexpr (WS) {
-    k<<<grid, threads, smem, c.stream>>>(*reinterpret_cast<const CUtensorMap*>(mapA),
+    launch_k(c, k, grid, threads, smem, *reinterpret_cast<const CUtensorMap*>(mapA),
                                          *reinterpret_cast<const CUtensorMap*>(mapB), to_fold(pr), bs, ts,
                                          tout, sched, g_gemm_wait);
   } else {
-    k<<<grid, threads, smem, c.stream>>>(*reinterpret_cast<const CUtensorMap*>(mapA),
+    launch_k(c, k, grid, threads, smem, *reinterpret_cast<const CUtensorMap*>(mapA),
                                          *reinterpret_cast<const CUtensorMap*>(mapB), to_fold(pr), bs, ts,
                                          tout, sched);
   }
@@ -811,7 +896,7 @@ void run_blocked(const LaunchCtx& c, const GroupParams& p, const BlockSpec& bs, 
                  const double* tb, double* tout) {
   auto k = fold_blocked_kernel<HAS_B, P, Q>;
   const int grid = grid_for(c, (const void*)k, kBlockThreads, 0, bs.units);
-  k<<<grid, kBlockThreads, 0, c.stream>>>(to_fold(p), bs, ta, tb, tout);
+  launch_k(c, k, grid, kBlockThreads, 0, to_fold(p), bs, ta, tb, tout);
   post_launch(c, "blocked fold kernel");
 }
 
@@ -874,7 +959,7 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
     set_smem_attr((const void*)k, smem);
     const int threads = Q == 8 ? 128 : 256;
     const int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
-    k<<<grid, threads, smem, c.stream>>>(to_fold(pr), bs, ta, tb, tout);
+    launch_k(c, k, grid, threads, smem, to_fold(pr), bs, ta, tb, tout);
     post_launch(c, coltree ? "gemm fold + column tree kernel (32-slot units)" : "gemm fold kernel (32-slot units)");
   } else if (gemm) {
     const size_t smem =
@@ -886,11 +971,11 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
     const int threads = Q == 16 ? 512 : 256;
     const int grid = grid_for(c, k, threads, smem, bs.units);
     if (coltree)
-      fold_gemm_kernel<16, true><<<grid, threads, smem, c.stream>>>(to_fold(pr), bs, ta, tb, tout);
+      launch_k(c, fold_gemm_kernel<16, true>, grid, threads, smem, to_fold(pr), bs, ta, tb, tout);
     else if (Q == 16)
-      fold_gemm_kernel<16, false><<<grid, threads, smem, c.stream>>>(to_fold(pr), bs, ta, tb, tout);
+      launch_k(c, fold_gemm_kernel<16, false>, grid, threads, smem, to_fold(pr), bs, ta, tb, tout);
     else
-      fold_gemm_kernel<8, false><<<grid, threads, smem, c.stream>>>(to_fold(pr), bs, ta, tb, tout);
+      launch_k(c, fold_gemm_kernel<8, false>, grid, threads, smem, to_fold(pr), bs, ta, tb, tout);
     post_launch(c, coltree ? "gemm fold + column tree kernel" : "gemm fold kernel");
   } else if (P == 8 && Q == 8)
     run_blocked<HAS_B, 8, 8>(c, pr, bs, ta, tb, tout);
@@ -926,7 +1011,7 @@ void run_pow2(const LaunchCtx& c, const GroupParams& p, int threads, size_t smem
   auto k = group_pow2_kernel<VMAX, HAS_B, VEC>;
   set_smem_attr((const void*)k, smem);
   const int grid = grid_for(c, (const void*)k, threads, smem, p.g.groups);
-  k<<<grid, threads, smem, c.stream>>>(p, ta, tb, tout);
+  launch_k(c, k, grid, threads, smem, p, ta, tb, tout);
   post_launch(c, "group pow2 kernel");
 }
 
@@ -957,7 +1042,7 @@ void run_tma(const LaunchCtx& c, const GroupParams& p, const double* ta, const d
   auto k = group_tma_kernel<VMAX, HAS_B>;
   set_smem_attr((const void*)k, smem);
   const int grid = grid_for(c, (const void*)k, kTmaThreads, smem, p.g.groups);
-  k<<<grid, kTmaThreads, smem, c.stream>>>(p, ta, tb, tout, nstages);
+  launch_k(c, k, grid, kTmaThreads, smem, p, ta, tb, tout, nstages);
   post_launch(c, "group tma kernel");
 }
 
@@ -974,7 +1059,7 @@ void run_tma_win(const LaunchCtx& c, const GroupParams& p, int halo, const doubl
   auto k = group_tma_win_kernel<HAS_B>;
   set_smem_attr((const void*)k, smem);
   const int grid = grid_for(c, (const void*)k, kTmaThreads, smem, p.g.groups);
-  k<<<grid, kTmaThreads, smem, c.stream>>>(p, ta, tb, tout, nstages, halo);
+  launch_k(c, k, grid, kTmaThreads, smem, p, ta, tb, tout, nstages, halo);
   post_launch(c, "group tma window kernel");
 }
 
@@ -1010,6 +1095,14 @@ const int g_tree_smem = [] {
 // flight), so off (1) by default
 const int g_row_chain = [] {
   const char* e = std::getenv("TT_ROW_CHAIN");
+  return e ? std::atoi(e) : 0;
+}();
+
+// TT_TREE_TMA = 1 / 2: tree-only passes of GEMM-shaped products on the TMA
+// group kernels (1: sliding-window ring when the reach fits one chunk, 2:
+// whole tile in shared memory) instead of the register column / row passes
+const int g_tree_tma = [] {
+  const char* e = std::getenv("TT_TREE_TMA");
   return e ? std::atoi(e) : 0;
 }();
 
@@ -1086,9 +1179,9 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
     const int grid = grid_for(c, k, kTreeThreads, smem, n_tiles);
     const int4 lv0 = make_int4(lv[0], lv[1], lv[2], lv[3]), lv1 = make_int4(lv[4], lv[5], lv[6], lv[7]);
     if (s == 32 * kTreeThreads)
-      smem_tree_kernel<32><<<grid, kTreeThreads, smem, c.stream>>>(tout, n_tiles, p2.nlevels, lv0, lv1);
+      launch_k(c, smem_tree_kernel<32>, grid, kTreeThreads, smem, tout, n_tiles, p2.nlevels, lv0, lv1);
     else
-      smem_tree_kernel<16><<<grid, kTreeThreads, smem, c.stream>>>(tout, n_tiles, p2.nlevels, lv0, lv1);
+      launch_k(c, smem_tree_kernel<16>, grid, kTreeThreads, smem, tout, n_tiles, p2.nlevels, lv0, lv1);
     post_launch(c, "shared-memory tree pass");
     return;
   }
@@ -1100,7 +1193,7 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
 #define TT_COL(TV, BK, EP)                                                                       \
   {                                                                                             \
     const int grid = grid_for(c, (const void*)col_tree_kernel<TV, BK, EP>, 256, 0, work);       \
-    col_tree_kernel<TV, BK, EP><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, stride0, s, cd, ed); \
+    launch_k(c, col_tree_kernel<TV, BK, EP>, grid, 256, 0, folded, tout, n_tiles, stride0, s, cd, ed); \
   }
 #define TT_COL_T(BK, EP)              \
   switch (tp.t) {                     \
@@ -1138,15 +1231,15 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
     const int64_t work = (n_tiles * (s / 32 / 16 / CC) + 7) / 8;
     if (tp.back) {
       const int grid = grid_for(c, (const void*)row_tree_kernel<HR, 16, true, false, CC>, 256, 0, work);
-      row_tree_kernel<HR, 16, true, false, CC><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
+      launch_k(c, row_tree_kernel<HR, 16, true, false, CC>, grid, 256, 0, folded, tout, n_tiles, s, L, lv0,
                                                                             lv1, ed);
     } else if (fuse) {
       const int grid = grid_for(c, (const void*)row_tree_kernel<HR, 16, false, true, CC>, 256, 0, work);
-      row_tree_kernel<HR, 16, false, true, CC><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
+      launch_k(c, row_tree_kernel<HR, 16, false, true, CC>, grid, 256, 0, folded, tout, n_tiles, s, L, lv0,
                                                                             lv1, ed);
     } else {
       const int grid = grid_for(c, (const void*)row_tree_kernel<HR, 16, false, false, CC>, 256, 0, work);
-      row_tree_kernel<HR, 16, false, false, CC><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
+      launch_k(c, row_tree_kernel<HR, 16, false, false, CC>, grid, 256, 0, folded, tout, n_tiles, s, L, lv0,
                                                                              lv1, ed);
     }
   };
@@ -1165,14 +1258,14 @@ void run_tree_pass(const LaunchCtx& c, const TreePass& tp, const GroupParams& p2
     if (tp.back) {
       if (fuse) invalid_argument("tree epilogue: mirrored passes take none");
       const int grid = grid_for(c, (const void*)row_tree_kernel<HR, RR, true>, 256, 0, work);
-      row_tree_kernel<HR, RR, true><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1, ed);
+      launch_k(c, row_tree_kernel<HR, RR, true>, grid, 256, 0, folded, tout, n_tiles, s, L, lv0, lv1, ed);
     } else if (fuse) {
       const int grid = grid_for(c, (const void*)row_tree_kernel<HR, RR, false, true>, 256, 0, work);
-      row_tree_kernel<HR, RR, false, true><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0,
+      launch_k(c, row_tree_kernel<HR, RR, false, true>, grid, 256, 0, folded, tout, n_tiles, s, L, lv0,
                                                                        lv1, ed);
     } else {
       const int grid = grid_for(c, (const void*)row_tree_kernel<HR, RR, false>, 256, 0, work);
-      row_tree_kernel<HR, RR, false><<<grid, 256, 0, c.stream>>>(folded, tout, n_tiles, s, L, lv0, lv1, ed);
+      launch_k(c, row_tree_kernel<HR, RR, false>, grid, 256, 0, folded, tout, n_tiles, s, L, lv0, lv1, ed);
     }
   };
   using I1 = std::integral_constant<int, 1>;
@@ -1379,6 +1472,27 @@ bool launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
         launch_fold_blocked<HAS_B>(c, p, bplan, ta, tb, tout, true);
         return false;
       }
+      int64_t reach = 0;
+      for (int i = 0; i < p.nlevels; ++i) reach += p.rots[i];
+      const bool tree_tma = g_tree_tma && tma_ok && (tpass.kind == 1 || tpass.kind == 2) && !tpass.back &&
+                            (epi == nullptr || !epi->active()) && aligned16(fold_dst);
+      if (tree_tma) {
+        launch_fold_best<HAS_B>(c, p, ta, tb, fold_dst);
+        GroupParams p2 = p;
+        for (int i = 0; i < g.nd; ++i) {
+          p2.g.a_stride[i] = g.out_stride[i];
+          p2.g.b_stride[i] = 0;
+        }
+        p2.g.astep = 0;
+        p2.g.bstep = 0;
+        p2.ops[0].x = 0;
+        p2.ops[0].y = 1;
+        if (reach <= kTmaChunk && g_tree_tma == 1)
+          run_tma_win<false>(c, p2, static_cast<int>(reach), fold_dst, nullptr, tout);
+        else
+          dispatch_tma<false>(c, p2, fold_dst, nullptr, tout);
+        return false;
+      }
       if (tpass.kind != 0) {
         launch_fold_best<HAS_B>(c, p, ta, tb, fold_dst);
         const bool fuse_epi = tpass.kind == 1 || tpass.kind == 2;
@@ -1434,7 +1548,7 @@ bool launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
   }
   const int grid = grid_for(c, (const void*)k, gthreads, smem, g.groups);
   if (!p.use_smem) scratch = c.scratch(c.scratch_owner, phys * static_cast<size_t>(grid));
-  k<<<grid, gthreads, smem, c.stream>>>(p, ta, tb, tout, scratch);
+  launch_k(c, k, grid, gthreads, smem, p, ta, tb, tout, scratch);
   post_launch(c, "group generic kernel");
   return false;
 }
@@ -1518,7 +1632,7 @@ bool launch_chain(const LaunchCtx& c, const ChainStep* steps, int n, int64_t s) 
   const size_t smem = static_cast<size_t>(kChNS) * kChStage * sizeof(double) + 3 * kChNS * 8;
   set_smem_attr((const void*)chain_kernel, smem);
   const int grid = grid_for(c, (const void*)chain_kernel, kChThreads, smem,
-                            d.ph[0].nf + (n > 1 ? d.ph[1].nf : 0));
+                            d.ph[0].nf + (n > 1 ? d.ph[1].nf : 0), true);
   const CUtensorMap* m0a = reinterpret_cast<const CUtensorMap*>(cp[0].mapA);
   const CUtensorMap* m0b = reinterpret_cast<const CUtensorMap*>(cp[0].mapB);
   const CUtensorMap* m1a = reinterpret_cast<const CUtensorMap*>(n > 1 ? cp[1].mapA : cp[0].mapA);
@@ -1545,10 +1659,10 @@ void launch_epilogue(const LaunchCtx& c, const Epilogue& e, int64_t s, double* t
   const int64_t work = (n_tiles * per + 255) / 256;
   if (vec) {
     const int grid = grid_for(c, (const void*)epilogue_kernel<true>, 256, 0, work);
-    epilogue_kernel<true><<<grid, 256, 0, c.stream>>>(tiles, n_tiles, s, make_div64(static_cast<uint64_t>(per)), ed);
+    launch_k(c, epilogue_kernel<true>, grid, 256, 0, tiles, n_tiles, s, make_div64(static_cast<uint64_t>(per)), ed);
   } else {
     const int grid = grid_for(c, (const void*)epilogue_kernel<false>, 256, 0, work);
-    epilogue_kernel<false><<<grid, 256, 0, c.stream>>>(tiles, n_tiles, s, make_div64(static_cast<uint64_t>(per)), ed);
+    launch_k(c, epilogue_kernel<false>, grid, 256, 0, tiles, n_tiles, s, make_div64(static_cast<uint64_t>(per)), ed);
   }
   post_launch(c, "epilogue kernel");
 }

@@ -23,6 +23,7 @@
 #include <mutex>
 
 #include "tt_launch.hpp"
+#include "tt_pdl.cuh"
 
 namespace ttb {
 
@@ -165,6 +166,7 @@ template <int RK, bool PACK>
 __global__ void __launch_bounds__(32, 1) tma_pack_kernel(const __grid_constant__ CUtensorMap map,
                                                          const __grid_constant__ TmaPackParams pp,
                                                          double* tiles, int nbuf) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char sm[];
   if (threadIdx.x != 0) return;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
@@ -303,11 +305,11 @@ bool launch_tma_copy(const LaunchCtx& c, const Shape& sh, int64_t s, const doubl
   const int64_t grid64 = std::min<int64_t>(tp.pp.n_items, static_cast<int64_t>(c.sm_count) * std::max(per_sm, 1));
   const int grid = static_cast<int>(std::max<int64_t>(grid64, 1));
   switch (tp.pp.rank) {
-    case 1: tma_pack_kernel<1, PACK><<<grid, 32, tp.smem, c.stream>>>(tp.map, tp.pp, tiles, tp.nbuf); break;
-    case 2: tma_pack_kernel<2, PACK><<<grid, 32, tp.smem, c.stream>>>(tp.map, tp.pp, tiles, tp.nbuf); break;
-    case 3: tma_pack_kernel<3, PACK><<<grid, 32, tp.smem, c.stream>>>(tp.map, tp.pp, tiles, tp.nbuf); break;
-    case 4: tma_pack_kernel<4, PACK><<<grid, 32, tp.smem, c.stream>>>(tp.map, tp.pp, tiles, tp.nbuf); break;
-    default: tma_pack_kernel<5, PACK><<<grid, 32, tp.smem, c.stream>>>(tp.map, tp.pp, tiles, tp.nbuf); break;
+    case 1: launch_k(c, tma_pack_kernel<1, PACK>, grid, 32, tp.smem, tp.map, tp.pp, tiles, tp.nbuf); break;
+    case 2: launch_k(c, tma_pack_kernel<2, PACK>, grid, 32, tp.smem, tp.map, tp.pp, tiles, tp.nbuf); break;
+    case 3: launch_k(c, tma_pack_kernel<3, PACK>, grid, 32, tp.smem, tp.map, tp.pp, tiles, tp.nbuf); break;
+    case 4: launch_k(c, tma_pack_kernel<4, PACK>, grid, 32, tp.smem, tp.map, tp.pp, tiles, tp.nbuf); break;
+    default: launch_k(c, tma_pack_kernel<5, PACK>, grid, 32, tp.smem, tp.map, tp.pp, tiles, tp.nbuf); break;
   }
   if (c.launches) ++*c.launches;
   check_cuda(cudaGetLastError(), PACK ? "tma pack kernel" : "tma unpack kernel");

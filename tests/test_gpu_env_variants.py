@@ -1,7 +1,7 @@
 """GPU parity of the matmul-path kernel variants selected by environment knobs.
 
 The knobs (TT_GEMM_TMA, TT_GEMM_DYNAMIC, TT_GEMM_CFG, TT_GEMM_BC, TT_GEMM_ORDER,
-TT_TREE_SMEM, TT_ROW_ROWS) are read once when the native library loads, so each variant
+TT_TREE_SMEM, TT_ROW_ROWS, TT_TREE_TMA) are read once when the native library loads, so each variant
 runs in its own subprocess; every one must give the oracle's tiles bit for bit.
 The chain is the reference's matmul_b -> matmul_a (tests/test_linalg.cpp:157-178)
 on 8192-slot 16x32x16 tiles, at a size where both stages take the GEMM fold
@@ -81,6 +81,8 @@ VARIANTS = [
     {"TT_ROW_CHAIN": "4"},
     {"TT_ROW_ROWS": "32"},
     {"TT_ROW_ROWS": "64"},
+    {"TT_TREE_TMA": "1"},
+    {"TT_TREE_TMA": "2"},
 ]
 
 
