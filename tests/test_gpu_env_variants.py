@@ -83,6 +83,8 @@ VARIANTS = [
     {"TT_ROW_ROWS": "64"},
     {"TT_TREE_TMA": "1"},
     {"TT_TREE_TMA": "2"},
+    {"TT_PDL": "0"},
+    {"TT_PDL_OVERSUB": "1"},
 ]
 
 
