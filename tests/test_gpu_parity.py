@@ -740,3 +740,26 @@ def test_interleaved_kats_on_gpu(gpu):
     assert r.tiles().tolist() == [[36.0, 36.0, 36.0, 36.0]]
     c = S.cost_report()
     assert (c.additions, c.rotations) == (3, 2)
+
+
+@pytest.mark.parametrize("case", [
+    # (a shape, b shape): b broadcast along dims 1 (and 3), a broadcast along dim 2;
+    # > 64 MiB of output, so the L2-hinted broadcast kernel runs;
+    # the broadcast operand on either side, one or two broadcast dims
+    ("[640/16,64/32,256/32]", "[*/16,64/32,256/32]"),
+    ("[*/16,640/32,256/32]", "[64/16,640/32,256/32]"),
+    ("[96/16,64/32,1504/32]", "[*/16,64/32,*/32]"),
+])
+@pytest.mark.parametrize("op", [tt.OpKind.add, tt.OpKind.mul], ids=["add", "mul"])
+def test_broadcast_elementwise_large(gpu, oracle, case, op):
+    s = 16 * 32 * 32
+    S = session(s)
+    sa, sb = parse_shape(case[0]), parse_shape(case[1])
+    nrng = np.random.default_rng(11 + int(op))
+    ta = nrng.uniform(-3, 3, size=(sa.tile_count(), s))
+    tb = nrng.uniform(-3, 3, size=(sb.tile_count(), s))
+    got = tt.tt_elementwise(TileTensor(sa, ta, S), TileTensor(sb, tb, S), op)
+    ws, wt, _ = oracle.elementwise(int(op), sa, ta, sb, tb, s)
+    assert got.shape() == ws
+    assert got.tiles().nbytes > (64 << 20)
+    assert_bitwise(got.tiles(), wt, f"ew {case}")
