@@ -163,7 +163,7 @@ class _CDim(ctypes.Structure):  # tt_dim, include/tiletensor_b200.h
 
 
 class _CShape(ctypes.Structure):  # tt_shape
-    _fields_ = [("rank", ctypes.c_int32), ("relaxed", ctypes.c_int32), ("dims", _CDim * 8)]
+    _fields_ = [("rank", ctypes.c_int32), ("relaxed", ctypes.c_int32), ("dims", _CDim * 16)]  # TT_MAX_RANK
 
 
 def _cshape(dims):

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define TT_MAX_RANK 8
+#define TT_MAX_RANK 16
 
 /* Status codes; map 1:1 onto the reference's exception types. */
 typedef enum tt_status {

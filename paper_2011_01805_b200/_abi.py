@@ -9,7 +9,7 @@ from __future__ import annotations
 import ctypes
 from pathlib import Path
 
-TT_MAX_RANK = 8
+TT_MAX_RANK = 16  # include/tiletensor_b200.h
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libtiletensor_b200.so"
 
 

@@ -763,3 +763,27 @@ def test_broadcast_elementwise_large(gpu, oracle, case, op):
     assert got.shape() == ws
     assert got.tiles().nbytes > (64 << 20)
     assert_bitwise(got.tiles(), wt, f"ew {case}")
+
+
+def test_high_rank_pack_sum_unpack(gpu, oracle):
+    # rank 12 (TT_MAX_RANK = 16; the reference has no limit): pack, fused
+    # multiply + sum over a middle dim, elementwise with a broadcast, unpack
+    s = 4096
+    S = session(s)
+    sh = parse_shape("[" + ",".join(["3/2"] * 12) + "]")
+    nrng = np.random.default_rng(1212)
+    dense = nrng.uniform(-1, 1, size=(3,) * 12)
+    T = tt.pack(dense, sh, S)
+    assert_bitwise(T.tiles(), oracle.pack(dense, sh, s), "rank-12 pack")
+    assert_bitwise(tt.unpack(T), dense, "rank-12 unpack")
+    for dim in (1, 7, 12):
+        got = tt.tt_mul_sum(T, T, dim)
+        ws, wt, _ = oracle.mul_sum(sh, T.tiles(), sh, T.tiles(), s, dim)
+        assert got.shape() == ws
+        assert_bitwise(got.tiles(), wt, f"rank-12 mul_sum dim {dim}")
+    sb = parse_shape("[" + ",".join(["3/2"] * 5 + ["*/2"] + ["3/2"] * 6) + "]")
+    tb = nrng.uniform(-1, 1, size=(sb.tile_count(), s))
+    got = tt.tt_elementwise(T, TileTensor(sb, tb, S), tt.OpKind.mul)
+    ws, wt, _ = oracle.elementwise(int(tt.OpKind.mul), sh, T.tiles(), sb, tb, s)
+    assert got.shape() == ws
+    assert_bitwise(got.tiles(), wt, "rank-12 broadcast mul")

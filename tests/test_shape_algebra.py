@@ -252,3 +252,20 @@ def test_interleaved_sum_kat(oracle):
     assert format_shape(so) == "[*/4]"
     assert out.tolist() == [[36.0, 36.0, 36.0, 36.0]]
     assert (cost.additions, cost.rotations) == (1 + 2, 2)
+
+
+def test_high_rank_shapes(oracle):
+    # the reference has no rank limit; this build holds up to TT_MAX_RANK (16) dims
+    from paper_2011_01805_b200._abi import TT_MAX_RANK
+    assert TT_MAX_RANK == 16
+    text = "[" + ",".join(["3/2"] * 12) + "]"
+    sh = parse_shape(text)
+    assert sh.rank() == 12 and format_shape(sh) == text
+    assert sh.tile_count() == 2 ** 12
+    r = tt.sum_result_shape(tt.elementwise_result_shape(sh, sh, OpKind.mul), 7)
+    assert format_shape(r) == "[" + ",".join(["3/2"] * 6 + ["1?/2"] + ["3/2"] * 5) + "]"
+    dense = np.arange(3 ** 12, dtype=np.float64).reshape((3,) * 12)
+    want = oracle.pack(dense, sh, 4096)
+    assert want.shape == (2 ** 12, 4096)
+    with pytest.raises(ShapeError):
+        parse_shape("[" + ",".join(["2"] * 17) + "]")
