@@ -7,9 +7,11 @@
 // A TileTensor keeps its tiles as ONE contiguous device array
 // [tile_count][s] (the concatenation of the reference's tiles()[i].slots()).
 // tiles() hands out a host mirror std::vector<Tile> built on demand; the
-// mutable overload marks the mirror authoritative, and the next operator
-// that reads the tensor uploads it first -- so code that edits slots in
-// place (the reference's fuzzing tests do) keeps the reference semantics.
+// mutable overload marks the mirror authoritative from then on: every later
+// operator that reads the tensor uploads it first -- so code that edits slots
+// in place (the reference's fuzzing tests do), including through a reference
+// to tiles() kept across operator calls, keeps the reference semantics.  A
+// tensor whose tiles were never handed out mutably is never re-uploaded.
 
 #include <cstdint>
 #include <memory>
@@ -75,12 +77,15 @@ class TileTensor {
   const std::vector<Tile>& tiles() const { return mirror(); }
   std::vector<Tile>& tiles() {
     auto& m = mirror();
-    host_dirty_ = true;  // caller may edit slots in place
+    // the caller may edit slots in place -- now or through the returned
+    // reference at any later time -- so the mirror stays authoritative
+    host_dirty_ = true;
+    exposed_ = true;
     return m;
   }
   const Tile& tile_at(std::size_t flat) const { return mirror().at(flat); }
   std::int64_t chain_index() const {
-    if (host_dirty_ && mirror_) {
+    if ((host_dirty_ || exposed_) && mirror_) {
       std::int64_t c = session_->max_chain_index();
       for (const auto& t : *mirror_) c = std::min(c, t.chain_index());
       return c;
@@ -116,7 +121,7 @@ class TileTensor {
     return out;
   }
   void sync_to_device() const {
-    if (dev_ && !host_dirty_) return;
+    if (dev_ && !host_dirty_ && !exposed_) return;
     const std::int64_t s = session_->slot_count();
     const std::int64_t n = shape_.tile_count() * s;
     if (!dev_) dev_ = std::make_shared<DeviceArray>(session_->handle(), std::max<std::int64_t>(n, 1));
@@ -140,6 +145,7 @@ class TileTensor {
   mutable std::shared_ptr<std::vector<Tile>> mirror_;
   mutable std::int64_t chain_ = 0;
   mutable bool host_dirty_ = false;
+  bool exposed_ = false;  // tiles() was handed out mutably: re-upload before every read
 };
 
 namespace detail {

@@ -654,6 +654,21 @@ static void nn_suite() {
   }
 }
 
+// A reference to tiles() kept across operator calls: every later edit through it
+// is seen by the next operator, as with the reference's host-resident tiles.
+static void held_tiles_suite() {
+  Session session(4, 8);
+  TileTensor t = pack(DenseTensor({2, 2}, {1, 2, 3, 4}), parse_shape("[2/2,2/2]"), session);
+  auto& held = t.tiles();
+  held[0].slots()[0] = 10.0;  // tile = {10, 2, 3, 4}
+  CHECK(tt_sum(t, 2).tiles()[0].slots()[0] == 12.0);
+  held[0].slots()[1] = 20.0;  // edited again after an operator read the tensor
+  CHECK(tt_sum(t, 2).tiles()[0].slots()[0] == 30.0);
+  CHECK(tt_add(t, t).tiles()[0].slots()[1] == 40.0);
+  held[0].slots()[3] = -4.0;
+  CHECK(tt_mul(t, t).tiles()[0].slots()[3] == 16.0);
+}
+
 // packed tile file (tools/tiletensor_main.cpp:76-128): text and bit-exact round trip
 static void formats_suite() {
   Session session(4, 8);
@@ -682,7 +697,7 @@ static void formats_suite() {
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> suites = {
       {"shapes", shapes}, {"backend", backend}, {"rotate_sum", rotate_sum},
-      {"tile_tensor", tile_tensor}, {"linalg", linalg}, {"pipeline", pipeline_suite}, {"nn", nn_suite}, {"formats", formats_suite}};
+      {"tile_tensor", tile_tensor}, {"linalg", linalg}, {"pipeline", pipeline_suite}, {"nn", nn_suite}, {"held_tiles", held_tiles_suite}, {"formats", formats_suite}};
   for (const auto& [name, fn] : suites) {
     const int before = g_failed;
     try {
