@@ -1106,10 +1106,12 @@ const int g_tree_tma = [] {
   return e ? std::atoi(e) : 0;
 }();
 
-// rows per warp of the wide-halo row tree (TT_ROW_ROWS = 16 / 32 / 64)
+// rows per warp of the wide-halo row tree (TT_ROW_ROWS = 16 / 32 / 64): 32
+// reads each row 1.5x instead of 2x (config 3 row tree 12.8 -> 11.6 us,
+// literal chain 219 -> 210 us, measured with PDL); 64 spills
 const int g_row_rows = [] {
   const char* e = std::getenv("TT_ROW_ROWS");
-  return e ? std::atoi(e) : 16;
+  return e ? std::atoi(e) : 32;
 }();
 
 struct TreePass {

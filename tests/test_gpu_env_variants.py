@@ -79,7 +79,7 @@ VARIANTS = [
     {"TT_FOLD_RING": "0"},
     {"TT_ROW_CHAIN": "2"},
     {"TT_ROW_CHAIN": "4"},
-    {"TT_ROW_ROWS": "32"},
+    {"TT_ROW_ROWS": "16"},
     {"TT_ROW_ROWS": "64"},
     {"TT_TREE_TMA": "1"},
     {"TT_TREE_TMA": "2"},
