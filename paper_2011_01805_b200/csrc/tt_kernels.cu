@@ -157,7 +157,7 @@ int grid_for(const LaunchCtx& c, const void* kernel, int threads, size_t smem, i
   // Under PDL a grid is dispatched while its predecessor still holds most SMs:
   // the SMs that free up first would take all of a one-wave persistent grid's
   // CTAs.  Several waves' worth of CTAs keep the grid-stride loops balanced.
-  const int64_t waves = per_sm > 1 && !one_wave && pdl_would_allow(c, kernel, smem) ? pdl_oversub() : 1;
+  const int64_t waves = per_sm > 1 && !one_wave && pdl_would_allow(c, kernel, threads, smem) ? pdl_oversub() : 1;
   const int64_t cap = static_cast<int64_t>(c.sm_count) * per_sm * waves;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cap, work)));
 }
@@ -175,8 +175,10 @@ std::mutex g_pdl_mu;
 std::map<cudaStream_t, size_t> g_pdl_last;  // per-SM smem of each stream's last launch
 
 // per-CTA shared memory (dynamic + static) and resident CTAs per SM
-std::pair<size_t, size_t> smem_footprint(const LaunchCtx& c, const void* kernel, size_t dyn_smem) {
-  size_t cta = dyn_smem, per_sm = 1;
+// per-CTA shared memory (dynamic + static) and resident CTAs per SM, cached
+// per (device, kernel, block size, dynamic smem) like grid_for's occupancy
+std::pair<size_t, size_t> smem_footprint(const LaunchCtx& c, const void* kernel, int threads,
+                                         size_t dyn_smem) {
   std::lock_guard<std::mutex> lk(g_launch_cache_mu);
   auto it = g_static_smem.find(kernel);
   if (it == g_static_smem.end()) {
@@ -184,11 +186,15 @@ std::pair<size_t, size_t> smem_footprint(const LaunchCtx& c, const void* kernel,
     if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) fa.sharedSizeBytes = 0;
     it = g_static_smem.emplace(kernel, fa.sharedSizeBytes).first;
   }
-  cta += it->second;
-  for (const auto& [key, occ] : g_occupancy)
-    if (key.kernel == kernel && key.device == c.device && key.smem == dyn_smem)
-      per_sm = std::max(per_sm, static_cast<size_t>(occ));
-  return {cta, per_sm};
+  const OccKey key{c.device, kernel, threads, dyn_smem};
+  auto oc = g_occupancy.find(key);
+  if (oc == g_occupancy.end()) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn_smem) != cudaSuccess)
+      per_sm = 1;
+    oc = g_occupancy.emplace(key, per_sm).first;
+  }
+  return {dyn_smem + it->second, static_cast<size_t>(std::max(1, oc->second))};
 }
 
 bool pdl_rule(size_t prev_per_sm, size_t cta) {
@@ -197,9 +203,9 @@ bool pdl_rule(size_t prev_per_sm, size_t cta) {
 }  // namespace
 
 // peek: would a launch of `kernel` on c.stream get the PDL attribute now?
-bool pdl_would_allow(const LaunchCtx& c, const void* kernel, size_t dyn_smem) {
+bool pdl_would_allow(const LaunchCtx& c, const void* kernel, int threads, size_t dyn_smem) {
   if (!pdl_enabled()) return false;
-  const size_t cta = smem_footprint(c, kernel, dyn_smem).first;
+  const size_t cta = smem_footprint(c, kernel, threads, dyn_smem).first;
   std::lock_guard<std::mutex> lk(g_pdl_mu);
   auto it = g_pdl_last.find(c.stream);
   return pdl_rule(it == g_pdl_last.end() ? 0 : it->second, cta);
@@ -208,9 +214,9 @@ bool pdl_would_allow(const LaunchCtx& c, const void* kernel, size_t dyn_smem) {
 // A grid smaller than one full wave is launched without the attribute too:
 // dispatched early it would be packed onto the first SMs to free up (config 4's
 // 512-CTA layer-2 fold on ~70 SMs: 22 -> 28 us) instead of spread over all.
-bool pdl_allow(const LaunchCtx& c, const void* kernel, size_t dyn_smem, int64_t grid) {
+bool pdl_allow(const LaunchCtx& c, const void* kernel, int threads, size_t dyn_smem, int64_t grid) {
   if (!pdl_enabled()) return false;
-  const auto [cta, per_sm] = smem_footprint(c, kernel, dyn_smem);
+  const auto [cta, per_sm] = smem_footprint(c, kernel, threads, dyn_smem);
   std::lock_guard<std::mutex> lk(g_pdl_mu);
   if (g_pdl_last.size() > 4096) g_pdl_last.clear();  // streams come and go; a forgotten one costs one overlap
   size_t& prev = g_pdl_last[c.stream];

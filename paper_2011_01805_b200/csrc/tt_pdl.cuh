@@ -33,8 +33,8 @@ int pdl_enabled();
 int pdl_oversub();
 // Whether this launch may overlap its predecessor on the stream, and record
 // its footprint for the next launch (see tt_kernels.cu).
-bool pdl_allow(const LaunchCtx& c, const void* kernel, size_t dyn_smem, int64_t grid);
-bool pdl_would_allow(const LaunchCtx& c, const void* kernel, size_t dyn_smem);
+bool pdl_allow(const LaunchCtx& c, const void* kernel, int threads, size_t dyn_smem, int64_t grid);
+bool pdl_would_allow(const LaunchCtx& c, const void* kernel, int threads, size_t dyn_smem);
 
 // kernel<<<grid, block, smem, c.stream>>>(args...) with the PDL attribute
 template <typename... KArgs, typename... Args>
@@ -49,7 +49,8 @@ inline void launch_k(const LaunchCtx& c, void (*kernel)(KArgs...), dim3 grid, di
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_allow(c, reinterpret_cast<const void*>(kernel), smem,
+  cfg.numAttrs = pdl_allow(c, reinterpret_cast<const void*>(kernel),
+                           static_cast<int>(block.x * block.y * block.z), smem,
                            static_cast<int64_t>(grid.x) * grid.y * grid.z) ? 1 : 0;
   // launch errors surface through cudaGetLastError() in post_launch()
   (void)cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
