@@ -787,3 +787,43 @@ def test_high_rank_pack_sum_unpack(gpu, oracle):
     ws, wt, _ = oracle.elementwise(int(tt.OpKind.mul), sh, T.tiles(), sb, tb, s)
     assert got.shape() == ws
     assert_bitwise(got.tiles(), wt, "rank-12 broadcast mul")
+
+
+def test_dependent_launch_chain(gpu, oracle):
+    # 300 back-to-back operators, each reading the previous one's result (and
+    # some overwriting a block the one before read): with programmatic dependent
+    # launch every kernel is dispatched while its predecessor drains, so any
+    # early read / early write would show in the bits.  Same chain on the oracle.
+    s = 512
+    S = tt.Session(s, 1000)  # ~200 multiplications deep
+    sh = parse_shape("[40/16,60/32]")
+    nrng = np.random.default_rng(300)
+    x = nrng.uniform(-1, 1, size=(sh.tile_count(), s))
+    y = nrng.uniform(-1, 1, size=(sh.tile_count(), s))
+    c = nrng.uniform(0.4, 0.6, size=(sh.tile_count(), s))   # X <- (X + Y) * c stays bounded
+    d = nrng.uniform(0.9, 1.0, size=(sh.tile_count(), s))
+    X, Y = TileTensor(sh, x, S), TileTensor(sh, y, S)
+    C, D = TileTensor(sh, c, S), TileTensor(sh, d, S)
+    wx, wy = x, y
+    sums = []
+    for i in range(300):
+        if i % 3 == 0:
+            X = tt.tt_elementwise(X, Y, tt.OpKind.add)
+            _, wx, _ = oracle.elementwise(int(tt.OpKind.add), sh, wx, sh, wy, s)
+        elif i % 3 == 1:
+            X = tt.tt_elementwise(X, C, tt.OpKind.mul)
+            _, wx, _ = oracle.elementwise(int(tt.OpKind.mul), sh, wx, sh, c, s)
+        else:
+            Y = tt.tt_elementwise(Y, D, tt.OpKind.mul)
+            _, wy, _ = oracle.elementwise(int(tt.OpKind.mul), sh, wy, sh, d, s)
+            Y = tt.tt_elementwise(Y, X, tt.OpKind.add)
+            _, wy, _ = oracle.elementwise(int(tt.OpKind.add), sh, wy, sh, wx, s)
+            Y = tt.tt_elementwise(Y, C, tt.OpKind.mul)
+            _, wy, _ = oracle.elementwise(int(tt.OpKind.mul), sh, wy, sh, c, s)
+        if i % 25 == 24:  # a reduction in the chain
+            sums.append((tt.tt_sum(X, 2), oracle.sum(sh, wx, s, 2)[1]))
+    assert np.isfinite(wx).all() and np.isfinite(wy).all()
+    assert_bitwise(X.tiles(), wx, "dependent chain X")
+    assert_bitwise(Y.tiles(), wy, "dependent chain Y")
+    for k, (got, want) in enumerate(sums):
+        assert_bitwise(got.tiles(), want, f"dependent chain sum {k}")
