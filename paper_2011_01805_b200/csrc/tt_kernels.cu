@@ -174,7 +174,6 @@ namespace {
 std::mutex g_pdl_mu;
 std::map<cudaStream_t, size_t> g_pdl_last;  // per-SM smem of each stream's last launch
 
-// per-CTA shared memory (dynamic + static) and resident CTAs per SM
 // per-CTA shared memory (dynamic + static) and resident CTAs per SM, cached
 // per (device, kernel, block size, dynamic smem) like grid_for's occupancy
 std::pair<size_t, size_t> smem_footprint(const LaunchCtx& c, const void* kernel, int threads,
