@@ -666,10 +666,15 @@ __global__ void __launch_bounds__((tg_warps<BC, SL, SC, PB>() + 1) * 32, 3)
                         const __grid_constant__ CUtensorMap mapB,
                         const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
                         const __grid_constant__ TgSpec ts, double* __restrict__ OUT,
-                        unsigned int* __restrict__ sched, int wait_mode) {
-  pdl_enter();
-  // wait_mode (TT_GEMM_WAIT): 0 = every mbarrier waiter spins on try_wait,
-  // 1 = the producer sleeps on try_wait's suspend hint, 2 = every waiter does
+                        unsigned int* __restrict__ sched, int wait_mode_bits) {
+  // wait_mode (TT_GEMM_WAIT, low 2 bits): 0 = every mbarrier waiter spins on
+  // try_wait, 1 = the producer sleeps on try_wait's suspend hint, 2 = every
+  // waiter does; bit 2: release dependents at entry (else at CTA exit)
+  const int wait_mode = wait_mode_bits & 3;
+  if (wait_mode_bits & 4)
+    pdl_enter();
+  else
+    pdl_wait();
   constexpr int kW = tg_warps<BC, SL, SC, PB>();  // consumer warps
   constexpr int kA = kTgSteps * PB * SL;           // doubles per stage
   constexpr int kB = kTgSteps * BC * SL;

@@ -172,7 +172,13 @@ int grid_for(const LaunchCtx& c, const void* kernel, int threads, size_t smem, i
 // it then starts on drained SMs, which reconfigure their carve-out.
 namespace {
 std::mutex g_pdl_mu;
-std::map<cudaStream_t, size_t> g_pdl_last;  // per-SM smem of each stream's last launch
+// each stream's last launch: its per-SM shared memory and whether it releases
+// its dependents at entry (early) or only at CTA exit
+struct PdlPrev {
+  size_t smem = 0;
+  bool early = false;
+};
+std::map<cudaStream_t, PdlPrev> g_pdl_last;
 
 // per-CTA shared memory (dynamic + static) and resident CTAs per SM, cached
 // per (device, kernel, block size, dynamic smem) like grid_for's occupancy
@@ -201,26 +207,35 @@ bool pdl_rule(size_t prev_per_sm, size_t cta) {
 }
 }  // namespace
 
-// peek: would a launch of `kernel` on c.stream get the PDL attribute now?
+// peek: would a launch of `kernel` on c.stream be dispatched early (PDL
+// attribute, predecessor releasing at entry)?
 bool pdl_would_allow(const LaunchCtx& c, const void* kernel, int threads, size_t dyn_smem) {
   if (!pdl_enabled()) return false;
   const size_t cta = smem_footprint(c, kernel, threads, dyn_smem).first;
   std::lock_guard<std::mutex> lk(g_pdl_mu);
   auto it = g_pdl_last.find(c.stream);
-  return pdl_rule(it == g_pdl_last.end() ? 0 : it->second, cta);
+  const PdlPrev prev = it == g_pdl_last.end() ? PdlPrev{} : it->second;
+  return prev.early && pdl_rule(prev.smem, cta);
 }
 
 // A grid smaller than one full wave is launched without the attribute too:
 // dispatched early it would be packed onto the first SMs to free up (config 4's
 // 512-CTA layer-2 fold on ~70 SMs: 22 -> 28 us) instead of spread over all.
+void pdl_note_late_release(const LaunchCtx& c) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  g_pdl_last[c.stream] = PdlPrev{0, false};  // nothing lands on its SMs early
+}
+
 bool pdl_allow(const LaunchCtx& c, const void* kernel, int threads, size_t dyn_smem, int64_t grid) {
   if (!pdl_enabled()) return false;
   const auto [cta, per_sm] = smem_footprint(c, kernel, threads, dyn_smem);
   std::lock_guard<std::mutex> lk(g_pdl_mu);
   if (g_pdl_last.size() > 4096) g_pdl_last.clear();  // streams come and go; a forgotten one costs one overlap
-  size_t& prev = g_pdl_last[c.stream];
-  const bool allow = pdl_rule(prev, cta) && grid >= static_cast<int64_t>(c.sm_count) * static_cast<int64_t>(per_sm);
-  prev = cta * per_sm;
+  PdlPrev& prev = g_pdl_last[c.stream];
+  // a predecessor that releases only at exit cannot have this grid placed early
+  const bool allow = !prev.early || (pdl_rule(prev.smem, cta) &&
+                                     grid >= static_cast<int64_t>(c.sm_count) * static_cast<int64_t>(per_sm));
+  prev = PdlPrev{cta * per_sm, true};
   return allow;
 }
 
@@ -789,6 +804,16 @@ const int g_gemm_wait = [] {
   return e ? std::atoi(e) : 1;
 }();
 
+// The warp-specialised fold releases its dependents at CTA exit (TT_GEMM_LATE=0:
+// at entry), so the tree pass after it is PDL-launched -- its launch overlaps
+// the fold's end -- without landing early on SMs whose shared-memory carve-out
+// the fold still holds: config 3 chain 92.8 -> 88.1 us through the API (graph
+// replay unchanged), config 4 130 -> 128 us
+const int g_gemm_late = [] {
+  const char* e = std::getenv("TT_GEMM_LATE");
+  return e ? std::atoi(e) : 1;
+}();
+
 // WS: warp-specialised kernel (a producer warp issues the TMA loads)
 template <int SL, int kTgSteps, int kTgStages, int SC, int PB = kGemmBlk, bool WS = false>
 bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupParams& pr,
@@ -860,7 +885,8 @@ bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupPar
   if constexpr (WS) {
     launch_k(c, k, grid, threads, smem, *reinterpret_cast<const CUtensorMap*>(mapA),
                                          *reinterpret_cast<const CUtensorMap*>(mapB), to_fold(pr), bs, ts,
-                                         tout, sched, g_gemm_wait);
+                                         tout, sched, g_gemm_wait | (g_gemm_late ? 0 : 4));
+    if (g_gemm_late) pdl_note_late_release(c);
   } else {
     launch_k(c, k, grid, threads, smem, *reinterpret_cast<const CUtensorMap*>(mapA),
                                          *reinterpret_cast<const CUtensorMap*>(mapB), to_fold(pr), bs, ts,

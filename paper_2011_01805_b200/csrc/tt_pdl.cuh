@@ -29,7 +29,15 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Wait only: the kernel releases its dependents when its CTAs exit (for
+// shared-memory-heavy kernels whose successors should not land on SMs they
+// still hold).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 int pdl_enabled();
+// The stream's last launch releases its dependents only at exit: the next
+// launch may take the attribute whatever its footprint.
+void pdl_note_late_release(const LaunchCtx& c);
 int pdl_oversub();
 // Whether this launch may overlap its predecessor on the stream, and record
 // its footprint for the next launch (see tt_kernels.cu).

@@ -85,6 +85,7 @@ VARIANTS = [
     {"TT_TREE_TMA": "2"},
     {"TT_PDL": "0"},
     {"TT_PDL_OVERSUB": "1"},
+    {"TT_GEMM_LATE": "0"},
 ]
 
 
