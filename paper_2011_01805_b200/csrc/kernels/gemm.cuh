@@ -31,7 +31,7 @@ template <bool HAS_B, int P, int Q>
 __global__ void __launch_bounds__(kBlockThreads) fold_blocked_kernel(
     const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
     const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ OUT) {
-  pdl_enter();
+  pdl_enter(p.late != 0);
   const int64_t s = p.s;
   const int64_t first = p.first;
   const int64_t count = p.count;
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(128) fold_ring_kernel(const __grid_constant__ 
                                                         const double* __restrict__ A,
                                                         const double* __restrict__ B,
                                                         double* __restrict__ OUT, FastDiv64 runs_div) {
-  pdl_enter();
+  pdl_enter(p.late != 0);
   __shared__ __align__(16) double2 ring[kFoldRing][HAS_B ? 2 : 1][128];
   const int64_t s = p.s;
   const int64_t count = p.count;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__((SLOTS / 32) * (kGemmBlk / kGemmSubR) * (BC / 
     fold_gemm_kernel(const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
                      const double* __restrict__ A, const double* __restrict__ B,
                      double* __restrict__ OUT) {
-  pdl_enter();
+  pdl_enter(p.late != 0);
   constexpr int kHalves = SLOTS / 32;
   constexpr int kThreads = kHalves * (kGemmBlk / kGemmSubR) * (BC / kGemmSubC) * 32;
   constexpr int kSubCols = BC / kGemmSubC;
@@ -469,7 +469,7 @@ __global__ void __maxnreg__(SC == 8 ? 232 : 128)
                          const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
                          const __grid_constant__ TgSpec ts, double* __restrict__ OUT,
                          unsigned int* __restrict__ sched) {
-  pdl_enter();
+  pdl_enter(p.late != 0);
   constexpr int kW = tg_warps<BC, SL, SC, PB>();
   constexpr int kTgRows = 8 / SC;  // rows of products batched before their adds
   constexpr int kA = kTgSteps * PB * SL;  // doubles per stage
@@ -666,15 +666,10 @@ __global__ void __launch_bounds__((tg_warps<BC, SL, SC, PB>() + 1) * 32, 3)
                         const __grid_constant__ CUtensorMap mapB,
                         const __grid_constant__ FoldParams p, const __grid_constant__ BlockSpec bs,
                         const __grid_constant__ TgSpec ts, double* __restrict__ OUT,
-                        unsigned int* __restrict__ sched, int wait_mode_bits) {
-  // wait_mode (TT_GEMM_WAIT, low 2 bits): 0 = every mbarrier waiter spins on
-  // try_wait, 1 = the producer sleeps on try_wait's suspend hint, 2 = every
-  // waiter does; bit 2: release dependents at entry (else at CTA exit)
-  const int wait_mode = wait_mode_bits & 3;
-  if (wait_mode_bits & 4)
-    pdl_enter();
-  else
-    pdl_wait();
+                        unsigned int* __restrict__ sched, int wait_mode) {
+  pdl_enter(p.late != 0);
+  // wait_mode (TT_GEMM_WAIT): 0 = every mbarrier waiter spins on try_wait,
+  // 1 = the producer sleeps on try_wait's suspend hint, 2 = every waiter does
   constexpr int kW = tg_warps<BC, SL, SC, PB>();  // consumer warps
   constexpr int kA = kTgSteps * PB * SL;           // doubles per stage
   constexpr int kB = kTgSteps * BC * SL;

@@ -32,10 +32,12 @@ struct FoldParams {
   int64_t s;
   int64_t first, count;  // FOLD over operand steps [first, first + count)
   int nlevels;           // column-tree fusion: power-of-two levels
+  int late;              // release PDL dependents at CTA exit (a tree pass follows)
 };
 
-FoldParams to_fold(const GroupParams& p) {
+FoldParams to_fold(const GroupParams& p, bool late = false) {
   FoldParams f;
+  f.late = late ? 1 : 0;
   f.g = p.g;
   for (int i = 0; i < R; ++i) f.gdiv[i] = p.gdiv[i];
   f.s = p.s;
@@ -765,7 +767,7 @@ __global__ void __launch_bounds__(256) fold_kernel(const __grid_constant__ FoldP
                                                     const double* __restrict__ B,
                                                     double* __restrict__ OUT,
                                                     FastDiv64 units_div) {
-  pdl_enter();
+  pdl_enter(p.late != 0);
   const int64_t first = p.first;
   const int64_t count = p.count;
   const int64_t s = p.s;

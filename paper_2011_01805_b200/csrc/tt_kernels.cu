@@ -248,6 +248,7 @@ void count_launch(const LaunchCtx& c) {
 void post_launch(const LaunchCtx& c, const char* what) {
   count_launch(c);
   check_cuda(cudaGetLastError(), what);
+  if (c.release_late) pdl_note_late_release(c);
 }
 
 // Device form of an Epilogue (tt_launch.hpp): the add operand's tile for
@@ -725,19 +726,19 @@ void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, con
     const uint64_t units = static_cast<uint64_t>((s / 2 + 127) / 128);
     const int64_t work = (p.g.groups * static_cast<int64_t>(units) + 7) / 8;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, true>, 256, 0, work);
-    launch_k(c, fold_kernel<HAS_B, true>, grid, 256, 0, to_fold(p), ta, tb, tout, make_div64(units));
+    launch_k(c, fold_kernel<HAS_B, true>, grid, 256, 0, to_fold(p, c.release_late), ta, tb, tout, make_div64(units));
   } else if ((g_fold_ring == 1 ||
               (g_fold_ring < 0 && p.g.groups * p.ops[0].y * s * 8 > static_cast<int64_t>(c.l2_bytes / 2))) &&
              s % 256 == 0 && p.ops[0].y > 1 && aligned16(ta) && (!HAS_B || aligned16(tb)) &&
              aligned16(tout)) {
     const int64_t runs = s / 256;
     const int grid = grid_for(c, (const void*)fold_ring_kernel<HAS_B>, 128, 0, p.g.groups * runs);
-    launch_k(c, fold_ring_kernel<HAS_B>, grid, 128, 0, to_fold(p), ta, tb, tout,
+    launch_k(c, fold_ring_kernel<HAS_B>, grid, 128, 0, to_fold(p, c.release_late), ta, tb, tout,
                                                         make_div64(static_cast<uint64_t>(runs)));
   } else {
     const int64_t work = (p.g.groups * s + 255) / 256;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, false>, 256, 0, work);
-    launch_k(c, fold_kernel<HAS_B, false>, grid, 256, 0, to_fold(p), ta, tb, tout,
+    launch_k(c, fold_kernel<HAS_B, false>, grid, 256, 0, to_fold(p, c.release_late), ta, tb, tout,
                                                            make_div64(static_cast<uint64_t>(s)));
   }
   post_launch(c, "fold kernel");
@@ -884,12 +885,12 @@ bool launch_gemm_tma_sl(const LaunchCtx& c, const GroupParams& p, const GroupPar
   if (g_gemm_grid > 0) grid = std::min(grid, g_gemm_grid);  // measurement knob
   if constexpr (WS) {
     launch_k(c, k, grid, threads, smem, *reinterpret_cast<const CUtensorMap*>(mapA),
-                                         *reinterpret_cast<const CUtensorMap*>(mapB), to_fold(pr), bs, ts,
-                                         tout, sched, g_gemm_wait | (g_gemm_late ? 0 : 4));
+                                         *reinterpret_cast<const CUtensorMap*>(mapB), to_fold(pr, c.release_late || g_gemm_late != 0), bs, ts,
+                                         tout, sched, g_gemm_wait);
     if (g_gemm_late) pdl_note_late_release(c);
   } else {
     launch_k(c, k, grid, threads, smem, *reinterpret_cast<const CUtensorMap*>(mapA),
-                                         *reinterpret_cast<const CUtensorMap*>(mapB), to_fold(pr), bs, ts,
+                                         *reinterpret_cast<const CUtensorMap*>(mapB), to_fold(pr, c.release_late), bs, ts,
                                          tout, sched);
   }
   post_launch(c, "gemm fold kernel (TMA)");
@@ -927,7 +928,7 @@ void run_blocked(const LaunchCtx& c, const GroupParams& p, const BlockSpec& bs, 
                  const double* tb, double* tout) {
   auto k = fold_blocked_kernel<HAS_B, P, Q>;
   const int grid = grid_for(c, (const void*)k, kBlockThreads, 0, bs.units);
-  launch_k(c, k, grid, kBlockThreads, 0, to_fold(p), bs, ta, tb, tout);
+  launch_k(c, k, grid, kBlockThreads, 0, to_fold(p, c.release_late), bs, ta, tb, tout);
   post_launch(c, "blocked fold kernel");
 }
 
@@ -990,7 +991,7 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
     set_smem_attr((const void*)k, smem);
     const int threads = Q == 8 ? 128 : 256;
     const int grid = grid_for(c, (const void*)k, threads, smem, bs.units);
-    launch_k(c, k, grid, threads, smem, to_fold(pr), bs, ta, tb, tout);
+    launch_k(c, k, grid, threads, smem, to_fold(pr, c.release_late), bs, ta, tb, tout);
     post_launch(c, coltree ? "gemm fold + column tree kernel (32-slot units)" : "gemm fold kernel (32-slot units)");
   } else if (gemm) {
     const size_t smem =
@@ -1002,11 +1003,11 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
     const int threads = Q == 16 ? 512 : 256;
     const int grid = grid_for(c, k, threads, smem, bs.units);
     if (coltree)
-      launch_k(c, fold_gemm_kernel<16, true>, grid, threads, smem, to_fold(pr), bs, ta, tb, tout);
+      launch_k(c, fold_gemm_kernel<16, true>, grid, threads, smem, to_fold(pr, c.release_late), bs, ta, tb, tout);
     else if (Q == 16)
-      launch_k(c, fold_gemm_kernel<16, false>, grid, threads, smem, to_fold(pr), bs, ta, tb, tout);
+      launch_k(c, fold_gemm_kernel<16, false>, grid, threads, smem, to_fold(pr, c.release_late), bs, ta, tb, tout);
     else
-      launch_k(c, fold_gemm_kernel<8, false>, grid, threads, smem, to_fold(pr), bs, ta, tb, tout);
+      launch_k(c, fold_gemm_kernel<8, false>, grid, threads, smem, to_fold(pr, c.release_late), bs, ta, tb, tout);
     post_launch(c, coltree ? "gemm fold + column tree kernel" : "gemm fold kernel");
   } else if (P == 8 && Q == 8)
     run_blocked<HAS_B, 8, 8>(c, pr, bs, ta, tb, tout);
@@ -1432,7 +1433,9 @@ bool launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
   const size_t tile_bytes = static_cast<size_t>(s) * sizeof(double);
   // 1) No in-tile schedule: the fold is the whole program.
   if (prog.ops.size() == 1 && prog.ops[0].kind == GOP_FOLD && prog.ops[0].dst == BUF_OUT) {
-    launch_fold_best<HAS_B>(c, p, ta, tb, tout);
+    LaunchCtx cl = c;  // an epilogue pass follows: the fold releases it at exit
+    cl.release_late = epi != nullptr;
+    launch_fold_best<HAS_B>(cl, p, ta, tb, tout);
     return false;
   }
   const BlockPlan bplan = block_plan(g, HAS_B);
@@ -1527,7 +1530,9 @@ bool launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
         return false;
       }
       if (tpass.kind != 0) {
-        launch_fold_best<HAS_B>(c, p, ta, tb, fold_dst);
+        LaunchCtx cl = c;  // the tree pass follows: the fold releases it at exit
+        cl.release_late = true;
+        launch_fold_best<HAS_B>(cl, p, ta, tb, fold_dst);
         const bool fuse_epi = tpass.kind == 1 || tpass.kind == 2;
         run_tree_pass(c, tpass, p, g.groups, s, fold_dst, tout, fuse_epi ? epi : nullptr);
         return fuse_epi;

@@ -24,6 +24,9 @@ struct LaunchCtx {
   unsigned int* sched_next = nullptr;
   unsigned int* chain_base = nullptr;   // kChainSlots blocks of kChainCounters
   unsigned int* chain_next = nullptr;
+  // The fold launched with this context is followed by a tree pass of the same
+  // operator: it releases its PDL dependents at CTA exit (tt_pdl.cuh).
+  bool release_late = false;
 };
 
 constexpr unsigned int kSchedSlots = 256;

@@ -33,6 +33,12 @@ __device__ __forceinline__ void pdl_enter() {
 // shared-memory-heavy kernels whose successors should not land on SMs they
 // still hold).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter(bool release_late) {
+  if (release_late)
+    pdl_wait();
+  else
+    pdl_enter();
+}
 
 int pdl_enabled();
 // The stream's last launch releases its dependents only at exit: the next
