@@ -55,25 +55,45 @@ __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* m, int c0, in
       : "memory");
 }
 
-constexpr int NI = 32, NJ = 16, K = 48, S = 8192;
+#ifndef S_SLOTS
+#define S_SLOTS 8192
+#endif
+#ifndef K_STEPS
+#define K_STEPS 48
+#endif
+constexpr int NI = 32, NJ = 16, K = K_STEPS, S = S_SLOTS;
+// G_GROUPS > 1: one CTA holds G_GROUPS independent consumer groups, each with its own ring,
+// producer warp and unit stream (the warps of one CTA share the schedulers fairly; CTAs of
+// one SM are served oldest first, tools/micro/warp_fair.cu)
+#ifndef G_GROUPS
+#define G_GROUPS 1
+#endif
+constexpr int G = G_GROUPS;
 
 template <int PI, int PJ, int SL, int RI, int RJ, int KS, int NS, int MODE, int MINB, int SCHED>
-__global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
+__global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32) * G, MINB)
     sg_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, double* out,
-              int reps, unsigned* q, unsigned long long* rec) {
-  constexpr int kC = (PI / RI) * (PJ / RJ) * SL;  // consumer threads
+              int reps, unsigned* q, unsigned long long* rec, unsigned long long* crec) {
+  constexpr int kC = (PI / RI) * (PJ / RJ) * SL;  // consumer threads per group
   constexpr int kCW = kC / 32;
+  const bool is_prod = threadIdx.x >= G * kC;
+  const int grp = is_prod ? (threadIdx.x - G * kC) / 32 : threadIdx.x / kC;
+  const int tg = is_prod ? 0 : threadIdx.x % kC;  // consumer thread within its group
+  const int vb = blockIdx.x * G + grp, vgrid = gridDim.x * G;
+  if (crec && !is_prod && tg == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(crec[3 * vb]));
   constexpr int kA = KS * PI * SL, kB = KS * PJ * SL, kSt = kA + kB;
   constexpr int nbi = NI / PI, nbj = NJ / PJ, nch = S / SL;
   constexpr int units1 = nbi * nbj * nch;
   constexpr int nst = K / KS;
-  extern __shared__ __align__(1024) double sm[];
+  extern __shared__ __align__(1024) double sm_all[];
+  constexpr int kGS = NS * kSt + (3 * NS + 15) / 16 * 16;  // doubles per group (ring + barriers + stage units)
+  double* sm = sm_all + grp * kGS;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + NS * kSt);
   uint64_t* empty = full + NS;
   int* stu = reinterpret_cast<int*>(empty + NS);  // unit of each stage (-1: done)
   const int units = units1 * reps;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
+  if (!is_prod && tg == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kCW);
@@ -81,21 +101,30 @@ __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == kCW) {
+  if (is_prod) {
     if (lane != 0) return;
     int st = 0;
     uint32_t ph = 0;
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    const int nsm = gridDim.x / MINB;
+    const int nsm = gridDim.x / MINB;  // SMs
     const int lo = (int)((long long)units * smid / nsm), hi = (int)((long long)units * (smid + 1) / nsm);
+    // SCHED: 0 static round-robin, 1 per-SM queue, 2 one global queue (the library's);
+    // +10*D: pace the CTAs of an SM (a producer issues a stage only while its CTA is
+    // at most D stages ahead of the slowest sibling still running)
+    constexpr int kSched = SCHED % 10, kPace = SCHED / 10;
     auto next = [&](int prev) -> int {
-      if (SCHED == 0) return prev < 0 ? blockIdx.x : prev + gridDim.x;
+      if (kSched == 0) return prev < 0 ? vb : prev + vgrid;
+      if (kSched == 2) return prev < 0 ? vb : (int)(vgrid + atomicAdd(&q[1023], 1u));
       const int v = lo + (int)atomicAdd(&q[smid], 1u);
       return v < hi ? v : units;
     };
+    volatile unsigned* pg = q + 384 + smid * 4;
+    unsigned myslot = 0, total = 0;
+    if (kPace) myslot = atomicAdd(&q[192 + smid], 1u);
     for (int u = next(-1); ; u = next(u)) {
       if (u >= units) {
+        if (kPace) pg[myslot] = 0x7fffffffu;
         mbar_wait(&empty[st], ph ^ 1);
         stu[st] = -1;
         mbar_arrive(&full[st]);
@@ -105,6 +134,17 @@ __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
       const int ch = uu % nch, b = uu / nch, bi = b % nbi, bj = b / nbi;
       for (int k = 0; k < nst; ++k) {
         mbar_wait(&empty[st], ph ^ 1);
+        if (kPace) {
+          pg[myslot] = ++total;
+          for (;;) {
+            const unsigned n = *(volatile unsigned*)&q[192 + smid];
+            unsigned m = 0x7fffffffu;
+            for (unsigned j = 0; j < n && j < 4; ++j)
+              if (j != myslot) m = min(m, pg[j]);
+            if (total <= m + kPace) break;
+            __nanosleep(100);
+          }
+        }
         stu[st] = u;
         if (MODE == 2) {
           mbar_arrive(&full[st]);
@@ -121,18 +161,21 @@ __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
     }
     return;
   }
-  const int sub = threadIdx.x / SL, slot = threadIdx.x % SL;
+  const int sub = tg / SL, slot = tg % SL;
   const int r0 = (sub / (PJ / RJ)) * RI, c0 = (sub % (PJ / RJ)) * RJ;
   int st = 0;
   uint32_t ph = 0;
+  bool first = true;
   for (;;) {
     mbar_wait(&full[st], ph);
+    if (first && crec && tg == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(crec[3 * vb + 1]));
+    first = false;
     const int u = stu[st];
     if (u < 0) break;
     const int uu = u % units1;
     const int ch = uu % nch, b = uu / nch, bi = b % nbi, bj = b / nbi;
     unsigned long long t_begin = 0;
-    if (rec && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+    if (rec && tg == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
     double acc[RI][RJ];
 #pragma unroll
     for (int i = 0; i < RI; ++i)
@@ -161,14 +204,14 @@ __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
         ph ^= 1;
       }
     }
-    if (rec && threadIdx.x == 0) {
+    if (rec && tg == 0) {
       unsigned long long t_end;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       rec[3 * u] = t_begin;
       rec[3 * u + 1] = t_end;
-      rec[3 * u + 2] = smid * 65536ull + blockIdx.x;
+      rec[3 * u + 2] = smid * 65536ull + vb;
     }
     if (u < units1 || MODE != 0) {
       double* o = out + ((size_t)(bi * PI + r0) * NJ + bj * PJ + c0) * S + ch * SL + slot;
@@ -178,6 +221,11 @@ __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32), MINB)
         for (int j = 0; j < RJ; ++j) o[((size_t)i * NJ + j) * S] = acc[i][j];
     }
   }
+  if (crec && tg == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(crec[3 * vb + 2]));
+}
+
+__global__ void stamp_kernel(unsigned long long* t) {
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t[0]));
 }
 
 __global__ void ref_kernel(const double* A, const double* B, double* out) {
@@ -216,14 +264,17 @@ static void make_map(CUtensorMap* m, const double* base, int rows, int box_s, in
 double *gA, *gB, *gO, *gR;
 unsigned* gQ;
 int g_sms;
+int g_run_idx = 0;
 
 template <int PI, int PJ, int SL, int RI, int RJ, int KS, int NS, int MODE, int MINB, int SCHED = 1>
 void run(const char* name, int reps) {
+  const int me = g_run_idx++;
+  if (getenv("SG_ONLY") && atoi(getenv("SG_ONLY")) != me) return;
   CUtensorMap mA, mB;
   make_map(&mA, gA, NI, SL, PI, KS);
   make_map(&mB, gB, NJ, SL, PJ, KS);
-  constexpr int threads = (PI / RI) * (PJ / RJ) * SL + 32;
-  constexpr size_t smem = (size_t)NS * KS * (PI + PJ) * SL * 8 + 3 * NS * 8;
+  constexpr int threads = ((PI / RI) * (PJ / RJ) * SL + 32) * G;
+  constexpr size_t smem = ((size_t)NS * KS * (PI + PJ) * SL * 8 + (3 * NS + 15) / 16 * 128) * G;
   auto k = sg_kernel<PI, PJ, SL, RI, RJ, KS, NS, MODE, MINB, SCHED>;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
@@ -238,7 +289,7 @@ void run(const char* name, int reps) {
   cudaEventCreate(&e1);
   CK(cudaMemset(gO, 0xff, (size_t)NI * NJ * S * 8));
   CK(cudaMemset(gQ, 0, 4096));
-  k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ, nullptr);
+  k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ, nullptr, nullptr);
   CK(cudaDeviceSynchronize());
   bool ok = true;
   if (MODE == 0) {
@@ -251,7 +302,7 @@ void run(const char* name, int reps) {
   for (int it = 0; it < 5; ++it) {
     CK(cudaMemsetAsync(gQ, 0, 4096));
     cudaEventRecord(e0);
-    k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ, nullptr);
+    k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ, nullptr, nullptr);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -263,8 +314,40 @@ void run(const char* name, int reps) {
     unsigned long long* rec;
     CK(cudaMalloc(&rec, units * 24));
     CK(cudaMemsetAsync(gQ, 0, 4096));
-    k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ, rec);
+    unsigned long long* crec;
+    const int vg = grid * G;
+    CK(cudaMalloc(&crec, (vg * 3 + 2) * 8));
+    CK(cudaMemsetAsync(crec, 0, (vg * 3 + 2) * 8));
     CK(cudaDeviceSynchronize());
+    stamp_kernel<<<1, 1>>>(crec + vg * 3);  // ends right before the fold kernel starts
+    k<<<grid, threads, smem>>>(mA, mB, gO, reps, gQ, rec, crec);
+    stamp_kernel<<<1, 1>>>(crec + vg * 3 + 1);  // starts right after it ends
+    CK(cudaDeviceSynchronize());
+    {
+      std::vector<unsigned long long> c(vg * 3 + 2);
+      CK(cudaMemcpy(c.data(), crec, c.size() * 8, cudaMemcpyDeviceToHost));
+      const unsigned long long pre = c[vg * 3], post = c[vg * 3 + 1];
+      std::vector<double> en, fd, ex;
+      for (int b = 0; b < vg; ++b) {
+        en.push_back((c[3 * b] - pre) * 1e-3);
+        fd.push_back((c[3 * b + 1] - pre) * 1e-3);
+        ex.push_back((c[3 * b + 2] - pre) * 1e-3);
+      }
+      {
+        const int tiers = vg / g_sms;
+        printf("   mean CTA exit by launch tier (blockIdx / #SMs):");
+        for (int t = 0; t < tiers; ++t) {
+          double a = 0;
+          for (int b = t * g_sms; b < (t + 1) * g_sms; ++b) a += ex[b] - en[b];
+          printf(" %.1f", a / g_sms);
+        }
+        printf(" us after entry\n");
+      }
+      std::sort(en.begin(), en.end()); std::sort(fd.begin(), fd.end()); std::sort(ex.begin(), ex.end());
+      printf("   CTA stamps (us after the preceding kernel's stamp): entry %.2f/%.2f/%.2f  first data %.2f/%.2f/%.2f  exit %.2f/%.2f/%.2f  next kernel %.2f\n",
+             en[0], en[vg / 2], en[vg - 1], fd[0], fd[vg / 2], fd[vg - 1], ex[0], ex[vg / 2], ex[vg - 1], (post - pre) * 1e-3);
+    }
+    cudaFree(crec);
     std::vector<unsigned long long> h(units * 3);
     CK(cudaMemcpy(h.data(), rec, units * 24, cudaMemcpyDeviceToHost));
     unsigned long long t0 = ~0ull, t1 = 0;
@@ -317,8 +400,29 @@ int main() {
   CK(cudaMemcpy(gB, h.data() + 7, nb * 8, cudaMemcpyHostToDevice));
   ref_kernel<<<(NI * NJ * S + 255) / 256, 256>>>(gA, gB, gR);
   CK(cudaDeviceSynchronize());
+#if G_GROUPS > 1
+  run<16, 16, 16, 8, 4, 4, 4, 0, 1, 1>("G groups/CTA per-SM queue", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 1, 0>("G groups/CTA static", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 1, 2>("G groups/CTA global queue", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 2, 1, 0>("G groups/CTA static MODE2 (no TMA)", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 2, 1, 0>("G groups/CTA static MODE2 (no TMA)", 4);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 1, 2>("G groups/CTA global queue", 4);
+  return 0;
+#endif
   run<16, 16, 16, 8, 4, 4, 4, 0, 3, 1>("16x16x16 8x4 ks4 ns4 per-SM", 1);
   run<16, 16, 16, 8, 4, 4, 4, 0, 3, 0>("16x16x16 8x4 ks4 ns4 static", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 2>("16x16x16 8x4 ks4 ns4 global queue", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 2, 3, 0>("16x16x16 static MODE2 (no TMA)", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 2, 3, 20>("16x16x16 static MODE2 pace 2", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 2, 3, 40>("16x16x16 static MODE2 pace 4", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 20>("16x16x16 static pace 2", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 40>("16x16x16 static pace 4", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 21>("16x16x16 per-SM pace 2", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 41>("16x16x16 per-SM pace 4", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 22>("16x16x16 global pace 2", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 42>("16x16x16 global pace 4", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 82>("16x16x16 global pace 8", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 42>("16x16x16 global pace 4", 4);
   run<16, 16, 16, 8, 4, 4, 4, 0, 3, 1>("16x16x16 8x4 ks4 ns4 per-SM", 4);
   return 0;
 }
