@@ -13,6 +13,7 @@ import torch
 
 import paper_2011_01805_b200 as tt
 from paper_2011_01805_b200 import DimSpec, TileTensor, TileTensorShape, parse_shape, format_shape
+from oracle_lib import CheckerError
 from shapes import (fuzz_unknown_regions, partner_shape, random_pack_shape, random_tensor,
                     used_mask)
 
@@ -827,3 +828,59 @@ def test_dependent_launch_chain(gpu, oracle):
     assert_bitwise(Y.tiles(), wy, "dependent chain Y")
     for k, (got, want) in enumerate(sums):
         assert_bitwise(got.tiles(), want, f"dependent chain sum {k}")
+
+
+def test_tile_matmul_random_shapes(gpu, oracle):
+    """Random products with two broadcast dims (the GEMM-shaped fold): both summed
+    dims, block counts that cross the 16 x 16 group blocks with partial edge blocks,
+    fold lengths that are not a multiple of the ring's 4-step stages, partial tiles
+    ('?' results), and zero to two further group dims -- bitwise and counter parity."""
+    rng = random.Random(20241021)
+    nrng = np.random.default_rng(4242)
+    done = 0
+    while done < 36:
+        rank = rng.choice([3, 3, 4, 5])
+        s = rng.choice([256, 512, 1024])
+        # tile dims: powers of two with product s
+        logs = [0] * rank
+        for _ in range(s.bit_length() - 1):
+            logs[rng.randrange(rank)] += 1
+        t = [1 << l for l in logs]
+        dim = rng.choice([1, 2])           # the summed (fold) dim
+        other = 2 if dim == 1 else 1        # A varies, B broadcasts
+        third = 3                           # B varies, A broadcasts
+        ext = [1] * rank
+        ext[dim - 1] = rng.randint(1, 13)
+        ext[other - 1] = rng.choice([1, 2, 5, 15, 16, 17, 31, 33, 40])
+        ext[third - 1] = rng.choice([1, 3, 8, 16, 18, 23, 32, 37])
+        for i in range(3, rank):
+            ext[i] = rng.randint(1, 3)
+        if ext[0] * ext[1] * ext[2] * int(np.prod(ext[3:])) > 16000:
+            continue
+        n = [rng.randint((e - 1) * ti + 1, e * ti) for e, ti in zip(ext, t)]
+        da, db = [], []
+        for i in range(rank):
+            if i == other - 1:
+                da.append(DimSpec(n[i], 1, t[i]))
+                db.append(DimSpec(1, t[i], t[i]) if t[i] > 1 and rng.random() < 0.8 else DimSpec(1, 1, t[i]))
+            elif i == third - 1:
+                da.append(DimSpec(1, t[i], t[i]) if t[i] > 1 and rng.random() < 0.8 else DimSpec(1, 1, t[i]))
+                db.append(DimSpec(n[i], 1, t[i]))
+            else:
+                da.append(DimSpec(n[i], 1, t[i]))
+                db.append(DimSpec(n[i], 1, t[i]))
+        sa, sb = TileTensorShape(da), TileTensorShape(db)
+        try:
+            ta = nrng.uniform(-1, 1, size=(sa.tile_count(), s))
+            tb = nrng.uniform(-1, 1, size=(sb.tile_count(), s))
+            ws, wt, wc = oracle.mul_sum(sa, ta, sb, tb, s, dim)
+        except CheckerError:
+            continue
+        S = session(s)
+        S.reset_counters()
+        got = tt.tt_mul_sum(TileTensor(sa, ta, S), TileTensor(sb, tb, S), dim)
+        what = f"{format_shape(sa)} x {format_shape(sb)} sum {dim} (s={s})"
+        assert got.shape() == ws, what
+        assert_bitwise(got.tiles(), wt, what)
+        assert same_cost(S.cost_report(), wc), what
+        done += 1
