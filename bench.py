@@ -621,6 +621,10 @@ def bench_extra_ops(tt, X, W, x_dense, sx, S, stream, hbm_peak, args, out_tiles)
     ops["pack"] = {"ms": t * 1e3, "GB/s": pb / t / 1e9, "frac": pb / t / 1e9 / hbm_peak,
                    "frac_of_8TBps": pb / t / 1e12 / 8.0, "tile_slots_per_s": x_tiles * S5 / t,
                    "alg_bytes": pb}
+    t = time_events(lambda: tt.unpack_device(X), max(1, min(5, args.steps)), stream)
+    ops["unpack"] = {"ms": t * 1e3, "GB/s": pb / t / 1e9, "frac": pb / t / 1e9 / hbm_peak,
+                     "frac_of_8TBps": pb / t / 1e12 / 8.0, "tile_slots_per_s": x_tiles * S5 / t,
+                     "alg_bytes": pb}
     # unfused elementwise (tt_mul with W broadcast along dim 1, tt_add)
     for name, fn, nb in (("ew_mul_bcast", lambda: tt.tt_mul(X, W), (2 * x_tiles + W_TILES) * S5 * 8),
                          ("ew_add", lambda: tt.tt_add(X, X), 2 * x_tiles * S5 * 8)):
