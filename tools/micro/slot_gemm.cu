@@ -409,20 +409,18 @@ int main() {
   run<16, 16, 16, 8, 4, 4, 4, 0, 1, 2>("G groups/CTA global queue", 4);
   return 0;
 #endif
+  // index (SG_ONLY):  0 shipped shape, per-SM queue   1 static   2 the library's global queue
+  //   3 no TMA, static   4 no TMA, 4 reps (steady state)   5 ring 6 steps x 3 stages
+  //   6 ring 12 steps x 2 stages at 2 CTAs/SM   7 CTAs of an SM paced against each other
+  //   8 shipped shape, 4 reps (steady state)
   run<16, 16, 16, 8, 4, 4, 4, 0, 3, 1>("16x16x16 8x4 ks4 ns4 per-SM", 1);
   run<16, 16, 16, 8, 4, 4, 4, 0, 3, 0>("16x16x16 8x4 ks4 ns4 static", 1);
   run<16, 16, 16, 8, 4, 4, 4, 0, 3, 2>("16x16x16 8x4 ks4 ns4 global queue", 1);
   run<16, 16, 16, 8, 4, 4, 4, 2, 3, 0>("16x16x16 static MODE2 (no TMA)", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 2, 3, 20>("16x16x16 static MODE2 pace 2", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 2, 3, 40>("16x16x16 static MODE2 pace 4", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 20>("16x16x16 static pace 2", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 40>("16x16x16 static pace 4", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 21>("16x16x16 per-SM pace 2", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 41>("16x16x16 per-SM pace 4", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 22>("16x16x16 global pace 2", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 42>("16x16x16 global pace 4", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 82>("16x16x16 global pace 8", 1);
-  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 42>("16x16x16 global pace 4", 4);
+  run<16, 16, 16, 8, 4, 4, 4, 2, 3, 0>("16x16x16 static MODE2 (no TMA)", 4);
+  run<16, 16, 16, 8, 4, 6, 3, 0, 3, 1>("16x16x16 8x4 ks6 ns3 per-SM", 1);
+  run<16, 16, 16, 8, 4, 12, 2, 0, 2, 1>("16x16x16 8x4 ks12 ns2 2 CTAs/SM", 1);
+  run<16, 16, 16, 8, 4, 4, 4, 0, 3, 42>("16x16x16 global queue, paced (4 stages)", 1);
   run<16, 16, 16, 8, 4, 4, 4, 0, 3, 1>("16x16x16 8x4 ks4 ns4 per-SM", 4);
   return 0;
 }
