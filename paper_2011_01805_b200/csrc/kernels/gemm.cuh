@@ -172,6 +172,74 @@ __global__ void __launch_bounds__(128) fold_ring_kernel(const __grid_constant__ 
   }
 }
 
+// Group-blocked ring fold: few groups, long folds in which ONE operand is the
+// same for all groups along a group dim (config 2: the vector's tiles for the
+// 16 row blocks of the matrix; config 4's second layer: the weight tiles for
+// the 16 batch tiles).  The plain ring fold above re-reads that operand from L2
+// once per group, and such folds run at the L2's ~9 TB/s, not at HBM's rate.
+// Here a thread folds its slot pair for Q consecutive groups along that dim:
+// one copy of the shared operand and Q of the other per step, through the same
+// per-thread cp.async ring (no barrier).  The host passes a group grid whose
+// blocked dim is already divided by Q (strides multiplied), `vq` / `oq` = tile
+// strides between the Q groups of the varying operand / the output.  SHARED_A:
+// A is the shared operand.  The products and the left fold are those of
+// fold_ring_kernel (IEEE multiplication commutes).
+template <int Q, int T, bool SHARED_A>
+__global__ void __launch_bounds__(T) fold_ring_blk_kernel(const __grid_constant__ FoldParams p,
+                                                          const double* __restrict__ A,
+                                                          const double* __restrict__ B,
+                                                          double* __restrict__ OUT, FastDiv64 runs_div,
+                                                          int64_t vq, int64_t oq) {
+  pdl_enter(p.late != 0);
+  extern __shared__ __align__(16) double2 bring[];  // [kFoldRing][1 + Q][T]
+  const int64_t s = p.s;
+  const int64_t count = p.count;
+  const int64_t ss = (SHARED_A ? p.g.astep : p.g.bstep) * s;  // fold strides
+  const int64_t sv = (SHARED_A ? p.g.bstep : p.g.astep) * s;
+  const int t = threadIdx.x;
+  auto cell = [&](int slot, int which) { return bring + (slot * (1 + Q) + which) * T + t; };
+  const uint64_t total = static_cast<uint64_t>(p.g.groups) * runs_div.d;
+  for (uint64_t r = blockIdx.x; r < total; r += gridDim.x) {
+    const uint64_t v = fdiv(r, runs_div);
+    const int64_t j0 = static_cast<int64_t>(r - v * runs_div.d) * (2 * T) + 2 * t;
+    const GroupBase gb = group_base(p, v);
+    const double* pa = A + (gb.a + p.first * p.g.astep) * s + j0;
+    const double* pb = B + (gb.b + p.first * p.g.bstep) * s + j0;
+    const double* psh = SHARED_A ? pa : pb;
+    const double* pv = SHARED_A ? pb : pa;
+    auto issue = [&](int slot, int64_t step) {
+      cp_async16(cell(slot, 0), psh + step * ss);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) cp_async16(cell(slot, 1 + q), pv + step * sv + q * vq * s);
+    };
+#pragma unroll
+    for (int k = 0; k < kFoldRing; ++k) {
+      if (k < count) issue(k, k);
+      cp_async_commit();
+    }
+    double2 acc[Q];
+    int slot = 0;
+    for (int64_t c = 0; c < count; ++c) {
+      cp_async_wait<kFoldRing - 1>();  // step c has landed
+      const double2 y = *cell(slot, 0);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const double2 x = *cell(slot, 1 + q);
+        const double2 pr = make_double2(dmul(x.x, y.x), dmul(x.y, y.y));
+        acc[q] = c == 0 ? pr : make_double2(dadd(acc[q].x, pr.x), dadd(acc[q].y, pr.y));
+      }
+      const int64_t f = c + kFoldRing;  // refill this slot with step c + ring
+      if (f < count) issue(slot, f);
+      cp_async_commit();
+      if (++slot == kFoldRing) slot = 0;
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      *reinterpret_cast<double2*>(OUT + (gb.out + q * oq) * s + j0) = acc[q];
+  }
+}
+
 // BC = block columns (groups along ib): 16 (512 threads) or 8 (256 threads,
 // more and smaller work units when the 16 x 16 grid would leave SMs idle).
 // COLTREE: the reduction is over the first dim with t = 16 (s = 16 * stride):

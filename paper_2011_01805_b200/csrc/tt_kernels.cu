@@ -713,6 +713,59 @@ const int g_fold_ring = [] {
   return e ? std::atoi(e) : -1;
 }();
 
+// TT_FOLD_BLK=0: no group-blocked ring fold (parity variant)
+const int g_fold_blk = [] {
+  const char* e = std::getenv("TT_FOLD_BLK");
+  return e ? std::atoi(e) : 1;
+}();
+
+// Small few-group fold with one operand shared along a group dim (fold_ring_blk_kernel;
+// config 2's matvec: the fold 6.8 -> 5.5 us, the call 12.3 -> 10.7 us).  Folds large
+// enough for fold_ring_kernel stay there: config 4's second layer measured the same
+// either way (22.5 us: bound by DRAM, including the write-back of the activations the
+// pass before it left in L2, not by the L2 re-reads of the shared operand).
+template <int Q, int T, bool SHARED_A>
+void run_fold_ring_blk(const LaunchCtx& c, const GroupParams& p, int d, const double* ta,
+                       const double* tb, double* tout) {
+  FoldParams f = to_fold(p, c.release_late);
+  const int64_t vq = SHARED_A ? f.g.b_stride[d] : f.g.a_stride[d];
+  const int64_t oq = f.g.out_stride[d];
+  f.g.ext[d] /= Q;
+  f.g.out_stride[d] *= Q;
+  f.g.a_stride[d] *= Q;
+  f.g.b_stride[d] *= Q;
+  f.g.groups /= Q;
+  f.gdiv[d] = make_div64(static_cast<uint64_t>(f.g.ext[d]));
+  const int64_t runs = p.s / (2 * T);
+  constexpr size_t smem = static_cast<size_t>(kFoldRing) * (1 + Q) * T * sizeof(double2);
+  auto k = fold_ring_blk_kernel<Q, T, SHARED_A>;
+  set_smem_attr((const void*)k, smem);
+  const int grid = grid_for(c, (const void*)k, T, smem, f.g.groups * runs);
+  launch_k(c, k, grid, T, smem, f, ta, tb, tout, make_div64(static_cast<uint64_t>(runs)), vq, oq);
+}
+
+bool launch_fold_ring_blk(const LaunchCtx& c, const GroupParams& p, const double* ta,
+                          const double* tb, double* tout) {
+  const GroupSpec& g = p.g;
+  const int64_t s = p.s;
+  if (!g_fold_blk || g.astep == 0 || g.bstep == 0 || p.ops[0].y < 2 || s % 256 != 0 ||
+      !aligned16(ta) || !aligned16(tb) || !aligned16(tout))
+    return false;
+  int d = -1;
+  bool shared_a = false;
+  for (int i = 0; i < g.nd && d < 0; ++i) {
+    if (g.ext[i] < 2 || g.ext[i] % 2 != 0 || g.out_stride[i] == 0) continue;
+    if (g.a_stride[i] == 0 && g.b_stride[i] > 0) d = i, shared_a = true;
+    else if (g.b_stride[i] == 0 && g.a_stride[i] > 0) d = i, shared_a = false;
+  }
+  if (d < 0) return false;
+  // Q = 2 groups per thread, 64-thread CTAs (measured on config 2: Q = 2 5.5 us, Q = 4
+  // 5.9 us, scalar fold 6.8 us; 128-thread CTAs the same)
+  if (shared_a) run_fold_ring_blk<2, 64, true>(c, p, d, ta, tb, tout);
+  else run_fold_ring_blk<2, 64, false>(c, p, d, ta, tb, tout);
+  return true;
+}
+
 template <bool HAS_B>
 void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
                  double* tout) {
@@ -735,6 +788,8 @@ void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, con
     const int grid = grid_for(c, (const void*)fold_ring_kernel<HAS_B>, 128, 0, p.g.groups * runs);
     launch_k(c, fold_ring_kernel<HAS_B>, grid, 128, 0, to_fold(p, c.release_late), ta, tb, tout,
                                                         make_div64(static_cast<uint64_t>(runs)));
+  } else if (HAS_B && launch_fold_ring_blk(c, p, ta, tb, tout)) {
+    // small fold, few groups sharing one operand: group-blocked ring fold
   } else {
     const int64_t work = (p.g.groups * s + 255) / 256;
     const int grid = grid_for(c, (const void*)fold_kernel<HAS_B, false>, 256, 0, work);

@@ -884,3 +884,31 @@ def test_tile_matmul_random_shapes(gpu, oracle):
         assert_bitwise(got.tiles(), wt, what)
         assert same_cost(S.cost_report(), wc), what
         done += 1
+
+
+def test_few_group_shared_operand_folds(gpu, oracle):
+    """Small folds over few groups in which one operand is the same for every group
+    along a dim (matvec forms: the group-blocked ring fold): both orientations, fold
+    lengths below and above the ring depth, a further group dim, large and small tiles."""
+    nrng = np.random.default_rng(99)
+    cases = [  # (A shape, B shape, summed dim, slots)
+        ("[1024/64,4096/128]", "[*/64,4096/128]", 2, 8192),        # config 2
+        ("[*/64,640/128]", "[384/64,640/128]", 2, 8192),           # the shared operand first
+        ("[128/32,66/2,*/4]", "[*/32,66/2,8/4]", 2, 256),          # 33 steps, both dims broadcast
+        ("[20/2,7,48/128]", "[*/2,7,48/128]", 2, 256),             # t2 = 1: fold only, 7 steps
+        ("[12/2,300/8,5/16]", "[*/2,300/8,5/16]", 2, 256),         # odd third dim: partial tiles
+        ("[8/4,100/4,3,6/64]", "[8/4,100/4,3,*/64]", 2, 1024),     # shared along the last dim
+        ("[6/2,9/2,2/64]", "[*/2,9/2,2/64]", 2, 256),              # 5 steps: shorter than the ring
+        ("[64/16,2048/512]", "[*/16,2048/512]", 2, 8192),
+    ]
+    for xa, xb, dim, s in cases:
+        S = session(s)
+        sa, sb = parse_shape(xa), parse_shape(xb)
+        ta = nrng.uniform(-1, 1, size=(sa.tile_count(), s))
+        tb = nrng.uniform(-1, 1, size=(sb.tile_count(), s))
+        ws, wt, wc = oracle.mul_sum(sa, ta, sb, tb, s, dim)
+        S.reset_counters()
+        got = tt.tt_mul_sum(TileTensor(sa, ta, S), TileTensor(sb, tb, S), dim)
+        assert got.shape() == ws, f"{xa} x {xb}"
+        assert_bitwise(got.tiles(), wt, f"{xa} x {xb}")
+        assert same_cost(S.cost_report(), wc), f"{xa} x {xb}"
