@@ -750,6 +750,9 @@ def test_interleaved_kats_on_gpu(gpu):
     ("[640/16,64/32,256/32]", "[*/16,64/32,256/32]"),
     ("[*/16,640/32,256/32]", "[64/16,640/32,256/32]"),
     ("[96/16,64/32,1504/32]", "[*/16,64/32,*/32]"),
+    # even innermost broadcast extent with two broadcast dims (paired items), either side
+    ("[96/16,64/32,1536/32]", "[*/16,64/32,*/32]"),
+    ("[*/16,64/32,*/32]", "[96/16,64/32,1536/32]"),
 ])
 @pytest.mark.parametrize("op", [tt.OpKind.add, tt.OpKind.mul], ids=["add", "mul"])
 def test_broadcast_elementwise_large(gpu, oracle, case, op):
