@@ -1,7 +1,7 @@
 """GPU parity of the matmul-path kernel variants selected by environment knobs.
 
 The knobs (TT_GEMM_TMA, TT_GEMM_DYNAMIC, TT_GEMM_CFG, TT_GEMM_BC, TT_GEMM_ORDER,
-TT_TREE_SMEM, TT_ROW_ROWS, TT_TREE_TMA) are read once when the native library loads, so each variant
+TT_TREE_SMEM, TT_ROW_ROWS, TT_TREE_TMA, TT_FOLD_RING, TT_FOLD_BLK) are read once when the native library loads, so each variant
 runs in its own subprocess; every one must give the oracle's tiles bit for bit.
 The chain is the reference's matmul_b -> matmul_a (tests/test_linalg.cpp:157-178)
 on 8192-slot 16x32x16 tiles, at a size where both stages take the GEMM fold
@@ -45,12 +45,15 @@ for i, (k, v) in enumerate(sorted(json.loads(sys.argv[3]).items())):
     sh = parse_shape(v)
     rng = np.random.default_rng(200 + i)
     F[k] = TileTensor(sh, rng.uniform(-1, 1, size=(sh.tile_count(), 8192)), S)
-folds = [tt.tt_mul_sum(F["M"], F["V"], 1), tt.tt_mul_sum(F["M"], F["W"], 1), tt.tt_sum(F["M"], 1)]
+folds = [tt.tt_mul_sum(F["M"], F["V"], 1), tt.tt_mul_sum(F["M"], F["W"], 1), tt.tt_sum(F["M"], 1),
+         tt.tt_mul_sum(F["N"], F["U"], 1), tt.tt_mul_sum(F["U"], F["N"], 1)]
 h = lambda t: hashlib.sha256(np.ascontiguousarray(t.tiles()).tobytes()).hexdigest()
 print(json.dumps({"s1": h(s1), "r": h(r), "folds": [h(f) for f in folds]}))
 """
 # few-group folds (t = 1 summed dim, 40 steps): the plain and the cp.async-ring fold
-FOLD_SHAPES = {"M": "[40,2/2,4096/4096]", "V": "[40,2/2,4096/4096]", "W": "[*,2/2,4096/4096]"}
+# N x U: two groups along dim 2 that share U's tiles (the group-blocked ring fold)
+FOLD_SHAPES = {"M": "[40,2/2,4096/4096]", "V": "[40,2/2,4096/4096]", "W": "[*,2/2,4096/4096]",
+               "N": "[40,4/2,4096/4096]", "U": "[40,*/2,4096/4096]"}
 
 VARIANTS = [
     {},
@@ -77,6 +80,7 @@ VARIANTS = [
     {"TT_TREE_SMEM": "1"},
     {"TT_FOLD_RING": "1"},
     {"TT_FOLD_RING": "0"},
+    {"TT_FOLD_BLK": "0"},
     {"TT_ROW_CHAIN": "2"},
     {"TT_ROW_CHAIN": "4"},
     {"TT_ROW_ROWS": "16"},
@@ -108,7 +112,8 @@ def expected(oracle):
         rng = np.random.default_rng(200 + i)
         F[k] = (sh, rng.uniform(-1, 1, size=(sh.tile_count(), S)))
     folds = [oracle.mul_sum(*F["M"], *F["V"], S, 1)[1], oracle.mul_sum(*F["M"], *F["W"], S, 1)[1],
-             oracle.sum(*F["M"], S, 1)[1]]
+             oracle.sum(*F["M"], S, 1)[1], oracle.mul_sum(*F["N"], *F["U"], S, 1)[1],
+             oracle.mul_sum(*F["U"], *F["N"], S, 1)[1]]
     return {"s1": _digest(s1t), "r": _digest(rt), "folds": [_digest(f) for f in folds]}
 
 
