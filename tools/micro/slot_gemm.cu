@@ -185,6 +185,34 @@ __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32) * G, MINB)
       if (k > 0) mbar_wait(&full[st], ph);
       const double* sA = sm + st * kSt + r0 * SL + slot;
       const double* sB = sm + st * kSt + kA + c0 * SL + slot;
+#ifdef SG_PIPE
+      // operands of step h + 1 loaded before the arithmetic of step h (register double buffer)
+      double a[RI], bb[RJ];
+#pragma unroll
+      for (int i = 0; i < RI; ++i) a[i] = sA[i * SL];
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) bb[j] = sB[j * SL];
+#pragma unroll
+      for (int h = 0; h < KS; ++h) {
+        double an[RI], bn[RJ];
+        if (h + 1 < KS) {
+#pragma unroll
+          for (int i = 0; i < RI; ++i) an[i] = sA[(h + 1) * PI * SL + i * SL];
+#pragma unroll
+          for (int j = 0; j < RJ; ++j) bn[j] = sB[(h + 1) * PJ * SL + j * SL];
+        }
+#pragma unroll
+        for (int i = 0; i < RI; ++i)
+#pragma unroll
+          for (int j = 0; j < RJ; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], bb[j]));
+        if (h + 1 < KS) {
+#pragma unroll
+          for (int i = 0; i < RI; ++i) a[i] = an[i];
+#pragma unroll
+          for (int j = 0; j < RJ; ++j) bb[j] = bn[j];
+        }
+      }
+#else
 #pragma unroll
       for (int h = 0; h < KS; ++h) {
         double a[RI], bb[RJ];
@@ -197,6 +225,7 @@ __global__ void __launch_bounds__(((PI / RI) * (PJ / RJ) * SL + 32) * G, MINB)
 #pragma unroll
           for (int j = 0; j < RJ; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], bb[j]));
       }
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
       if (++st == NS) {
