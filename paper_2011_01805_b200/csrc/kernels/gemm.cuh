@@ -121,11 +121,15 @@ __device__ __forceinline__ void cp_async_wait() {
 // kFoldRing fold steps of loads are in flight per thread.  A CTA owns 256
 // consecutive slots of one group (s % 256 == 0, 16-byte aligned operands).
 constexpr int kFoldRing = 8;
-template <bool HAS_B>
+// EPI: the reduction's elementwise tail (+ C, square: tt_mul_sum_affine) applied to
+// the folded pair before its store -- no separate in-place pass over the result
+// (config 4's second layer: fold 22.5 us + epilogue pass 3.2 us -> one kernel).
+template <bool HAS_B, bool EPI = false>
 __global__ void __launch_bounds__(128) fold_ring_kernel(const __grid_constant__ FoldParams p,
                                                         const double* __restrict__ A,
                                                         const double* __restrict__ B,
-                                                        double* __restrict__ OUT, FastDiv64 runs_div) {
+                                                        double* __restrict__ OUT, FastDiv64 runs_div,
+                                                        const __grid_constant__ EpiDev epi) {
   pdl_enter(p.late != 0);
   __shared__ __align__(16) double2 ring[kFoldRing][HAS_B ? 2 : 1][128];
   const int64_t s = p.s;
@@ -168,6 +172,11 @@ __global__ void __launch_bounds__(128) fold_ring_kernel(const __grid_constant__ 
       if (++slot == kFoldRing) slot = 0;
     }
     cp_async_wait<0>();
+    if (EPI) {
+      double x[2] = {acc.x, acc.y};
+      epi_apply_n<2>(epi, x, epi_tile(epi, static_cast<uint64_t>(gb.out), s), j0, 1);
+      acc = make_double2(x[0], x[1]);
+    }
     *reinterpret_cast<double2*>(OUT + gb.out * s + j0) = acc;
   }
 }

@@ -798,10 +798,13 @@ bool launch_fold_ring_blk(const LaunchCtx& c, const GroupParams& p, const double
   return true;
 }
 
+// Returns true when `epi` (the reduction's elementwise tail, may be null) was applied
+// in the fold's store; the caller runs it as its own pass otherwise.
 template <bool HAS_B>
-void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
-                 double* tout) {
+bool launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, const double* tb,
+                 double* tout, const Epilogue* epi = nullptr) {
   const int64_t s = p.s;
+  bool fused = false;
   // 256 slots per warp when that still gives every SM >= 8 warps; otherwise
   // one slot per thread (small folds are latency bound: more loads in flight)
   const int64_t vec_warps = p.g.groups * ((s / 2 + 127) / 128);
@@ -817,9 +820,18 @@ void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, con
              s % 256 == 0 && p.ops[0].y > 1 && aligned16(ta) && (!HAS_B || aligned16(tb)) &&
              aligned16(tout)) {
     const int64_t runs = s / 256;
-    const int grid = grid_for(c, (const void*)fold_ring_kernel<HAS_B>, 128, 0, p.g.groups * runs);
-    launch_k(c, fold_ring_kernel<HAS_B>, grid, 128, 0, to_fold(p, c.release_late), ta, tb, tout,
-                                                        make_div64(static_cast<uint64_t>(runs)));
+    static const int fuse_epi = [] { const char* e = std::getenv("TT_FOLD_EPI"); return e ? std::atoi(e) : 1; }();
+    if (epi != nullptr && epi->active() && epi->nmask == 0 && fuse_epi) {
+      // the tail rides on the fold's store: no pass follows, no late release
+      const int grid = grid_for(c, (const void*)fold_ring_kernel<HAS_B, true>, 128, 0, p.g.groups * runs);
+      launch_k(c, fold_ring_kernel<HAS_B, true>, grid, 128, 0, to_fold(p, false), ta, tb, tout,
+               make_div64(static_cast<uint64_t>(runs)), make_epi_dev(*epi));
+      fused = true;
+    } else {
+      const int grid = grid_for(c, (const void*)fold_ring_kernel<HAS_B>, 128, 0, p.g.groups * runs);
+      launch_k(c, fold_ring_kernel<HAS_B>, grid, 128, 0, to_fold(p, c.release_late), ta, tb, tout,
+               make_div64(static_cast<uint64_t>(runs)), EpiDev{});
+    }
   } else if (HAS_B && launch_fold_ring_blk(c, p, ta, tb, tout)) {
     // small fold, few groups sharing one operand: group-blocked ring fold
   } else {
@@ -829,6 +841,7 @@ void launch_fold(const LaunchCtx& c, const GroupParams& p, const double* ta, con
                                                            make_div64(static_cast<uint64_t>(s)));
   }
   post_launch(c, "fold kernel");
+  return fused;
 }
 
 // GEMM unit width (TT_GEMM_SLOTS=64 forces the 64-slot, 1-CTA-per-SM variant).
@@ -1106,8 +1119,8 @@ void launch_fold_blocked(const LaunchCtx& c, const GroupParams& p, const BlockPl
 
 // Phase-1 fold: blocked when the product has a broadcast structure to exploit.
 template <bool HAS_B>
-void launch_fold_best(const LaunchCtx& c, const GroupParams& p, const double* ta,
-                      const double* tb, double* tout) {
+bool launch_fold_best(const LaunchCtx& c, const GroupParams& p, const double* ta,
+                      const double* tb, double* tout, const Epilogue* epi = nullptr) {
   const BlockPlan bp = block_plan(p.g, HAS_B);
   bool blocked = HAS_B && (bp.ia >= 0 || bp.ib >= 0) && p.ops[0].y > 1 && forced_path() != 3;
   if (blocked && (bp.ia < 0 || bp.ib < 0)) {
@@ -1118,10 +1131,11 @@ void launch_fold_best(const LaunchCtx& c, const GroupParams& p, const double* ta
     const int64_t units = (p.g.groups / e) * ((e + 7) / 8) * ((p.s + kBlockThreads - 1) / kBlockThreads);
     if (units < 2 * static_cast<int64_t>(c.sm_count)) blocked = false;
   }
-  if (blocked)
+  if (blocked) {
     launch_fold_blocked<HAS_B>(c, p, bp, ta, tb, tout);
-  else
-    launch_fold<HAS_B>(c, p, ta, tb, tout);
+    return false;
+  }
+  return launch_fold<HAS_B>(c, p, ta, tb, tout, epi);
 }
 
 template <int VMAX, bool HAS_B, bool VEC>
@@ -1520,10 +1534,9 @@ bool launch_program_impl(const LaunchCtx& c, const Program& prog, const GroupSpe
   const size_t tile_bytes = static_cast<size_t>(s) * sizeof(double);
   // 1) No in-tile schedule: the fold is the whole program.
   if (prog.ops.size() == 1 && prog.ops[0].kind == GOP_FOLD && prog.ops[0].dst == BUF_OUT) {
-    LaunchCtx cl = c;  // an epilogue pass follows: the fold releases it at exit
+    LaunchCtx cl = c;  // an epilogue pass follows (unless the fold applies it): late release
     cl.release_late = epi != nullptr;
-    launch_fold_best<HAS_B>(cl, p, ta, tb, tout);
-    return false;
+    return launch_fold_best<HAS_B>(cl, p, ta, tb, tout, epi);
   }
   const BlockPlan bplan = block_plan(g, HAS_B);
   const bool matmul_like = HAS_B && bplan.ia >= 0 && bplan.ib >= 0;
