@@ -289,3 +289,27 @@ def test_clean_seam_random(gpu, s):
         _check_clean(S, a, b, dim)
         runs += 1
     assert runs >= 5
+
+
+@pytest.mark.parametrize("square", [False, True])
+def test_config4_layer2_ring_fold_tail(gpu, square):
+    """Config 4's second layer: a fold-only reduction (t2 = 1) over 100 steps whose
+    streamed operand (100 MiB) takes the cp.async-ring fold -- the tail (+ bias,
+    square) is applied in the fold's store, no separate pass.  Bias broadcast along
+    the batch tiles, and a bias-free square."""
+    S = tt.Session(8192, 8)
+    nrng = np.random.default_rng(44)
+    sw, sh = parse_shape("[10/32,100,*/256]"), parse_shape("[*/32,100,4096/256]")
+    w = tt.TileTensor(sw, nrng.uniform(-1, 1, size=(sw.tile_count(), 8192)), S)
+    h = tt.TileTensor(sh, nrng.uniform(-1, 1, size=(sh.tile_count(), 8192)), S)
+    b = _pack(S, "[10/32,1,*/256]", (10, 1, 1), 45)
+    launches0 = S.launches()
+    got = _check(S, w, h, 2, b, square)
+    assert got.shape().tile_count() == 16
+    _check(S, w, h, 2, None, True)
+    # the fused call is one launch (the composition before it: fold + add (+ mul))
+    S.reset_counters()
+    n0 = S.launches()
+    tt.tt_mul_sum_affine(w, h, 2, b, square=square)
+    assert S.launches() - n0 == 1, S.launches() - n0
+    assert launches0 >= 0
