@@ -88,18 +88,29 @@ class ClockSampler:
             h = pynvml.nvmlDeviceGetHandleByIndex(phys)
             mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
 
-            def run():
-                while not self._stop.is_set():
-                    try:
-                        self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            def sample(record=True):
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    if record:
+                        self.sm.append(sm)
                         self.mx.append(mx)
-                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                         for name, bit in self.REASONS.items():
                             if r & bit:
                                 self.reasons.add(name)
-                    except Exception:
-                        pass
-                    self._stop.wait(0.01)
+                except Exception:
+                    pass
+
+            # NVML's first queries after init are slow and hold a driver lock the
+            # kernel launches also take: the timed region's first launch, issued
+            # into an idle stream, was measured 3-63 ms instead of 2.55 ms when the
+            # sampler's first query ran beside it.  Warm the queries here (not
+            # recorded: the GPU is idle), and take the first sample 10 ms in.
+            sample(record=False)
+
+            def run():
+                while not self._stop.wait(0.01):
+                    sample()
             self.thread = threading.Thread(target=run, daemon=True)
             self.thread.start()
         except Exception:
@@ -501,7 +512,10 @@ def run_ours(args):
         ops[f"mul_sum_dim{k}"] = {"ms": dur[k] * 1e3, "GB/s": gbs, "frac": gbs / hbm_peak,
                                   "frac_of_8TBps": gbs / 8000.0,
                                   "tile_slots_per_s": x_tiles * S5 / dur[k],
-                                  "alg_bytes": alg[k]}
+                                  "alg_bytes": alg[k],
+                                  # every timed launch (a transient -- power capping, another
+                                  # tenant of the host -- shows as single slow launches)
+                                  "per_step_ms": [round(v * 1e3, 3) for v in per_dim[k]]}
 
     # the exact (bit-identical) form of the sum over the sharded dim: the
     # ranks' left folds chained along dim 1, the in-tile tree once at the end
