@@ -74,12 +74,17 @@ class ClockSampler:
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
+        """NVML is initialised and its queries warmed HERE -- construct the sampler
+        before the warm-up steps, so that nothing but the synchronize and the barrier
+        sits between the warm-up and the timed region (NVML's init and first queries
+        take tens of ms and hold a driver lock the kernel launches also take: run
+        beside the first timed launch they made it read 3-63 ms instead of 2.55 ms,
+        and run before it they leave the GPU idle long enough to drop its clocks)."""
         self.index = index
         self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self.thread = None
-
-    def __enter__(self):
+        self._sample = None
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -100,21 +105,18 @@ class ClockSampler:
                                 self.reasons.add(name)
                 except Exception:
                     pass
-
-            # NVML's first queries after init are slow and hold a driver lock the
-            # kernel launches also take: the timed region's first launch, issued
-            # into an idle stream, was measured 3-63 ms instead of 2.55 ms when the
-            # sampler's first query ran beside it.  Warm the queries here (not
-            # recorded: the GPU is idle), and take the first sample 10 ms in.
             sample(record=False)
+            self._sample = sample
+        except Exception:
+            self._sample = None
 
-            def run():
+    def __enter__(self):
+        if self._sample is not None:
+            def run():  # first sample 10 ms into the timed region
                 while not self._stop.wait(0.01):
-                    sample()
+                    self._sample()
             self.thread = threading.Thread(target=run, daemon=True)
             self.thread.start()
-        except Exception:
-            self.thread = None
         return self
 
     def __exit__(self, *exc):
@@ -453,6 +455,7 @@ def run_ours(args):
             outs.append(r)
         return outs, work
 
+    sampler = ClockSampler(local)  # NVML set up before the warm-up (see its docstring)
     for _ in range(args.warmup):
         _, w = step()
         if w is not None:
@@ -465,7 +468,7 @@ def run_ours(args):
     # region (no host synchronisation inside it)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     launches0 = S.launches()
-    with ClockSampler(local) as clk:
+    with sampler as clk:
         torch.cuda.synchronize(dev)
         if dist is not None:
             dist.barrier()
