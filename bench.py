@@ -456,10 +456,16 @@ def run_ours(args):
         return outs, work
 
     sampler = ClockSampler(local)  # NVML set up before the warm-up (see its docstring)
-    for _ in range(args.warmup):
-        _, w = step()
+    for _i in range(args.warmup):
+        warm_outs, w = step()
         if w is not None:
             w.wait()
+        # release the warm-up results: their blocks go back to the session's tile
+        # cache, so the timed steps allocate nothing (while the last warm-up step's
+        # results were still referenced, the first timed step had to cudaMalloc its
+        # 128 MiB - 1 GiB results: its first launch read ~3.0 ms instead of 2.55 ms,
+        # and 4.7 - 63 ms when the allocation met another driver call)
+        del warm_outs
     torch.cuda.synchronize(dev)
     if dist is not None:
         dist.barrier()
