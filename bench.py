@@ -534,6 +534,7 @@ def run_ours(args):
         def chain():
             return sharding.chain_mul_sum(X, W, 1, plan, fold, finish, n_out, new_acc)
         chain_res = chain()
+        chain_res = None  # back to the tile cache: the timed calls allocate nothing
         torch.cuda.synchronize(dev)
         if dist is not None:
             dist.barrier()
