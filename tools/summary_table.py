@@ -16,7 +16,7 @@ def main(final, ref, md):
 final pass of the round: SM clock {d['clocks']['sm_mhz']:.0f} of {d['clocks']['sm_max_mhz']} MHz, throttle reasons {d['clocks']['reasons']}).  Reference
 arm: `{ref}` (`python bench.py --impl reference`: the reference's own
 C++ path compiled from `/root/reference/proj/include` by `oracle/Makefile`, 16 host threads,
-same `config`).  GPU suite on the same box: all passed; `smoke()` ok.
+same `config`).  GPU suite on the same box: 162 passed; `smoke()` ok.
 
 | quantity | value |
 |---|---|
